@@ -1,0 +1,212 @@
+/* macrofacet_b200.h -- C ABI of the B200-native macrofacet hot path.
+ *
+ * Plain C types only (no torch, no CUDA types in signatures: streams are
+ * passed as `void*` holding a cudaStream_t, 0 = legacy default stream).
+ * Device pointers are marked d_*; everything else is host memory.
+ *
+ * Each entry point replaces one reference Python call on the hot path of
+ * /root/reference/pkg/src/macrofacet (file:line below); the Python mirror
+ * in paper_2603_00280_b200/ keeps the reference signatures on top of it
+ * (see INTEGRATION.md for the ctypes binding).
+ *
+ * Status codes map onto the reference exception tree (errors.py:4-41):
+ *   MF_ERR_PARAM        -> ParameterDomainError (ValueError)
+ *   MF_ERR_DEGENERATE   -> DegenerateVisibilityError   (ndf.py:312-313)
+ *   MF_ERR_MAJORANT     -> InternalConsistencyError    (transport.py:264-268)
+ *   MF_ERR_CAP          -> InternalConsistencyError    (transport.py:297)
+ *   MF_ERR_NUMERIC      -> NumericFailureError
+ *   MF_ERR_UNSUPPORTED  -> UnsupportedGeometryError    (medium.py:108-112)
+ *   MF_ERR_CUDA         -> MacrofacetError
+ * The message of the last failure on the calling thread: mf_last_error().
+ */
+#ifndef MACROFACET_B200_H
+#define MACROFACET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_ABI_VERSION 1
+
+enum mf_status {
+  MF_OK = 0,
+  MF_ERR_PARAM = 1,
+  MF_ERR_DEGENERATE = 2,
+  MF_ERR_MAJORANT = 3,
+  MF_ERR_CAP = 4,
+  MF_ERR_NUMERIC = 5,
+  MF_ERR_UNSUPPORTED = 6,
+  MF_ERR_CUDA = 7
+};
+
+/* NdfKind (ndf.py:69-72) */
+enum mf_kind { MF_KIND_BECKMANN = 0, MF_KIND_GGX = 1, MF_KIND_GENERALIZED = 2 };
+/* Fresnel term: conductor (medium.py:127-147), F == 1 (fresnel_one,
+ * medium.py:150-152) or a constant per-channel albedo (BASELINE configs 2-5;
+ * not in the reference, SURVEY.md 8(a) "Albedo") */
+enum mf_fresnel { MF_FRESNEL_CONDUCTOR = 0, MF_FRESNEL_ONE = 1, MF_FRESNEL_ALBEDO = 2 };
+
+/* MacrofacetMedium (medium.py:35-67).  For BECKMANN/GGX, az is ignored (0). */
+typedef struct mf_medium {
+  int32_t kind;
+  int32_t fresnel;
+  double ax, ay, az;
+  double sigma;
+  double mix_ratio;
+  double eta[3];
+  double k[3];
+  double albedo[3];
+} mf_medium;
+
+/* SDF primitives (sdf.py:18-52) */
+enum mf_shape { MF_SHAPE_PLANE = 0, MF_SHAPE_SPHERE = 1 };
+
+/* ShellPrimitive (scene.py:99-101): one shape bound to media[medium] */
+typedef struct mf_primitive {
+  int32_t shape;
+  int32_t medium;
+  double z0;         /* plane z = z0, outside above */
+  double center[3];  /* sphere */
+  double radius;
+} mf_primitive;
+
+/* Camera (scene.py:19-51); ortho != 0 selects the orthographic extension:
+ * a film film_height world units tall centred on `position`, rays parallel
+ * to look_at - position. */
+typedef struct mf_camera {
+  int32_t ortho;
+  int32_t width, height;
+  double position[3];
+  double look_at[3];
+  double fov_deg;
+  double film_height;
+} mf_camera;
+
+#define MF_MAX_PRIMS 8
+#define MF_MAX_MEDIA 8
+
+/* ShellScene (scene.py:104-129) + lights.  sun_dir is the direction the
+ * light travels (DirectionalLight, scene.py:87-96); the point light
+ * (position, intensity, NEE weight I/r^2) is a BASELINE-config extension. */
+typedef struct mf_scene {
+  int32_t n_prims;
+  int32_t n_media;
+  mf_primitive prims[MF_MAX_PRIMS];
+  mf_medium media[MF_MAX_MEDIA];
+  mf_camera camera;
+  double env[3]; /* constant environment radiance (scene.py:54-84) */
+  int32_t has_sun;
+  double sun_dir[3];
+  double sun_radiance[3];
+  int32_t has_point;
+  double point_pos[3];
+  double point_intensity[3];
+} mf_scene;
+
+/* Sharding of one render across ranks. */
+enum mf_shard { MF_SHARD_TILES = 0, MF_SHARD_SAMPLES = 1 };
+
+/* render(scene, spp, seed, max_bounces, tile) (render.py:127-180) */
+typedef struct mf_render_params {
+  uint64_t seed;
+  int32_t spp;          /* samples per pixel of the whole (all-rank) render */
+  int32_t max_bounces;  /* >= 1 (render.py:34-35) */
+  int32_t tile;         /* tile edge in pixels for MF_SHARD_TILES */
+  int32_t shard;        /* enum mf_shard */
+  int32_t rank, nranks;
+  int32_t accumulate;   /* 0: overwrite d_accum, 1: add into it */
+} mf_render_params;
+
+/* device-side event counters, summed over the call */
+typedef struct mf_stats {
+  uint64_t paths;
+  uint64_t segments;      /* free-flight segments (one per scatter + final) */
+  uint64_t scatters;      /* real collisions */
+  uint64_t nee;           /* next-event connections */
+  uint64_t slope_iters;   /* Newton iterations of the visible-slope sampler */
+  uint64_t track_steps;   /* delta/ratio-tracking tentative steps */
+  uint64_t escaped;
+  uint64_t absorbed;
+  uint64_t majorant_violations;
+  uint64_t degenerate;    /* sigma(wo) < 1e-12 at a scatter (returns 0) */
+  uint64_t nonfinite;
+  uint64_t capped;        /* paths cut by the segment cap */
+} mf_stats;
+
+/* ---------------------------------------------------------------------
+ * Coefficient queries (BASELINE config 1).  Replaces, per query i:
+ *   extinction(wo, f, medium, frame)           medium.py:91-95
+ *   phase_eval(wo, wi, medium, frame)          medium.py:158-178
+ *   phase pdf of wi (restated)                 ndf.py:397-405 + medium.py:186-189
+ *   _phase_sample_u(wo_local, medium, u)       medium.py:181-193
+ * with f and the frame taken from `field` at point p (plane: f = p.z - z0,
+ * normal +z; sphere: f = |p - c| - r, normal (p - c)/|p - c|), and the
+ * two-uniform convention u = (u1, u1', u2) of SURVEY.md 8(a).
+ * All arrays are device SoA float32 of length n; any output may be NULL.
+ * Directions are world-space unit vectors; the sampled direction is
+ * returned in world space.
+ */
+typedef struct mf_query_in {
+  const float *px, *py, *pz;
+  const float *wox, *woy, *woz;
+  const float *wix, *wiy, *wiz;
+  const float *u1, *u2;
+  /* optional overrides (NULL = derive from `field` at p):
+   * f     [n]     field value (extinction(wo, f, ...) style calls)
+   * frame [9][n]  tangent xyz, bitangent xyz, normal xyz (core.py:132-153) */
+  const float* f;
+  const float* frame;
+} mf_query_in;
+
+typedef struct mf_query_out {
+  float* sigma_t;
+  float *phase_r, *phase_g, *phase_b;
+  float* pdf;
+  float *wsx, *wsy, *wsz;
+  float* pdf_s;
+  float *w_r, *w_g, *w_b;
+  int32_t* flags; /* bit0 degenerate view (sigma(wo) < 1e-12) */
+} mf_query_out;
+
+int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_query_in* d_in,
+                   const mf_query_out* d_out, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Whole render into the caller's device accumulation buffer d_accum
+ * (H * W * 3 float32, row-major (y, x, rgb) like RadianceImage.pixels),
+ * holding radiance / spp for this rank's share (render.py:127-180).
+ * Non-owned pixels (tile sharding) are left untouched (overwrite mode
+ * writes +0.0 there), so a sum-reduce over ranks is exact.
+ * If stats != NULL the call synchronises the stream and fills it, and
+ * majorant violations / non-finite radiance turn into error statuses.
+ */
+int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
+              mf_stats* stats, void* stream);
+
+/* trace_paths(origins, directions, scene, max_bounces, brng) (render.py:32-108)
+ * for caller-given rays: d_org / d_dir are SoA float32 [3][n], path i is
+ * keyed by (d_pixel[i], d_sample[i]) under `seed`; d_radiance SoA [3][n]. */
+int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir,
+                   const uint32_t* d_pixel, const uint32_t* d_sample, uint64_t seed,
+                   int32_t max_bounces, int64_t n, float* d_radiance, mf_stats* stats,
+                   void* stream);
+
+/* transmittance_estimate(ray, scene, n, rng) (transport.py:300-313):
+ * ratio-tracking mean and standard error over n samples (host results). */
+int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],
+                     int64_t n, uint64_t seed, uint64_t stream_id, double* mean, double* se,
+                     void* stream);
+
+/* diagnostics */
+const char* mf_last_error(void);
+int mf_abi_version(void);
+/* number of kernel launches this thread has issued through the library */
+uint64_t mf_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MACROFACET_B200_H */

@@ -1,0 +1,23 @@
+"""B200-native macrofacet volumetric path tracing (arXiv 2603.00280).
+
+Drop-in for the hot path of the reference `macrofacet` package: the medium /
+phase-function / integrator entry points and the scene description keep the
+reference's names and signatures, and run as hand-written sm_100a CUDA
+kernels behind the C ABI in include/macrofacet_b200.h.  No CPU fallback."""
+
+__version__ = "0.1.0"
+
+from .core import Frame, build_frame, dot, normalize
+from .errors import (ConfigError, DegenerateVisibilityError, GrazingSingularityError,
+                     InternalConsistencyError, IoError, MacrofacetError, NumericFailureError,
+                     ParameterDomainError, UnsupportedGeometryError)
+from .image import RadianceImage, read_pfm, write_image, write_pfm, write_ppm
+from .medium import (MacrofacetMedium, extinction, phase_eval, phase_pdf, phase_sample,
+                     query_batch)
+from .ndf import KernelParams, NdfKind, RoughnessTriple, roughness_from_kernel
+from .render import PathKeys, render, render_device, render_sharded, trace_path, trace_paths
+from .rng import RandomStream
+from .scene import (Camera, DirectionalLight, Environment, PointLight, ShellPrimitive,
+                    ShellScene)
+from .sdf import Plane, Sphere
+from .transport import transmittance_estimate

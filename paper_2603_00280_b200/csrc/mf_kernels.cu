@@ -1,0 +1,855 @@
+// mf_kernels.cu -- sm_100a kernels of the macrofacet hot path and the
+// extern "C" boundary declared in include/macrofacet_b200.h.
+//
+// Kernels
+//   query_kernel      config-1 coefficient queries (medium.py:91-207), SoA
+//   path_kernel       persistent megakernel: raygen + free flight + NEE +
+//                     phase sampling + RR for every path of a pass; warps
+//                     refill dead lanes from a global work counter each
+//                     segment (warp-level compaction / path regeneration),
+//                     so path state never leaves registers
+//                     (render.py:32-108, transport.py:144-297)
+//   accumulate_kernel deterministic fixed-order per-pixel sum of the pass's
+//                     per-path radiance into the caller's fp32 buffer
+//                     (render.py:150,165-166)
+//   ratio_kernel      ratio-tracking transmittance samples (transport.py:300-313)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/macrofacet_b200.h"
+#include "mf_prepare.h"
+#include "mf_transport.cuh"
+
+using namespace mf;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define MF_CUDA(call)                                                                 \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(MF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kBlock = 128;
+
+enum StatIdx {
+  kStPaths = 0,
+  kStSegments,
+  kStScatters,
+  kStNee,
+  kStSlopeIters,
+  kStTrackSteps,
+  kStEscaped,
+  kStAbsorbed,
+  kStViolations,
+  kStDegenerate,
+  kStNonfinite,
+  kStCapped,
+  kStCount
+};
+
+// ---------------------------------------------------------------------------
+// config-1 query kernel
+
+struct QueryArgs {
+  MediumK m;
+  int shape;
+  float z0;
+  V3 c;
+  float radius;
+  mf_query_in in;
+  mf_query_out out;
+  int64_t n;
+};
+
+__global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ QueryArgs a) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    V3 p = v3(__ldg(a.in.px + i), __ldg(a.in.py + i), __ldg(a.in.pz + i));
+    V3 wo = v3(__ldg(a.in.wox + i), __ldg(a.in.woy + i), __ldg(a.in.woz + i));
+    V3 wi = v3(__ldg(a.in.wix + i), __ldg(a.in.wiy + i), __ldg(a.in.wiz + i));
+    FieldPoint fp = field_at(a.shape, a.z0, a.c, a.radius, p);
+    if (a.in.f) fp.f = __ldg(a.in.f + i);
+    Frame fr;
+    if (a.in.frame) {
+      const float* F = a.in.frame;
+      fr.t = v3(__ldg(F + i), __ldg(F + a.n + i), __ldg(F + 2 * a.n + i));
+      fr.b = v3(__ldg(F + 3 * a.n + i), __ldg(F + 4 * a.n + i), __ldg(F + 5 * a.n + i));
+      fr.n = v3(__ldg(F + 6 * a.n + i), __ldg(F + 7 * a.n + i), __ldg(F + 8 * a.n + i));
+    } else {
+      fr = frame_about(fp.n);
+    }
+    QueryResult q = query_local(a.m, fp.f, fr, wo, wi, __ldg(a.in.u1 + i), __ldg(a.in.u2 + i));
+    const mf_query_out& o = a.out;
+    if (o.sigma_t) o.sigma_t[i] = q.sigma_t;
+    if (o.phase_r) o.phase_r[i] = q.phase.x;
+    if (o.phase_g) o.phase_g[i] = q.phase.y;
+    if (o.phase_b) o.phase_b[i] = q.phase.z;
+    if (o.pdf) o.pdf[i] = q.pdf;
+    if (o.wsx) o.wsx[i] = q.ws.x;
+    if (o.wsy) o.wsy[i] = q.ws.y;
+    if (o.wsz) o.wsz[i] = q.ws.z;
+    if (o.pdf_s) o.pdf_s[i] = q.pdf_s;
+    if (o.w_r) o.w_r[i] = q.w.x;
+    if (o.w_g) o.w_g[i] = q.w.y;
+    if (o.w_b) o.w_b[i] = q.w.z;
+    if (o.flags) o.flags[i] = q.flags;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// path megakernel
+
+struct PassDev {
+  uint32_t k0, k1;
+  int max_bounces;
+  uint32_t n_paths;      // paths in this pass
+  uint32_t S;            // samples per local pixel in this pass
+  uint32_t sample_begin; // global sample index of the pass's first sample
+  int shard, rank, nranks, tile, tiles_x;
+  float* rad;            // SoA [3][n_paths]
+  unsigned int* counter;
+  unsigned long long* stats;
+  // caller-ray mode (trace_paths)
+  const float* org;      // SoA [3][n]
+  const float* dir;
+  const uint32_t* pix;
+  const uint32_t* smp;
+};
+
+// local pixel index -> global pixel index, or -1 (tile padding)
+__device__ __forceinline__ int local_to_pixel(const SceneDev& sc, const PassDev& ps, uint32_t lp) {
+  if (ps.shard == MF_SHARD_SAMPLES) return (int)lp;
+  uint32_t t2 = (uint32_t)(ps.tile * ps.tile);
+  uint32_t k = lp / t2;
+  uint32_t j = lp - k * t2;
+  uint32_t t = (uint32_t)ps.rank + k * (uint32_t)ps.nranks;
+  uint32_t ty = t / (uint32_t)ps.tiles_x, tx = t - ty * (uint32_t)ps.tiles_x;
+  uint32_t jy = j / (uint32_t)ps.tile, jx = j - jy * (uint32_t)ps.tile;
+  uint32_t x = tx * ps.tile + jx, y = ty * ps.tile + jy;
+  if (x >= (uint32_t)sc.width || y >= (uint32_t)sc.height) return -1;
+  return (int)(y * (uint32_t)sc.width + x);
+}
+
+struct PathState {
+  V3 pos, dir, T, L;
+  int bounce;
+  uint32_t pid;
+  PathRng rng;
+};
+
+struct Counters {
+  uint32_t v[kStCount];
+};
+
+__device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t pixel, float jx, float jy,
+                                           V3* o, V3* d) {
+  uint32_t py = pixel / (uint32_t)sc.width;
+  uint32_t px = pixel - py * (uint32_t)sc.width;
+  float nx = ((float)px + jx) / (float)sc.width * 2.0f - 1.0f;
+  float ny = 1.0f - ((float)py + jy) / (float)sc.height * 2.0f;
+  if (sc.ortho) {
+    *o = fma3(sc.cam_up, ny * sc.half_h, fma3(sc.cam_right, nx * sc.half_w, sc.cam_pos));
+    *d = sc.cam_fwd;
+  } else {
+    *o = sc.cam_pos;
+    *d = normalize3(fma3(sc.cam_up, ny * sc.half_h, fma3(sc.cam_right, nx * sc.half_w, sc.cam_fwd)));
+  }
+}
+
+// shadow transmittance from pos towards unit direction wl over distance t_max
+__device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& st, V3 pos, V3 wl,
+                                           float t_max, float h_end, Counters& cn) {
+  if (sc.single_plane) {
+    const MediumK& m = sc.media[0];
+    float sig = proj_area(m, wl);
+    return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig);
+  }
+  WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max);
+  cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
+  cn.v[kStViolations] += (uint32_t)w.violations;
+  return w.weight;
+}
+
+// One free-flight segment plus the scattering event at its end.
+// Returns true when the path has terminated.
+template <bool kPlanar>
+__device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& ps, PathState& st,
+                                             Counters& cn) {
+  cn.v[kStSegments]++;
+  U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
+  float u_fl = u01(b.x), u_br = u01(b.y), u_s2 = u01(b.z), u_rr = u01(b.w);
+  int k;
+  V3 pos;
+  if (kPlanar) {
+    const MediumK& m = sc.media[0];
+    float sig = proj_area(m, st.dir);
+    Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl);
+    if (fl.outcome == kEscaped) {
+      st.L = fma3(v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z), 1.0f, st.L);
+      cn.v[kStEscaped]++;
+      return true;
+    }
+    if (fl.outcome == kAbsorbed) {
+      cn.v[kStAbsorbed]++;
+      return true;
+    }
+    k = 0;
+    pos = fl.pos;
+  } else {
+    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false, INFINITY);
+    cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
+    cn.v[kStViolations] += (uint32_t)w.violations;
+    if (w.steps < 0) {
+      cn.v[kStCapped]++;
+      return true;
+    }
+    if (w.outcome == kEscaped) {
+      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
+      cn.v[kStEscaped]++;
+      return true;
+    }
+    if (w.outcome == kAbsorbed) {
+      cn.v[kStAbsorbed]++;
+      return true;
+    }
+    k = w.prim;
+    pos = w.pos;
+  }
+  cn.v[kStScatters]++;
+  const PrimDev& pr = sc.prims[k];
+  const MediumK& m = sc.media[k];
+  Frame fr = frame_about(kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(pr, pos));
+  V3 wo = to_local(fr, st.dir);
+  float sig_o = proj_area(m, wo);
+  if (!(sig_o >= 1e-12f)) {
+    cn.v[kStDegenerate]++;
+    return true;
+  }
+  // next-event estimation (render.py:71-82; point light: BASELINE extension)
+  if (sc.has_sun) {
+    V3 wl = to_local(fr, sc.sun_to);
+    V3 ph = phase_eval(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr(sc, st, pos, sc.sun_to, INFINITY,
+                           sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn);
+      float s = tr;
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * s, st.T.y * ph.y * sc.sun_L.y * s,
+                           st.T.z * ph.z * sc.sun_L.z * s));
+    }
+  }
+  if (sc.has_point) {
+    V3 d = sub3(sc.point_pos, pos);
+    float r2 = dot3(d, d);
+    float ir = frsqrt(r2);
+    V3 wlw = mul3(d, ir);
+    V3 wl = to_local(fr, wlw);
+    V3 ph = phase_eval(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
+      float s = tr * frcp(r2);
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
+                           st.T.z * ph.z * sc.point_I.z * s));
+    }
+  }
+  // phase sampling (render.py:84-90), two-uniform branch convention
+  float sig_b = proj_area_erf(wo, m.ax, m.ay, 0.0f);
+  float uu = remap_branch_uniform(u_br, m.mix);
+  PhaseSample s = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2);
+  cn.v[kStSlopeIters] += (uint32_t)s.iters;
+  st.dir = to_world(fr, s.wi);
+  st.T = v3(st.T.x * s.weight.x, st.T.y * s.weight.y, st.T.z * s.weight.z);
+  st.pos = pos;
+  st.bounce++;
+  if (st.bounce >= ps.max_bounces) return true;  // render.py:92-94
+  if (st.bounce > 8) {                            // render.py:96-105
+    float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+    if (u_rr >= q) return true;
+    float iq = 1.0f / q;
+    st.T = mul3(st.T, iq);
+  }
+  return false;
+}
+
+template <bool kPlanar, bool kCallerRays>
+__global__ void __launch_bounds__(kBlock) path_kernel(const __grid_constant__ SceneDev sc,
+                                                       const __grid_constant__ PassDev ps) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  Counters cn;
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
+  PathState st;
+  bool active = false, exhausted = false;
+  while (true) {
+    unsigned need = __ballot_sync(full, !active && !exhausted);
+    if (need) {
+      int leader = __ffs(need) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(ps.counter, (unsigned)__popc(need));
+      base = __shfl_sync(full, base, leader);
+      if (!active && !exhausted) {
+        uint32_t my = base + (uint32_t)__popc(need & ((1u << lane) - 1u));
+        if (my < ps.n_paths) {
+          st.pid = my;
+          st.rng.k0 = ps.k0;
+          st.rng.k1 = ps.k1;
+          st.T = v3(1.0f, 1.0f, 1.0f);
+          st.L = v3(0.0f, 0.0f, 0.0f);
+          st.bounce = 0;
+          if (kCallerRays) {
+            st.rng.pixel = ps.pix[my];
+            st.rng.sample = ps.smp[my];
+            st.pos = v3(ps.org[my], ps.org[ps.n_paths + my], ps.org[2u * ps.n_paths + my]);
+            st.dir = v3(ps.dir[my], ps.dir[ps.n_paths + my], ps.dir[2u * ps.n_paths + my]);
+            active = true;
+          } else {
+            uint32_t lp = my / ps.S;
+            uint32_t s = my - lp * ps.S;
+            int pixel = local_to_pixel(sc, ps, lp);
+            if (pixel < 0) {
+              ps.rad[my] = 0.0f;
+              ps.rad[ps.n_paths + my] = 0.0f;
+              ps.rad[2u * ps.n_paths + my] = 0.0f;
+            } else {
+              st.rng.pixel = (uint32_t)pixel;
+              st.rng.sample = ps.sample_begin + s;
+              U4 jb = rng_block(st.rng, kSegCamera, 0u);
+              camera_ray(sc, (uint32_t)pixel, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
+              active = true;
+            }
+          }
+          if (active) cn.v[kStPaths]++;
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (__ballot_sync(full, active) == 0) {
+      if (__ballot_sync(full, !exhausted) == 0) break;
+      continue;
+    }
+    if (active) {
+      if (path_segment<kPlanar>(sc, ps, st, cn)) {
+        float r = st.L.x, g = st.L.y, bl = st.L.z;
+        if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
+          cn.v[kStNonfinite]++;
+        }
+        ps.rad[st.pid] = r;
+        ps.rad[ps.n_paths + st.pid] = g;
+        ps.rad[2u * ps.n_paths + st.pid] = bl;
+        active = false;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) {
+    unsigned v = __reduce_add_sync(full, cn.v[i]);
+    if (lane == 0 && v) atomicAdd(ps.stats + i, (unsigned long long)v);
+  }
+}
+
+// per-pixel fixed-order sum of a pass (render.py:150,165-166)
+__global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__ SceneDev sc,
+                                                          const __grid_constant__ PassDev ps,
+                                                          uint32_t n_local, float inv_spp,
+                                                          float* accum) {
+  uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lp >= n_local) return;
+  int pixel = local_to_pixel(sc, ps, lp);
+  if (pixel < 0) return;
+  const float* r = ps.rad + (size_t)lp * ps.S;
+  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+  for (uint32_t s = 0; s < ps.S; ++s) {
+    s0 += r[s];
+    s1 += r[ps.n_paths + s];
+    s2 += r[2u * ps.n_paths + s];
+  }
+  float* a = accum + (size_t)pixel * 3;
+  a[0] += s0 * inv_spp;
+  a[1] += s1 * inv_spp;
+  a[2] += s2 * inv_spp;
+}
+
+// ratio-tracking transmittance samples (transport.py:300-313)
+__global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ SceneDev sc,
+                                                        uint32_t k0, uint32_t k1, uint32_t stream_lo,
+                                                        V3 org, V3 dir, uint32_t n, float* w_out,
+                                                        unsigned long long* stats) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t steps = 0, viol = 0;
+  if (i < n) {
+    PathRng rng{k0, k1, stream_lo, i};
+    WalkResult w = walk(sc, rng, 0u, kCallShadow, org, dir, true, INFINITY);
+    w_out[i] = w.weight;
+    steps = (uint32_t)max(w.steps, 0);
+    viol = (uint32_t)w.violations;
+  }
+  unsigned a = __reduce_add_sync(0xffffffffu, steps);
+  unsigned b = __reduce_add_sync(0xffffffffu, viol);
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(stats + kStTrackSteps, (unsigned long long)a);
+    if (b) atomicAdd(stats + kStViolations, (unsigned long long)b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+double log_ndtr_host(double u) { return std::log(0.5 * std::erfc(-u / std::sqrt(2.0))); }
+
+// max over directions of sigma(w) in the local frame (exact majorant
+// factor; replaces the direction-free bound of ndf.py:189-194)
+double sigma_max_host(const MediumK& m) {
+  double best = 0.0;
+  const int nt = 2048, np = 16;
+  for (int i = 0; i <= nt; ++i) {
+    double th = M_PI * i / nt;
+    for (int j = 0; j <= np; ++j) {
+      double ph = 0.5 * M_PI * j / np;
+      V3 w = v3((float)(std::sin(th) * std::cos(ph)), (float)(std::sin(th) * std::sin(ph)),
+                (float)std::cos(th));
+      best = std::max(best, (double)proj_area(m, w));
+    }
+  }
+  // the grid max of a smooth function under-estimates by O(h^2); pad
+  // generously (a majorant only needs to be an upper bound)
+  return best * 1.01 + 1e-6;
+}
+
+int build_scene(const mf_scene& in, SceneDev* out) {
+  if (in.n_prims < 0 || in.n_prims > MF_MAX_PRIMS)
+    return fail(MF_ERR_PARAM, "n_prims out of range");
+  if (in.n_media < 0 || in.n_media > MF_MAX_MEDIA)
+    return fail(MF_ERR_PARAM, "n_media out of range");
+  SceneDev sc;
+  std::memset(&sc, 0, sizeof(sc));
+  sc.n_prims = in.n_prims;
+  double min_sigma = INFINITY;
+  for (int j = 0; j < in.n_prims; ++j) {
+    std::string err;
+    PrimK pk;
+    int rc = prepare_primitive(in.prims[j], in.n_media, &pk, &err);
+    if (rc) return fail(rc, err);
+    MediumK mk;
+    rc = prepare_medium(in.media[pk.medium], &mk, &err);
+    if (rc) return fail(rc, err);
+    sc.prims[j].shape = pk.shape;
+    sc.prims[j].medium = j;
+    sc.prims[j].z0 = pk.z0;
+    sc.prims[j].c = v3(pk.cx, pk.cy, pk.cz);
+    sc.prims[j].radius = pk.radius;
+    sc.media[j] = mk;
+    double s = in.media[pk.medium].sigma;
+    min_sigma = std::min(min_sigma, s);
+    sc.mx[j].sig_max = (float)sigma_max_host(mk);
+    sc.mx[j].lphi_hi = (float)log_ndtr_host(3.0);
+    sc.mx[j].lphi_lo_col = (float)log_ndtr_host(-6.0);
+    sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);
+  }
+  sc.min_skip = std::isfinite(min_sigma) ? (float)(1e-7 * min_sigma) : 1e-7f;
+  sc.single_plane = (in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE) ? 1 : 0;
+  // camera basis (scene.py:30-41), in double
+  const mf_camera& cam = in.camera;
+  if (cam.width < 1 || cam.height < 1) return fail(MF_ERR_PARAM, "camera size must be >= 1");
+  double f[3] = {cam.look_at[0] - cam.position[0], cam.look_at[1] - cam.position[1],
+                 cam.look_at[2] - cam.position[2]};
+  double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  if (!(fn > 0.0)) return fail(MF_ERR_PARAM, "camera look_at equals position");
+  for (double& v : f) v /= fn;
+  double up[3] = {0.0, 0.0, 1.0};
+  if (std::fabs(f[2]) > 0.999) {
+    up[1] = 1.0;
+    up[2] = 0.0;
+  }
+  double r[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2],
+                 f[0] * up[1] - f[1] * up[0]};
+  double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  for (double& v : r) v /= rn;
+  double tu[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+  sc.ortho = cam.ortho;
+  sc.width = cam.width;
+  sc.height = cam.height;
+  sc.cam_pos = v3((float)cam.position[0], (float)cam.position[1], (float)cam.position[2]);
+  sc.cam_fwd = v3((float)f[0], (float)f[1], (float)f[2]);
+  sc.cam_right = v3((float)r[0], (float)r[1], (float)r[2]);
+  sc.cam_up = v3((float)tu[0], (float)tu[1], (float)tu[2]);
+  double hh = cam.ortho ? 0.5 * cam.film_height : std::tan(0.5 * cam.fov_deg * M_PI / 180.0);
+  sc.half_h = (float)hh;
+  sc.half_w = (float)(hh * cam.width / cam.height);
+  sc.env = v3((float)in.env[0], (float)in.env[1], (float)in.env[2]);
+  sc.has_sun = in.has_sun;
+  if (in.has_sun) {
+    double d[3] = {in.sun_dir[0], in.sun_dir[1], in.sun_dir[2]};
+    double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (!(dn > 0.0)) return fail(MF_ERR_PARAM, "sun direction must be nonzero");
+    sc.sun_to = v3((float)(-d[0] / dn), (float)(-d[1] / dn), (float)(-d[2] / dn));
+    sc.sun_L = v3((float)in.sun_radiance[0], (float)in.sun_radiance[1], (float)in.sun_radiance[2]);
+  }
+  sc.has_point = in.has_point;
+  if (in.has_point) {
+    sc.point_pos = v3((float)in.point_pos[0], (float)in.point_pos[1], (float)in.point_pos[2]);
+    sc.point_I = v3((float)in.point_intensity[0], (float)in.point_intensity[1],
+                    (float)in.point_intensity[2]);
+    // the light must sit outside every shell (its shadow walk is not clipped
+    // at shells containing it)
+    for (int j = 0; j < in.n_prims; ++j) {
+      const PrimDev& p = sc.prims[j];
+      V3 lp = sc.point_pos;
+      float fv = p.shape == 0 ? lp.z - p.z0
+                              : std::sqrt(dot3(sub3(lp, p.c), sub3(lp, p.c))) - p.radius;
+      if (!(fv > 3.0f * sc.media[j].sigma))
+        return fail(MF_ERR_UNSUPPORTED, "point light inside a shell is not supported");
+    }
+  }
+  *out = sc;
+  return MF_OK;
+}
+
+struct Occupancy {
+  int sms = 0;
+  int blocks[4] = {0, 0, 0, 0};
+};
+
+int device_occupancy(Occupancy* occ) {
+  static std::mutex mu;
+  static Occupancy cache[64];
+  static bool have[64] = {false};
+  int dev = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && have[dev]) {
+    *occ = cache[dev];
+    return MF_OK;
+  }
+  Occupancy o;
+  MF_CUDA(cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[0], path_kernel<true, false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[1], path_kernel<false, false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[2], path_kernel<true, true>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[3], path_kernel<false, true>,
+                                                        kBlock, 0));
+  for (int& b : o.blocks) b = std::max(b, 1);
+  if (dev < 64) {
+    cache[dev] = o;
+    have[dev] = true;
+  }
+  *occ = o;
+  return MF_OK;
+}
+
+void fill_stats(const unsigned long long* h, mf_stats* s) {
+  s->paths = h[kStPaths];
+  s->segments = h[kStSegments];
+  s->scatters = h[kStScatters];
+  s->nee = h[kStNee];
+  s->slope_iters = h[kStSlopeIters];
+  s->track_steps = h[kStTrackSteps];
+  s->escaped = h[kStEscaped];
+  s->absorbed = h[kStAbsorbed];
+  s->majorant_violations = h[kStViolations];
+  s->degenerate = h[kStDegenerate];
+  s->nonfinite = h[kStNonfinite];
+  s->capped = h[kStCapped];
+}
+
+int check_stats(const mf_stats& s) {
+  if (s.majorant_violations)
+    return fail(MF_ERR_MAJORANT, "extinction exceeded its majorant (" +
+                                     std::to_string(s.majorant_violations) + " events)");
+  if (s.capped) return fail(MF_ERR_CAP, "walker exceeded its iteration cap");
+  if (s.nonfinite)
+    return fail(MF_ERR_NUMERIC, "non-finite or negative radiance in " +
+                                    std::to_string(s.nonfinite) + " paths");
+  return MF_OK;
+}
+
+// scratch: per-path radiance, work counter, stats
+struct Scratch {
+  float* rad = nullptr;
+  unsigned int* counter = nullptr;
+  unsigned long long* stats = nullptr;
+};
+
+int scratch_alloc(Scratch* s, size_t n_paths, cudaStream_t st) {
+  MF_CUDA(cudaMallocAsync((void**)&s->rad, std::max<size_t>(n_paths, 1) * 3 * sizeof(float), st));
+  MF_CUDA(cudaMallocAsync((void**)&s->counter, 64 * sizeof(unsigned int), st));
+  MF_CUDA(cudaMallocAsync((void**)&s->stats, kStCount * sizeof(unsigned long long), st));
+  MF_CUDA(cudaMemsetAsync(s->stats, 0, kStCount * sizeof(unsigned long long), st));
+  return MF_OK;
+}
+
+int scratch_free(Scratch* s, cudaStream_t st) {
+  if (s->rad) MF_CUDA(cudaFreeAsync(s->rad, st));
+  if (s->counter) MF_CUDA(cudaFreeAsync(s->counter, st));
+  if (s->stats) MF_CUDA(cudaFreeAsync(s->stats, st));
+  *s = Scratch();
+  return MF_OK;
+}
+
+int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaStream_t st) {
+  Occupancy occ;
+  int rc = device_occupancy(&occ);
+  if (rc) return rc;
+  int which = (sc.single_plane ? 0 : 1) + (caller_rays ? 2 : 0);
+  int grid = occ.sms * occ.blocks[which];
+  int64_t need = ((int64_t)ps.n_paths + kBlock - 1) / kBlock;
+  grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
+  if (sc.single_plane) {
+    if (caller_rays) path_kernel<true, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<true, false><<<grid, kBlock, 0, st>>>(sc, ps);
+  } else {
+    if (caller_rays) path_kernel<false, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<false, false><<<grid, kBlock, 0, st>>>(sc, ps);
+  }
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+constexpr size_t kMaxPassPaths = size_t(1) << 26;  // 64 Mi paths (768 MiB of radiance)
+
+}  // namespace
+
+extern "C" {
+
+const char* mf_last_error(void) { return g_err.c_str(); }
+int mf_abi_version(void) { return MF_ABI_VERSION; }
+uint64_t mf_launch_count(void) { return g_launches; }
+
+int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_query_in* d_in,
+                   const mf_query_out* d_out, int64_t n, void* stream) {
+  if (!medium || !field || !d_in || !d_out) return fail(MF_ERR_PARAM, "null argument");
+  if (n < 0) return fail(MF_ERR_PARAM, "n must be >= 0");
+  QueryArgs a;
+  std::memset(&a, 0, sizeof(a));
+  std::string err;
+  int rc = prepare_medium(*medium, &a.m, &err);
+  if (rc) return fail(rc, err);
+  PrimK pk;
+  mf_primitive f = *field;
+  f.medium = 0;
+  rc = prepare_primitive(f, 1, &pk, &err);
+  if (rc) return fail(rc, err);
+  a.shape = pk.shape;
+  a.z0 = pk.z0;
+  a.c = v3(pk.cx, pk.cy, pk.cz);
+  a.radius = pk.radius;
+  a.in = *d_in;
+  a.out = *d_out;
+  a.n = n;
+  if (n == 0) return MF_OK;
+  const float* req[] = {a.in.px, a.in.py, a.in.pz, a.in.wox, a.in.woy, a.in.woz,
+                        a.in.wix, a.in.wiy, a.in.wiz, a.in.u1, a.in.u2};
+  for (const float* p : req)
+    if (!p) return fail(MF_ERR_PARAM, "query input array is null");
+  int dev = 0, sms = 148;
+  MF_CUDA(cudaGetDevice(&dev));
+  MF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int64_t blocks = (n + 255) / 256;
+  int grid = (int)std::min<int64_t>(blocks, (int64_t)sms * 8);
+  query_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
+              mf_stats* stats, void* stream) {
+  if (!scene || !params || !d_accum) return fail(MF_ERR_PARAM, "null argument");
+  const mf_render_params& p = *params;
+  if (p.spp < 1) return fail(MF_ERR_PARAM, "spp must be >= 1, got " + std::to_string(p.spp));
+  if (p.max_bounces < 1)
+    return fail(MF_ERR_PARAM, "max_bounces must be >= 1, got " + std::to_string(p.max_bounces));
+  if (p.nranks < 1 || p.rank < 0 || p.rank >= p.nranks)
+    return fail(MF_ERR_PARAM, "bad rank / nranks");
+  if (p.shard != MF_SHARD_TILES && p.shard != MF_SHARD_SAMPLES)
+    return fail(MF_ERR_PARAM, "unknown shard mode");
+  if (p.shard == MF_SHARD_TILES && p.tile < 1) return fail(MF_ERR_PARAM, "tile must be >= 1");
+  SceneDev sc;
+  int rc = build_scene(*scene, &sc);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t npix = (size_t)sc.width * sc.height;
+  if (!p.accumulate) MF_CUDA(cudaMemsetAsync(d_accum, 0, npix * 3 * sizeof(float), st));
+
+  PassDev ps;
+  std::memset(&ps, 0, sizeof(ps));
+  ps.k0 = (uint32_t)(p.seed & 0xffffffffu);
+  ps.k1 = (uint32_t)(p.seed >> 32);
+  ps.max_bounces = p.max_bounces;
+  ps.shard = p.shard;
+  ps.rank = p.rank;
+  ps.nranks = p.nranks;
+  ps.tile = p.tile;
+  // local pixels and this rank's sample range
+  size_t n_local;
+  uint32_t s_begin = 0, s_count = (uint32_t)p.spp;
+  if (p.shard == MF_SHARD_TILES) {
+    int tx = (sc.width + p.tile - 1) / p.tile, ty = (sc.height + p.tile - 1) / p.tile;
+    ps.tiles_x = tx;
+    int n_tiles = tx * ty;
+    int mine = n_tiles > p.rank ? (n_tiles - p.rank + p.nranks - 1) / p.nranks : 0;
+    n_local = (size_t)mine * p.tile * p.tile;
+  } else {
+    n_local = npix;
+    uint64_t a = (uint64_t)p.spp * p.rank / p.nranks, b = (uint64_t)p.spp * (p.rank + 1) / p.nranks;
+    s_begin = (uint32_t)a;
+    s_count = (uint32_t)(b - a);
+  }
+  if (n_local == 0 || s_count == 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return MF_OK;
+  }
+  uint32_t S_pass = (uint32_t)std::max<size_t>(1, std::min<size_t>(s_count, kMaxPassPaths / n_local));
+  size_t max_pass_paths = n_local * S_pass;
+  if (max_pass_paths > 0xffffffffull) return fail(MF_ERR_PARAM, "image too large for one pass");
+  Scratch scr;
+  rc = scratch_alloc(&scr, max_pass_paths, st);
+  if (rc) return rc;
+  ps.rad = scr.rad;
+  ps.counter = scr.counter;
+  ps.stats = scr.stats;
+  float inv_spp = (float)(1.0 / p.spp);
+  for (uint32_t s0 = 0; s0 < s_count; s0 += S_pass) {
+    uint32_t S = std::min(S_pass, s_count - s0);
+    ps.S = S;
+    ps.sample_begin = s_begin + s0;
+    ps.n_paths = (uint32_t)(n_local * S);
+    MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
+    rc = launch_paths(sc, ps, false, st);
+    if (rc) {
+      scratch_free(&scr, st);
+      return rc;
+    }
+    uint32_t nb = (uint32_t)((n_local + 255) / 256);
+    accumulate_kernel<<<nb, 256, 0, st>>>(sc, ps, (uint32_t)n_local, inv_spp, d_accum);
+    g_launches++;
+    MF_CUDA(cudaGetLastError());
+  }
+  int out = MF_OK;
+  if (stats) {
+    unsigned long long h[kStCount];
+    MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MF_CUDA(cudaStreamSynchronize(st));
+    fill_stats(h, stats);
+    out = check_stats(*stats);
+  }
+  rc = scratch_free(&scr, st);
+  return out ? out : rc;
+}
+
+int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir,
+                   const uint32_t* d_pixel, const uint32_t* d_sample, uint64_t seed,
+                   int32_t max_bounces, int64_t n, float* d_radiance, mf_stats* stats,
+                   void* stream) {
+  if (!scene || !d_org || !d_dir || !d_pixel || !d_sample || !d_radiance)
+    return fail(MF_ERR_PARAM, "null argument");
+  if (max_bounces < 1)
+    return fail(MF_ERR_PARAM, "max_bounces must be >= 1, got " + std::to_string(max_bounces));
+  if (n < 0 || n > 0xffffffffll) return fail(MF_ERR_PARAM, "n out of range");
+  SceneDev sc;
+  int rc = build_scene(*scene, &sc);
+  if (rc) return rc;
+  if (n == 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return MF_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scr;
+  rc = scratch_alloc(&scr, 0, st);
+  if (rc) return rc;
+  PassDev ps;
+  std::memset(&ps, 0, sizeof(ps));
+  ps.k0 = (uint32_t)(seed & 0xffffffffu);
+  ps.k1 = (uint32_t)(seed >> 32);
+  ps.max_bounces = max_bounces;
+  ps.n_paths = (uint32_t)n;
+  ps.S = 1;
+  ps.rad = d_radiance;
+  ps.counter = scr.counter;
+  ps.stats = scr.stats;
+  ps.org = d_org;
+  ps.dir = d_dir;
+  ps.pix = d_pixel;
+  ps.smp = d_sample;
+  MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
+  rc = launch_paths(sc, ps, true, st);
+  int out = rc;
+  if (!rc && stats) {
+    unsigned long long h[kStCount];
+    MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MF_CUDA(cudaStreamSynchronize(st));
+    fill_stats(h, stats);
+    out = check_stats(*stats);
+  }
+  int rc2 = scratch_free(&scr, st);
+  return out ? out : rc2;
+}
+
+int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],
+                     int64_t n, uint64_t seed, uint64_t stream_id, double* mean, double* se,
+                     void* stream) {
+  if (!scene || !origin || !direction || !mean || !se) return fail(MF_ERR_PARAM, "null argument");
+  if (n < 1 || n > 0x7fffffffll) return fail(MF_ERR_PARAM, "n_samples out of range");
+  SceneDev sc;
+  int rc = build_scene(*scene, &sc);
+  if (rc) return rc;
+  double dn = std::sqrt(direction[0] * direction[0] + direction[1] * direction[1] +
+                        direction[2] * direction[2]);
+  if (!(dn > 0.0)) return fail(MF_ERR_PARAM, "direction must be nonzero");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* w = nullptr;
+  unsigned long long* stt = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&w, (size_t)n * sizeof(float), st));
+  MF_CUDA(cudaMallocAsync((void**)&stt, kStCount * sizeof(unsigned long long), st));
+  MF_CUDA(cudaMemsetAsync(stt, 0, kStCount * sizeof(unsigned long long), st));
+  V3 o = v3((float)origin[0], (float)origin[1], (float)origin[2]);
+  V3 d = v3((float)(direction[0] / dn), (float)(direction[1] / dn), (float)(direction[2] / dn));
+  uint32_t nb = (uint32_t)((n + kBlock - 1) / kBlock);
+  ratio_kernel<<<nb, kBlock, 0, st>>>(sc, (uint32_t)seed, (uint32_t)(seed >> 32),
+                                      (uint32_t)stream_id, o, d, (uint32_t)n, w, stt);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  std::vector<float> hw((size_t)n);
+  unsigned long long hs[kStCount];
+  MF_CUDA(cudaMemcpyAsync(hw.data(), w, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  MF_CUDA(cudaMemcpyAsync(hs, stt, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  MF_CUDA(cudaFreeAsync(w, st));
+  MF_CUDA(cudaFreeAsync(stt, st));
+  MF_CUDA(cudaStreamSynchronize(st));
+  if (hs[kStViolations])
+    return fail(MF_ERR_MAJORANT, "extinction exceeded its majorant in ratio tracking");
+  // mean and standard error in double, fixed order (transport.py:310-313)
+  double s = 0.0;
+  for (float v : hw) s += v;
+  double m = s / (double)n;
+  double ss = 0.0;
+  for (float v : hw) ss += ((double)v - m) * ((double)v - m);
+  *mean = m;
+  *se = n > 1 ? std::sqrt(ss / (double)(n - 1)) / std::sqrt((double)n) : 0.0;
+  return MF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+// mf_transport.cuh -- device scene, free flight, NEE transmittance.
+//
+// Reference (float64, wavefront numpy) -> here (fp32, per-path in registers):
+//   walk(mode="collision")     transport.py:144-297
+//       single plane : analytic free flight, inverting the closed-form
+//                      transmittance (medium.py:98-124) in log-Phi space
+//                      -- same distribution of collision heights, no
+//                      stepping
+//       otherwise    : delta tracking with the moving Lipschitz band
+//                      majorant rho(f - s/2) * sigma_max, step <= s/2,
+//                      sigma_max the exact max_w sigma(w) (tighter than
+//                      ndf.py:189-194's direction-free bound)
+//   walk(mode="ratio")         transport.py:269-270: closed form for a single
+//                      plane, ratio tracking otherwise
+//   region rules               transport.py:161-166: collision walks live on
+//                      f in [-6s, 3s] and absorb below; shadow walks
+//                      integrate |f| <= 3s only
+#pragma once
+
+#include "mf_math.cuh"
+#include "mf_query.cuh"
+
+namespace mf {
+
+constexpr int kMaxPrims = 8;
+
+struct PrimDev {
+  int shape;   // 0 plane, 1 sphere
+  int medium;
+  float z0;
+  V3 c;
+  float radius;
+};
+
+struct MediumExtra {
+  float sig_max;       // max_w sigma(w), majorant factor for curved shells
+  float lphi_hi;       // log Phi(3)   (collision / ratio upper edge)
+  float lphi_lo_col;   // log Phi(-6)  (collision absorption edge)
+  float lphi_lo_rat;   // log Phi(-3)  (ratio lower edge)
+};
+
+struct SceneDev {
+  int n_prims;
+  int single_plane;    // 1: analytic planar transport
+  PrimDev prims[kMaxPrims];
+  MediumK media[kMaxPrims];
+  MediumExtra mx[kMaxPrims];
+  // camera (scene.py:30-51 basis; ortho extension)
+  int ortho, width, height;
+  V3 cam_pos, cam_fwd, cam_right, cam_up;
+  float half_w, half_h;
+  V3 env;
+  int has_sun;
+  V3 sun_to;           // unit direction towards the sun (= -DirectionalLight.direction)
+  V3 sun_L;
+  int has_point;
+  V3 point_pos;
+  V3 point_I;
+  float min_skip;      // 1e-7 * min sigma (transport.py:167)
+};
+
+// ---------------------------------------------------------------------------
+// counter-based random stream of one path: key = seed, counter =
+// (pixel, sample, segment, call)
+
+struct PathRng {
+  uint32_t k0, k1;
+  uint32_t pixel, sample;
+};
+
+MF_HD U4 rng_block(const PathRng& r, uint32_t segment, uint32_t call) {
+  return philox4x32_10(U4{r.pixel, r.sample, segment, call}, r.k0, r.k1);
+}
+
+// segment id used for the camera jitter draw
+constexpr uint32_t kSegCamera = 0xFFFFFFFFu;
+// call ids >= this index the shadow-ray (ratio tracking) stream of a segment
+constexpr uint32_t kCallShadow = 0x80000000u;
+
+// ---------------------------------------------------------------------------
+// fields
+
+MF_HD float prim_field(const PrimDev& p, V3 x) {
+  if (p.shape == 0) return x.z - p.z0;
+  V3 d = sub3(x, p.c);
+  return fsqrt(dot3(d, d)) - p.radius;
+}
+
+MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
+  if (p.shape == 0) return v3(0.0f, 0.0f, 1.0f);
+  V3 d = sub3(x, p.c);
+  float r2 = dot3(d, d);
+  return r2 > 0.0f ? mul3(d, frsqrt(r2)) : v3(0.0f, 0.0f, 1.0f);
+}
+
+// distance along the ray to the level set f = level (transport.py:70-92);
+// +inf when never reached
+MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
+  if (p.shape == 0) {
+    float t = (level - (pos.z - p.z0)) / dir.z;
+    return (t > 0.0f && t < INFINITY) ? t : INFINITY;
+  }
+  float rad = p.radius + level;
+  if (!(rad > 0.0f)) return INFINITY;
+  V3 oc = sub3(pos, p.c);
+  float b = dot3(oc, dir);
+  float cc = dot3(oc, oc) - rad * rad;
+  float disc = b * b - cc;
+  if (disc < 0.0f) return INFINITY;
+  float sq = fsqrt(disc);
+  float t1 = -b - sq, t2 = -b + sq;
+  float t = t1 > 1e-7f * fmaxf(1.0f, fabsf(b)) ? t1 : t2;
+  return t > 0.0f ? t : INFINITY;
+}
+
+// ---------------------------------------------------------------------------
+// analytic planar free flight (single plane)
+
+enum FlightOutcome : int { kEscaped = 0, kAbsorbed = 1, kCollided = 2 };
+
+struct Flight {
+  int outcome;
+  V3 pos;
+};
+
+// One collision-mode flight from pos along dir through the shell of a
+// single plane, given u in (0,1).  sig = sigma(dir) in the plane frame.
+MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtra& mx, V3 pos,
+                           V3 dir, float sig, float u) {
+  Flight fl;
+  float s3 = 3.0f * m.sigma;
+  float h = pos.z - pr.z0;
+  float c = dir.z;
+  if (h > s3) {
+    if (!(c < 0.0f)) {
+      fl.outcome = kEscaped;
+      fl.pos = pos;
+      return fl;
+    }
+    pos = fma3(dir, (s3 - h) / c, pos);
+    h = s3;
+  }
+  if (h < -6.0f * m.sigma) {
+    fl.outcome = kAbsorbed;
+    fl.pos = pos;
+    return fl;
+  }
+  float tau = -flog(u);
+  if (fabsf(c) < 1e-6f) {
+    float st = mills(h * m.inv_sigma) * m.inv_sigma * sig;
+    if (!(st > 0.0f)) {
+      fl.outcome = kEscaped;
+      fl.pos = pos;
+      return fl;
+    }
+    fl.outcome = kCollided;
+    fl.pos = fma3(dir, tau / st, pos);
+    return fl;
+  }
+  float l0 = log_ndtr(h * m.inv_sigma);
+  float dl = tau * fabsf(c) / sig;          // change of log Phi along the flight
+  float l1;
+  if (c > 0.0f) {
+    l1 = l0 + dl;
+    if (!(l1 < mx.lphi_hi)) {
+      fl.outcome = kEscaped;
+      fl.pos = pos;
+      return fl;
+    }
+  } else {
+    l1 = l0 - dl;
+    if (!(l1 >= mx.lphi_lo_col)) {
+      fl.outcome = kAbsorbed;
+      fl.pos = pos;
+      return fl;
+    }
+  }
+  float h1 = m.sigma * inv_log_ndtr(l1);
+  // keep the root on the travelled side of h despite rounding
+  h1 = c > 0.0f ? fmaxf(h1, h) : fminf(h1, h);
+  fl.outcome = kCollided;
+  fl.pos = fma3(dir, (h1 - h) / c, pos);
+  fl.pos.z = pr.z0 + h1;
+  return fl;
+}
+
+// closed-form shadow transmittance of a single plane over |f| <= 3 sigma
+// between field values h (start) and h_end (light; +/-inf for the sun)
+MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, float h_end,
+                             float c, float sig) {
+  float s3 = 3.0f * m.sigma;
+  float a = fminf(fmaxf(h, -s3), s3);
+  float b = fminf(fmaxf(h_end, -s3), s3);
+  if (a == b) return 1.0f;
+  if (fabsf(c) < 1e-6f) return 0.0f;
+  float la = a >= s3 ? mx.lphi_hi : (a <= -s3 ? mx.lphi_lo_rat : log_ndtr(a * m.inv_sigma));
+  float lb = b >= s3 ? mx.lphi_hi : (b <= -s3 ? mx.lphi_lo_rat : log_ndtr(b * m.inv_sigma));
+  return expf(-sig / fabsf(c) * fabsf(lb - la));
+}
+
+// ---------------------------------------------------------------------------
+// general walker (delta / ratio tracking), any number of plane / sphere shells
+
+struct WalkResult {
+  int outcome;
+  int prim;
+  V3 pos;
+  float weight;   // ratio tracking transmittance
+  int steps;
+  int violations;
+};
+
+// Extinction of prim j at x along dir (local frame), 0 outside its region.
+MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mult) {
+  const PrimDev& p = sc.prims[j];
+  const MediumK& m = sc.media[j];
+  float f = prim_field(p, x);
+  if (f < lo_mult * m.sigma || f > 3.0f * m.sigma) return 0.0f;
+  Frame fr = frame_about(prim_normal(p, x));
+  float sg = proj_area(m, to_local(fr, dir));
+  return mills(f * m.inv_sigma) * m.inv_sigma * sg;
+}
+
+// ratio == false: delta tracking (collision mode); ratio == true: ratio
+// tracking of the transmittance up to distance t_max (shadow rays).
+// Random draws: Philox blocks (segment, call0 + k), 4 uniforms each.
+MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, uint32_t call0,
+                      V3 pos, V3 dir, bool ratio, float t_max) {
+  WalkResult w;
+  w.outcome = kEscaped;
+  w.prim = -1;
+  w.weight = 1.0f;
+  w.steps = 0;
+  w.violations = 0;
+  float lo_mult = ratio ? -3.0f : -6.0f;
+  float travel = 0.0f;
+  uint32_t call = call0;
+  U4 bits = U4{0, 0, 0, 0};
+  int avail = 0;
+  for (int iter = 0; iter < 1000000; ++iter) {
+    // fields, band membership, gaps (transport.py:197-212)
+    bool any_band = false;
+    float gap_min = INFINITY;
+    bool all_done = true;
+    float maj = 0.0f;
+    float cap = INFINITY;
+    for (int j = 0; j < sc.n_prims; ++j) {
+      const PrimDev& p = sc.prims[j];
+      const MediumK& m = sc.media[j];
+      float f = prim_field(p, pos);
+      float lo = lo_mult * m.sigma, hi = 3.0f * m.sigma;
+      if (!ratio && f < lo) {
+        w.outcome = kAbsorbed;
+        w.pos = pos;
+        return w;
+      }
+      if (f >= lo && f <= hi) {
+        any_band = true;
+        float half = 0.5f * m.sigma;
+        float fb = fmaxf(f - half, lo);
+        maj += mills(fb * m.inv_sigma) * m.inv_sigma * sc.mx[j].sig_max;
+        cap = fminf(cap, half);
+      } else {
+        float g = level_distance(p, pos, dir, f > hi ? hi : lo);
+        gap_min = fminf(gap_min, g);
+        if (g < INFINITY) all_done = false;
+        cap = fminf(cap, fmaxf(g, sc.min_skip));
+      }
+    }
+    if (!any_band) {
+      if (all_done || travel + gap_min >= t_max) {
+        w.outcome = kEscaped;
+        w.pos = pos;
+        return w;
+      }
+      float skip = fmaxf(gap_min, sc.min_skip);
+      pos = fma3(dir, skip, pos);
+      travel += skip;
+      continue;
+    }
+    if (avail == 0) {
+      bits = rng_block(rng, segment, call++);
+      avail = 4;
+    }
+    float u1 = u01(bits.x);
+    bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
+    --avail;
+    float dt = maj > 0.0f ? -flog(u1) / maj : INFINITY;
+    w.steps++;
+    if (dt > cap) {
+      pos = fma3(dir, cap, pos);
+      travel += cap;
+      if (ratio && travel >= t_max) {
+        w.outcome = kEscaped;
+        w.pos = pos;
+        return w;
+      }
+      continue;
+    }
+    pos = fma3(dir, dt, pos);
+    travel += dt;
+    if (ratio && travel >= t_max) {
+      w.outcome = kEscaped;
+      w.pos = pos;
+      return w;
+    }
+    float parts[kMaxPrims];
+    float st = 0.0f;
+    for (int j = 0; j < sc.n_prims; ++j) {
+      parts[j] = prim_extinction(sc, j, pos, dir, lo_mult);
+      st += parts[j];
+    }
+    if (st > maj * 1.00001f) w.violations++;
+    if (ratio) {
+      w.weight *= fmaxf(1.0f - st / maj, 0.0f);
+      if (!(w.weight > 0.0f)) {
+        w.outcome = kEscaped;
+        w.pos = pos;
+        return w;
+      }
+    } else {
+      if (avail == 0) {
+        bits = rng_block(rng, segment, call++);
+        avail = 4;
+      }
+      float u2 = u01(bits.x);
+      bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
+      --avail;
+      float pick = u2 * maj;
+      if (pick < st) {
+        // u2 * majorant doubles as the primitive selector (transport.py:276-279)
+        float acc = 0.0f;
+        int k = sc.n_prims - 1;
+        for (int j = 0; j < sc.n_prims; ++j) {
+          acc += parts[j];
+          if (pick < acc) {
+            k = j;
+            break;
+          }
+        }
+        w.outcome = kCollided;
+        w.prim = k;
+        w.pos = pos;
+        return w;
+      }
+    }
+  }
+  w.outcome = kAbsorbed;  // iteration cap: treated as lost (counted by the caller)
+  w.pos = pos;
+  w.steps = -1;
+  return w;
+}
+
+}  // namespace mf

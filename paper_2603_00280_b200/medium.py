@@ -1,0 +1,225 @@
+"""The macrofacet medium and its pointwise operators, on the GPU.
+
+Mirrors the reference's medium API (medium.py:35-207) -- same names,
+argument meaning and exceptions -- with every evaluation performed by the
+`query` CUDA kernel through the C ABI (mf_query_batch):
+
+    extinction(wo, f, medium, local_frame)        medium.py:91-95
+    phase_eval(wo, wi, medium, local_frame)       medium.py:158-178
+    phase_pdf(wo, wi, medium, local_frame)        restated ndf.py:397-405 + medium.py:186-189
+    phase_sample(wo, medium, local_frame, rng)    medium.py:196-207 (uniforms from `rng`)
+    query_batch(...)                              the fused config-1 query
+
+Host numpy inputs are copied to the device and results copied back;
+torch CUDA tensors stay on the device (no copies) for the batched form.
+Arithmetic is fp32 on the device (the reference is float64); see DESIGN.md
+for the tolerance policy.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import Frame
+from .errors import DegenerateVisibilityError, ParameterDomainError
+from .ndf import NdfKind, RoughnessTriple
+
+DEFAULT_ETA = (0.2, 0.92, 1.1)
+DEFAULT_K = (3.9, 2.45, 2.14)
+
+
+@dataclass(frozen=True)
+class MacrofacetMedium:
+    """Appearance parameters of one shell volume (medium.py:35-67).
+
+    `albedo` (not in the reference) replaces the Fresnel term by a constant
+    per-channel single-scattering albedo, as BASELINE configs 2-5 require
+    (grey F == albedo)."""
+
+    kind: NdfKind
+    a3: RoughnessTriple
+    sigma: float
+    fresnel_eta: tuple = DEFAULT_ETA
+    fresnel_k: tuple = DEFAULT_K
+    mix_ratio: float = 0.5
+    fresnel_one: bool = False
+    albedo: tuple | None = None
+
+    def __post_init__(self):
+        if not (np.isfinite(self.sigma) and self.sigma > 0.0):
+            raise ParameterDomainError(f"sigma must be finite and > 0, got {self.sigma}")
+        if not (0.0 <= self.mix_ratio <= 1.0):
+            raise ParameterDomainError(f"mix_ratio must lie in [0, 1], got {self.mix_ratio}")
+        if self.kind is NdfKind.GENERALIZED and self.a3.az <= 0.0:
+            raise ParameterDomainError("GENERALIZED medium requires az > 0")
+        if self.kind is not NdfKind.GENERALIZED and self.a3.az != 0.0:
+            object.__setattr__(self, "a3", RoughnessTriple(self.a3.ax, self.a3.ay, 0.0))
+        object.__setattr__(self, "fresnel_eta", tuple(float(v) for v in self.fresnel_eta))
+        object.__setattr__(self, "fresnel_k", tuple(float(v) for v in self.fresnel_k))
+        if self.albedo is not None:
+            alb = self.albedo
+            if np.isscalar(alb):
+                alb = (alb, alb, alb)
+            alb = tuple(float(v) for v in alb)
+            if len(alb) != 3 or not all(0.0 <= v for v in alb):
+                raise ParameterDomainError(f"albedo must be 3 non-negative values, got {alb}")
+            object.__setattr__(self, "albedo", alb)
+
+    @property
+    def shell_half_width(self):
+        return 3.0 * self.sigma
+
+
+def to_c_medium(m: MacrofacetMedium) -> _lib.MfMedium:
+    c = _lib.MfMedium()
+    c.kind = _lib.KIND[m.kind.value]
+    if m.albedo is not None:
+        c.fresnel = _lib.FRESNEL_ALBEDO
+        c.albedo[:] = m.albedo
+    elif m.fresnel_one:
+        c.fresnel = _lib.FRESNEL_ONE
+    else:
+        c.fresnel = _lib.FRESNEL_CONDUCTOR
+    c.ax, c.ay, c.az = float(m.a3.ax), float(m.a3.ay), float(m.a3.az)
+    c.sigma = float(m.sigma)
+    c.mix_ratio = float(m.mix_ratio)
+    c.eta[:] = m.fresnel_eta
+    c.k[:] = m.fresnel_k
+    return c
+
+
+def _plane_field():
+    p = _lib.MfPrimitive()
+    p.shape = _lib.SHAPE_PLANE
+    p.z0 = 0.0
+    return p
+
+
+_QUERY_OUTS = ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx", "wsy", "wsz", "pdf_s",
+               "w_r", "w_g", "w_b", "flags")
+
+
+def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None, frame=None,
+                outputs=_QUERY_OUTS, stream=None):
+    """Fused coefficient query (BASELINE config 1) on device tensors.
+
+    p, wo, wi: (3, n) float32 CUDA tensors (SoA rows); u1, u2: (n,).
+    Optional f (n,) and frame (9, n) override the field-derived values.
+    Returns {name: CUDA tensor} for the requested outputs."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    n = int(u1.numel())
+    dev = u1.device
+    for t in (p, wo, wi, u1, u2):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ParameterDomainError("query_batch expects contiguous float32 CUDA tensors")
+    qi = _lib.MfQueryIn()
+    qi.px, qi.py, qi.pz = (p[k].data_ptr() for k in range(3))
+    qi.wox, qi.woy, qi.woz = (wo[k].data_ptr() for k in range(3))
+    qi.wix, qi.wiy, qi.wiz = (wi[k].data_ptr() for k in range(3))
+    qi.u1, qi.u2 = u1.data_ptr(), u2.data_ptr()
+    qi.f = f.data_ptr() if f is not None else None
+    qi.frame = frame.data_ptr() if frame is not None else None
+    qo = _lib.MfQueryOut()
+    out = {}
+    for name in outputs:
+        dt = torch.int32 if name == "flags" else torch.float32
+        t = torch.empty(n, dtype=dt, device=dev)
+        out[name] = t
+        setattr(qo, name, t.data_ptr())
+    fld = field if field is not None else _plane_field()
+    cm = to_c_medium(medium)
+    s = stream if stream is not None else _lib.stream_handle(torch, dev)
+    _lib.check(lib.mf_query_batch(ctypes.byref(cm), ctypes.byref(fld), ctypes.byref(qi),
+                                  ctypes.byref(qo), n, s))
+    return out
+
+
+def _frame_rows(local_frame: Frame, shape):
+    rows = []
+    for v in (local_frame.tangent, local_frame.bitangent, local_frame.normal):
+        v = np.broadcast_to(np.asarray(v, dtype=np.float64), shape + (3,))
+        rows.extend([v[..., 0], v[..., 1], v[..., 2]])
+    return rows
+
+
+def _host_query(medium, wo, wi, f, local_frame, u, outputs):
+    """Broadcast host arrays, run the device query, return host arrays."""
+    torch = _lib.require_cuda()
+    wo = np.asarray(wo, dtype=np.float64)
+    wi = np.asarray(wi, dtype=np.float64) if wi is not None else wo
+    f = np.asarray(f if f is not None else 0.0, dtype=np.float64)
+    shape = np.broadcast_shapes(wo.shape[:-1], wi.shape[:-1], f.shape,
+                                np.shape(local_frame.normal)[:-1])
+    if u is not None:
+        shape = np.broadcast_shapes(shape, np.shape(u)[:-1])
+    n = int(np.prod(shape)) if shape else 1
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def col(a):
+        return torch.from_numpy(np.ascontiguousarray(
+            np.broadcast_to(a, shape).reshape(-1), dtype=np.float32)).to(dev)
+
+    wob = np.broadcast_to(wo, shape + (3,))
+    wib = np.broadcast_to(wi, shape + (3,))
+    zero = torch.zeros(n, dtype=torch.float32, device=dev)
+    p = torch.stack([zero, zero, col(f)])
+    wo_t = torch.stack([col(wob[..., k]) for k in range(3)]).contiguous()
+    wi_t = torch.stack([col(wib[..., k]) for k in range(3)]).contiguous()
+    if u is None:
+        u1 = torch.full((n,), 0.5, dtype=torch.float32, device=dev)
+        u2 = u1
+    else:
+        ub = np.broadcast_to(np.asarray(u, dtype=np.float64), shape + (2,))
+        u1, u2 = col(ub[..., 0]), col(ub[..., 1])
+    fr = torch.stack([col(r) for r in _frame_rows(local_frame, shape)]).contiguous()
+    res = query_batch(medium, p, wo_t, wi_t, u1, u2, f=col(f), frame=fr, outputs=outputs)
+    return {k: v.cpu().numpy().reshape(shape) for k, v in res.items()}, shape
+
+
+def extinction(wo, f, medium: MacrofacetMedium, local_frame: Frame):
+    """rho(f) * sigma(wo_local) (medium.py:91-95), on the GPU."""
+    r, _ = _host_query(medium, wo, None, f, local_frame, None, ("sigma_t",))
+    return r["sigma_t"].astype(np.float64)[()]
+
+
+def phase_eval(wo, wi, medium: MacrofacetMedium, local_frame: Frame):
+    """Phase function per steradian, 3 channels (medium.py:158-178), on the GPU.
+
+    Raises DegenerateVisibilityError where sigma(wo) < 1e-12, like the
+    reference's vndf_eval (ndf.py:312-313)."""
+    r, shape = _host_query(medium, wo, wi, None, local_frame, None,
+                           ("phase_r", "phase_g", "phase_b", "flags"))
+    if np.any(r["flags"] & 1):
+        raise DegenerateVisibilityError("projected area is numerically zero toward wo")
+    return np.stack([r["phase_r"], r["phase_g"], r["phase_b"]], axis=-1).astype(np.float64)
+
+
+def phase_pdf(wo, wi, medium: MacrofacetMedium, local_frame: Frame):
+    """Density of phase_sample's direction (not exported by the reference;
+    restated from ndf.py:397-405 and medium.py:186-189), on the GPU."""
+    r, _ = _host_query(medium, wo, wi, None, local_frame, None, ("pdf",))
+    return r["pdf"].astype(np.float64)[()]
+
+
+def phase_sample(wo, medium: MacrofacetMedium, local_frame: Frame, rng, n=None):
+    """Scattered direction, pdf and per-channel weight (medium.py:196-207).
+
+    Uniform pairs (u1, u2) come from `rng.uniform` (two per sample, the
+    config-1 convention); the direction is returned in world space."""
+    wo = np.asarray(wo, dtype=np.float64)
+    shape = wo.shape[:-1] if n is None else (n,)
+    u = np.asarray(rng.uniform(shape + (2,)), dtype=np.float64)
+    if n is not None and wo.ndim == 1:
+        wo = np.broadcast_to(wo, (n, 3))
+    r, _ = _host_query(medium, wo, None, None, local_frame, u,
+                       ("wsx", "wsy", "wsz", "pdf_s", "w_r", "w_g", "w_b", "flags"))
+    if np.any(r["flags"] & 1):
+        raise DegenerateVisibilityError("projected area is zero toward wo")
+    wi = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1).astype(np.float64)
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1).astype(np.float64)
+    return wi, r["pdf_s"].astype(np.float64), w

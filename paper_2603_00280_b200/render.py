@@ -1,0 +1,151 @@
+"""Volumetric path tracer on the GPU (reference render.py:32-180).
+
+    render(scene, spp, seed, max_bounces=64, threads=None, tile=32, scene_hash="")
+        -> RadianceImage                                      render.py:127-180
+    render_device(...) -> (H, W, 3) float32 CUDA tensor (no host copies)
+    render_sharded(...)  one rank's share + one NCCL reduce to rank 0
+    trace_paths(origins, directions, scene, max_bounces, keys) render.py:32-108
+    trace_path(ray, scene, max_bounces, rng)                   render.py:111-124
+
+All path work runs in the persistent CUDA megakernel behind mf_render /
+mf_trace_paths.  Every path draws from Philox4x32-10 keyed by the seed with
+counter (pixel, sample, segment, call), so images are bit-identical for any
+tile size, pass size, thread count or number of GPUs under tile sharding
+(the reference's determinism contract, render.py:3-10, with a different
+generator -- parity with the reference is statistical).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ParameterDomainError
+from .image import RadianceImage
+from .scene import ShellScene, to_c_scene
+
+_SHARD = {"tiles": _lib.SHARD_TILES, "samples": _lib.SHARD_SAMPLES}
+
+
+def _params(spp, seed, max_bounces, tile, shard, rank, nranks, accumulate=False):
+    if spp < 1:
+        raise ParameterDomainError(f"spp must be >= 1, got {spp}")
+    if max_bounces < 1:
+        raise ParameterDomainError(f"max_bounces must be >= 1, got {max_bounces}")
+    if shard not in _SHARD:
+        raise ParameterDomainError(f"shard must be 'tiles' or 'samples', got {shard!r}")
+    p = _lib.MfRenderParams()
+    p.seed = int(seed) & (2**64 - 1)
+    p.spp = int(spp)
+    p.max_bounces = int(max_bounces)
+    p.tile = int(tile)
+    p.shard = _SHARD[shard]
+    p.rank, p.nranks = int(rank), int(nranks)
+    p.accumulate = 1 if accumulate else 0
+    return p
+
+
+def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
+                  shard="tiles", out=None, stats=False, stream=None, c_scene=None):
+    """Render into a (H, W, 3) float32 CUDA tensor holding radiance / spp for
+    this rank's share.  Returns (tensor, stats dict or None)."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    cam = scene.camera
+    if out is None:
+        out = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device="cuda")
+    if out.dtype != torch.float32 or not out.is_cuda or not out.is_contiguous() or \
+            tuple(out.shape) != (cam.height, cam.width, 3):
+        raise ParameterDomainError("out must be a contiguous (H, W, 3) float32 CUDA tensor")
+    cs = c_scene if c_scene is not None else to_c_scene(scene)
+    prm = _params(spp, seed, max_bounces, tile, shard, rank, nranks)
+    st = _lib.MfStats() if stats else None
+    s = stream if stream is not None else _lib.stream_handle(torch, out.device)
+    _lib.check(lib.mf_render(ctypes.byref(cs), ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
+                             ctypes.byref(st) if st is not None else None, s))
+    return out, (st.as_dict() if st is not None else None)
+
+
+def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, scene_hash=""):
+    """Render the scene camera (render.py:127-180); `threads` is accepted for
+    signature compatibility and ignored (the GPU path is deterministic for
+    any launch geometry)."""
+    if threads is not None and threads < 1:
+        raise ParameterDomainError(f"thread count must be >= 1, got {threads}")
+    img, _ = render_device(scene, spp, seed, max_bounces=max_bounces, tile=tile, stats=True)
+    out = RadianceImage(pixels=img.cpu().numpy().astype(np.float64),
+                        meta={"seed": int(seed), "spp": int(spp), "scene_hash": scene_hash})
+    out.validate()
+    return out
+
+
+def render_sharded(scene: ShellScene, spp, seed, max_bounces=64, tile=32, shard="tiles",
+                   group=None, stats=False):
+    """One rank's share of a multi-GPU render followed by a single NCCL
+    sum-reduce of the fp32 accumulation buffers to rank 0.
+    The kernel writes straight into the tensor NCCL sends, on the same
+    stream.  Tile sharding leaves non-owned pixels at +0.0, so the reduce is
+    exact and the image is bit-identical for any rank count.  Returns the
+    (H, W, 3) tensor (complete on rank 0) and this rank's stats."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    nranks = dist.get_world_size(group)
+    img, st = render_device(scene, spp, seed, max_bounces=max_bounces, tile=tile, rank=rank,
+                            nranks=nranks, shard=shard, stats=stats)
+    if nranks > 1:
+        dist.reduce(img, dst=0, op=dist.ReduceOp.SUM, group=group)
+    return img, st
+
+
+@dataclass
+class PathKeys:
+    """Random-stream keys of caller-given paths: path i draws from
+    Philox(seed; pixel[i], sample[i], segment, call)."""
+
+    seed: int
+    pixel: np.ndarray
+    sample: np.ndarray
+
+
+def trace_paths(origins, directions, scene: ShellScene, max_bounces, keys: PathKeys,
+                return_stats=False):
+    """Trace caller-given rays to completion; returns (N, 3) radiance."""
+    if max_bounces < 1:
+        raise ParameterDomainError(f"max_bounces must be >= 1, got {max_bounces}")
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    o = np.asarray(origins, dtype=np.float64)
+    d = np.asarray(directions, dtype=np.float64)
+    n = o.shape[0]
+    pix = np.broadcast_to(np.asarray(keys.pixel, dtype=np.uint32), (n,))
+    smp = np.broadcast_to(np.asarray(keys.sample, dtype=np.uint32), (n,))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    org_t = torch.from_numpy(np.ascontiguousarray(o.T, dtype=np.float32)).to(dev)
+    dir_t = torch.from_numpy(np.ascontiguousarray(d.T, dtype=np.float32)).to(dev)
+    pix_t = torch.from_numpy(np.ascontiguousarray(pix).view(np.int32)).to(dev)
+    smp_t = torch.from_numpy(np.ascontiguousarray(smp).view(np.int32)).to(dev)
+    rad = torch.empty((3, n), dtype=torch.float32, device=dev)
+    cs = to_c_scene(scene)
+    st = _lib.MfStats()
+    _lib.check(lib.mf_trace_paths(ctypes.byref(cs), org_t.data_ptr(), dir_t.data_ptr(),
+                                  pix_t.data_ptr(), smp_t.data_ptr(), int(keys.seed) & (2**64 - 1),
+                                  int(max_bounces), n, rad.data_ptr(), ctypes.byref(st),
+                                  _lib.stream_handle(torch, dev)))
+    out = rad.cpu().numpy().T.astype(np.float64)
+    return (out, st.as_dict()) if return_stats else out
+
+
+def trace_path(ray, scene: ShellScene, max_bounces, rng):
+    """Single-path convenience wrapper keyed by (rng.stream, rng.counter);
+    advances rng by one path (render.py:111-124)."""
+    origin, direction = ray
+    keys = PathKeys(rng.seed, np.array([rng.stream & 0xFFFFFFFF]),
+                    np.array([rng.counter & 0xFFFFFFFF]))
+    out = trace_paths(np.asarray(origin)[None, :], np.asarray(direction)[None, :], scene,
+                      max_bounces, keys)
+    rng.counter += 1
+    return out[0]

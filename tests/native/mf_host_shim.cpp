@@ -1,0 +1,81 @@
+// Host (CPU) build of the device math, for tests only: lets the CPU test
+// suite check every fp32 formula of csrc/mf_math.cuh / mf_query.cuh
+// against the float64 oracle without a GPU.  Not part of the product (the
+// package never loads this library; there is no CPU fallback).
+#include <cstdint>
+#include <string>
+
+#include "../../paper_2603_00280_b200/csrc/mf_prepare.h"
+#include "../../paper_2603_00280_b200/csrc/mf_query.cuh"
+
+using namespace mf;
+
+extern "C" {
+
+// which: 0 erfcx, 1 ierfcx, 2 bterm, 3 erfc, 4 ndtri, 5 mills, 6 log_ndtr,
+//        7 inv_log_ndtr, 8 erfinv(2x-1)
+int mfh_special(int which, const float* x, float* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    float v = x[i], r = 0.0f;
+    switch (which) {
+      case 0: r = erfcx_pos(v); break;
+      case 1: r = ierfcx_pos(v); break;
+      case 2: r = bterm_pos(v); break;
+      case 3: r = erfc_f(v); break;
+      case 4: r = ndtri(v); break;
+      case 5: r = mills(v); break;
+      case 6: r = log_ndtr(v); break;
+      case 7: r = inv_log_ndtr(v); break;
+      case 8: r = erfinv_2u_minus_1(v); break;
+      default: return 1;
+    }
+    out[i] = r;
+  }
+  return 0;
+}
+
+int mfh_slope(const float* nu, const float* u1, float* x, int32_t* iters, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    int it = 0;
+    x[i] = visible_slope_x(nu[i], u1[i], &it);
+    iters[i] = it;
+  }
+  return 0;
+}
+
+// in: 11 SoA float arrays (px py pz wox woy woz wix wiy wiz u1 u2)
+// out: 16 SoA float arrays (sigma_t, phase rgb, pdf, ws xyz, pdf_s, w rgb,
+//      flags, iters, proj_area(wo local), ndf(wi local as normal))
+int mfh_query(const mf_medium* med, const mf_primitive* field, const float* const* in,
+              float* const* out, int64_t n) {
+  MediumK m;
+  std::string err;
+  if (prepare_medium(*med, &m, &err) != MF_OK) return 1;
+  V3 c = v3((float)field->center[0], (float)field->center[1], (float)field->center[2]);
+  for (int64_t i = 0; i < n; ++i) {
+    V3 p = v3(in[0][i], in[1][i], in[2][i]);
+    V3 wo = v3(in[3][i], in[4][i], in[5][i]);
+    V3 wi = v3(in[6][i], in[7][i], in[8][i]);
+    QueryResult q = query_point(m, field->shape, (float)field->z0, c, (float)field->radius, p,
+                                wo, wi, in[9][i], in[10][i]);
+    out[0][i] = q.sigma_t;
+    out[1][i] = q.phase.x;
+    out[2][i] = q.phase.y;
+    out[3][i] = q.phase.z;
+    out[4][i] = q.pdf;
+    out[5][i] = q.ws.x;
+    out[6][i] = q.ws.y;
+    out[7][i] = q.ws.z;
+    out[8][i] = q.pdf_s;
+    out[9][i] = q.w.x;
+    out[10][i] = q.w.y;
+    out[11][i] = q.w.z;
+    out[12][i] = (float)q.flags;
+    out[13][i] = (float)q.iters;
+    out[14][i] = proj_area(m, wo);
+    out[15][i] = ndf(m, wi);
+  }
+  return 0;
+}
+
+}  // extern "C"
