@@ -133,6 +133,7 @@ typedef struct mf_stats {
   uint64_t degenerate;    /* sigma(wo) < 1e-12 at a scatter (returns 0) */
   uint64_t nonfinite;
   uint64_t capped;        /* paths cut by the segment cap */
+  double path_kernel_ms;  /* CUDA-event time of the path megakernel launches */
 } mf_stats;
 
 /* ---------------------------------------------------------------------
@@ -198,6 +199,11 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
 int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],
                      int64_t n, uint64_t seed, uint64_t stream_id, double* mean, double* se,
                      void* stream);
+
+/* Issue-rate peaks of this device measured by microbenchmark kernels
+ * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane
+ * instructions per second: the FP32 / SFU roofline denominators. */
+int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream);
 
 /* diagnostics */
 const char* mf_last_error(void);

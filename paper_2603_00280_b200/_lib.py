@@ -67,10 +67,12 @@ STAT_FIELDS = ("paths", "segments", "scatters", "nee", "slope_iters", "track_ste
 
 
 class MfStats(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_uint64) for n in STAT_FIELDS]
+    _fields_ = [(n, ctypes.c_uint64) for n in STAT_FIELDS] + [("path_kernel_ms", ctypes.c_double)]
 
     def as_dict(self):
-        return {n: int(getattr(self, n)) for n in STAT_FIELDS}
+        d = {n: int(getattr(self, n)) for n in STAT_FIELDS}
+        d["path_kernel_ms"] = float(self.path_kernel_ms)
+        return d
 
 
 _vp = ctypes.c_void_p
@@ -100,6 +102,8 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                         ctypes.c_uint64, ctypes.c_uint64,
                                         ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_double), _vp]),
+    "mf_measure_peaks": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), _vp]),
     "mf_last_error": (ctypes.c_char_p, []),
     "mf_abi_version": (ctypes.c_int, []),

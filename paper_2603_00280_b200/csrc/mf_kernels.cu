@@ -412,6 +412,38 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
 }
 
 // ---------------------------------------------------------------------------
+// roofline microbenchmarks: 8 independent FFMA chains / 4 MUFU.EX2 chains
+
+__global__ void __launch_bounds__(256) peak_ffma_kernel(float* out, int iters, float a, float b) {
+  float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  float x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 123.456f) out[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) peak_mufu_kernel(float* out, int iters) {
+  float x0 = threadIdx.x * -1e-6f, x1 = x0 - 0.1f, x2 = x0 - 0.2f, x3 = x0 - 0.3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x0));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x1));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x2));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x3));
+    }
+  }
+  float s = x0 + x1 + x2 + x3;
+  if (s == 123.456f) out[threadIdx.x] = s;
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 double log_ndtr_host(double u) { return std::log(0.5 * std::erfc(-u / std::sqrt(2.0))); }
@@ -560,6 +592,7 @@ int device_occupancy(Occupancy* occ) {
 }
 
 void fill_stats(const unsigned long long* h, mf_stats* s) {
+  s->path_kernel_ms = 0.0;
   s->paths = h[kStPaths];
   s->segments = h[kStSegments];
   s->scatters = h[kStScatters];
@@ -635,6 +668,48 @@ constexpr size_t kMaxPassPaths = size_t(1) << 26;  // 64 Mi paths (768 MiB of ra
 extern "C" {
 
 const char* mf_last_error(void) { return g_err.c_str(); }
+
+int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream) {
+  if (!fp32_ginst_s || !sfu_ginst_s) return fail(MF_ERR_PARAM, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  MF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float* dummy = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&dummy, 256 * sizeof(float), st));
+  cudaEvent_t e0, e1;
+  MF_CUDA(cudaEventCreate(&e0));
+  MF_CUDA(cudaEventCreate(&e1));
+  const int blocks = sms * 8, threads = 256;
+  double best_f = 0.0, best_s = 0.0;
+  for (int rep = 0; rep < 3; ++rep) {
+    const int it_f = 4096;
+    MF_CUDA(cudaEventRecord(e0, st));
+    peak_ffma_kernel<<<blocks, threads, 0, st>>>(dummy, it_f, 0.9999f, 1e-4f);
+    MF_CUDA(cudaEventRecord(e1, st));
+    MF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    MF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    double n = (double)blocks * threads * it_f * 16 * 8;
+    if (rep) best_f = std::max(best_f, n / (ms * 1e-3) / 1e9);
+    const int it_s = 1024;
+    MF_CUDA(cudaEventRecord(e0, st));
+    peak_mufu_kernel<<<blocks, threads, 0, st>>>(dummy, it_s);
+    MF_CUDA(cudaEventRecord(e1, st));
+    MF_CUDA(cudaEventSynchronize(e1));
+    MF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    n = (double)blocks * threads * it_s * 16 * 4;
+    if (rep) best_s = std::max(best_s, n / (ms * 1e-3) / 1e9);
+    g_launches += 2;
+  }
+  MF_CUDA(cudaGetLastError());
+  MF_CUDA(cudaFreeAsync(dummy, st));
+  MF_CUDA(cudaEventDestroy(e0));
+  MF_CUDA(cudaEventDestroy(e1));
+  *fp32_ginst_s = best_f;
+  *sfu_ginst_s = best_s;
+  return MF_OK;
+}
 int mf_abi_version(void) { return MF_ABI_VERSION; }
 uint64_t mf_launch_count(void) { return g_launches; }
 
@@ -732,13 +807,27 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   ps.counter = scr.counter;
   ps.stats = scr.stats;
   float inv_spp = (float)(1.0 / p.spp);
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double kernel_ms = 0.0;
+  if (stats) {
+    MF_CUDA(cudaEventCreate(&ev[0]));
+    MF_CUDA(cudaEventCreate(&ev[1]));
+  }
   for (uint32_t s0 = 0; s0 < s_count; s0 += S_pass) {
     uint32_t S = std::min(S_pass, s_count - s0);
     ps.S = S;
     ps.sample_begin = s_begin + s0;
     ps.n_paths = (uint32_t)(n_local * S);
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
+    if (stats) MF_CUDA(cudaEventRecord(ev[0], st));
     rc = launch_paths(sc, ps, false, st);
+    if (stats && !rc) {
+      MF_CUDA(cudaEventRecord(ev[1], st));
+      MF_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0.0f;
+      MF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      kernel_ms += ms;
+    }
     if (rc) {
       scratch_free(&scr, st);
       return rc;
@@ -754,6 +843,9 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     MF_CUDA(cudaStreamSynchronize(st));
     fill_stats(h, stats);
+    stats->path_kernel_ms = kernel_ms;
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
     out = check_stats(*stats);
   }
   rc = scratch_free(&scr, st);

@@ -27,6 +27,7 @@ from . import _lib
 from .core import Frame
 from .errors import DegenerateVisibilityError, ParameterDomainError
 from .ndf import NdfKind, RoughnessTriple
+from .rng import draw_uniforms
 
 DEFAULT_ETA = (0.2, 0.92, 1.1)
 DEFAULT_K = (3.9, 2.45, 2.14)
@@ -213,7 +214,7 @@ def phase_sample(wo, medium: MacrofacetMedium, local_frame: Frame, rng, n=None):
     config-1 convention); the direction is returned in world space."""
     wo = np.asarray(wo, dtype=np.float64)
     shape = wo.shape[:-1] if n is None else (n,)
-    u = np.asarray(rng.uniform(shape + (2,)), dtype=np.float64)
+    u = draw_uniforms(rng, shape + (2,))
     if n is not None and wo.ndim == 1:
         wo = np.broadcast_to(wo, (n, 3))
     r, _ = _host_query(medium, wo, None, None, local_frame, u,

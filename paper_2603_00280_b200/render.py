@@ -52,6 +52,7 @@ def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0,
                   shard="tiles", out=None, stats=False, stream=None, c_scene=None):
     """Render into a (H, W, 3) float32 CUDA tensor holding radiance / spp for
     this rank's share.  Returns (tensor, stats dict or None)."""
+    prm = _params(spp, seed, max_bounces, tile, shard, rank, nranks)
     torch = _lib.require_cuda()
     lib = _lib.load()
     cam = scene.camera
@@ -61,7 +62,6 @@ def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0,
             tuple(out.shape) != (cam.height, cam.width, 3):
         raise ParameterDomainError("out must be a contiguous (H, W, 3) float32 CUDA tensor")
     cs = c_scene if c_scene is not None else to_c_scene(scene)
-    prm = _params(spp, seed, max_bounces, tile, shard, rank, nranks)
     st = _lib.MfStats() if stats else None
     s = stream if stream is not None else _lib.stream_handle(torch, out.device)
     _lib.check(lib.mf_render(ctypes.byref(cs), ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
@@ -99,6 +99,26 @@ def render_sharded(scene: ShellScene, spp, seed, max_bounces=64, tile=32, shard=
     if nranks > 1:
         dist.reduce(img, dst=0, op=dist.ReduceOp.SUM, group=group)
     return img, st
+
+
+def sample_range(spp, rank, nranks):
+    """[begin, end) of the samples rank `rank` renders under sample sharding
+    (same split as mf_render)."""
+    return spp * rank // nranks, spp * (rank + 1) // nranks
+
+
+def owned_pixels(width, height, tile, rank, nranks):
+    """Pixel indices rank `rank` renders under interleaved tile sharding:
+    tile t = ty * tiles_x + tx belongs to rank t mod nranks (the same map
+    as local_to_pixel in csrc/mf_kernels.cu)."""
+    tx = (width + tile - 1) // tile
+    ty = (height + tile - 1) // tile
+    out = []
+    for t in range(rank, tx * ty, nranks):
+        y0, x0 = (t // tx) * tile, (t % tx) * tile
+        yy, xx = np.mgrid[y0:min(height, y0 + tile), x0:min(width, x0 + tile)]
+        out.append((yy * width + xx).ravel())
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
 
 
 @dataclass

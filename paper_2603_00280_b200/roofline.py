@@ -1,0 +1,93 @@
+"""Frozen algorithmic work counts for the FP32 / SFU issue roofline.
+
+SURVEY.md 8(d): the per-unit work is counted from the fp32 SOURCE FORMULAS
+of csrc/mf_math.cuh / mf_transport.cuh (not from SASS), per device event,
+and multiplied by the event counters the kernels report (mf_stats):
+
+    F = sum_e count_e * fp32_e      (FMA / FMUL / FADD, integer IMAD of
+                                     Philox; 1 each on the FMA pipe)
+    S = sum_e count_e * sfu_e       (MUFU RCP / RSQ / SQRT / EX2 / LG2)
+    roofline fraction = max(F / P_fp32, S / P_sfu) / T_kernel
+
+Comparisons, selects, min/max, integer logic and conversions are NOT
+counted (ALU pipe); neither are divergence and re-convergence.  The
+peaks P are measured on the device by mf_measure_peaks (FFMA / MUFU.EX2
+microbenchmarks).  The per-primitive costs below are the counts of the
+formulas as written (library expf = 3 F + 1 S, logf = 10 F, log1pf = 12
+F, approximate division / sqrt = 1 F + 1 S).
+"""
+
+from __future__ import annotations
+
+# cost of the building blocks, (fp32, sfu)
+PRIMS = {
+    "erfcx": (16, 1),
+    "ierfcx": (18, 1),
+    "erfcx_pair": (32, 1),
+    "exp_neg_sq": (7, 1),
+    "mills": (22, 2.5),
+    "log_ndtr": (35, 1.5),
+    "ndtri": (27, 0),
+    "inv_log_ndtr": (89, 5),
+    "proj_area": (33, 3),
+    "frame": (10, 1),
+    "rotate": (9, 0),
+    "ndf_generalized": (45, 4.5),
+    "ndf_beckmann": (10, 2),
+    "phase_eval": (67, 8.5),
+    "mixture_pdf": (16, 3),
+    "philox": (44, 0),
+    "slope_log_cdf": (52, 2.5),
+}
+
+# per-event costs, (fp32, sfu)
+EVENTS = {
+    # raygen: Philox block + orthographic / pinhole camera ray
+    "paths": (54, 2),
+    # free-flight segment: Philox block + sigma(dir) + analytic planar flight
+    # (log(u), log_ndtr, division, inv_log_ndtr, position update)
+    "segments": (212, 12.5),
+    # real scatter: frame + sigma(wo) + phase sample (sigma_b, branch remap,
+    # mixture pdf, vNDF weight, 50/50 Beckmann (55 + 110 base) / hemisphere
+    # (43) proposal, rotation, throughput, RR)
+    "scatters": (275, 26),
+    # next-event estimation: phase_eval + sigma(wl) + closed-form / walk Tr
+    "nee": (157, 15),
+    # one Newton iteration of the visible-slope inversion
+    "slope_iters": (57, 3.5),
+    # one delta / ratio tracking step on a curved shell (majorant, sample,
+    # tentative extinction)
+    "track_steps": (70, 8),
+}
+
+
+def algorithmic_ops(stats):
+    """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters."""
+    f = s = 0.0
+    for ev, (cf, cs) in EVENTS.items():
+        n = float(stats.get(ev, 0))
+        f += n * cf
+        s += n * cs
+    return f, s
+
+
+def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst):
+    """Achieved issue rates and the roofline fraction of the path kernel."""
+    f, s = algorithmic_ops(stats)
+    t = kernel_ms * 1e-3
+    af = f / t / 1e9
+    asf = s / t / 1e9
+    ff = af / peak_fp32_ginst
+    fs = asf / peak_sfu_ginst
+    bound = "fp32" if ff >= fs else "sfu"
+    return {
+        "bound": bound,
+        "achieved": af if bound == "fp32" else asf,
+        "peak": peak_fp32_ginst if bound == "fp32" else peak_sfu_ginst,
+        "unit": "Ginst/s",
+        "frac": max(ff, fs),
+        "fp32_frac": ff,
+        "sfu_frac": fs,
+        "fp32_per_path": f / max(float(stats.get("paths", 1)), 1.0),
+        "sfu_per_path": s / max(float(stats.get("paths", 1)), 1.0),
+    }

@@ -1,0 +1,144 @@
+"""Shared parity policy: fp32 device results vs the float64 oracle.
+
+Bar (BASELINE north_star): sigma_t, phase value / pdf and sampled
+directions within 1e-5 relative of the oracle on identical inputs.  Inputs
+(and medium parameters) are rounded to float32 first and the oracle
+consumes exactly those values.  Where float32 cannot represent the
+problem to 1e-5 the tolerance follows the conditioning:
+
+* sigma_t: rounding u = f/sigma costs ~u^2 2^-24 relative, so
+  tol = max(1e-5, 4 u^2 2^-24); values below FLT_MIN * 1e3 in float64 only
+  need to be tiny on the device (underflow policy).
+* phase value: 1e-5 relative.  pdf: 1e-5 relative, loosened to
+  4 ulp / (v.h) for near-forward pairs: the pdf carries 1 / (v.h) and
+  v.h = (1 + v.wi)/|v + wi| -> 0 cancels in any float32 evaluation (the
+  phase value does not: its vNDF numerator carries the same v.h).
+* sampled direction: <= 1e-5 rad for >= 99.99 % of queries, and every
+  query within max(1e-5, 16 kappa), kappa the angle the oracle's own
+  output moves when its uniforms move by one float32 ulp (the sampler's
+  inverse-CDF conditioning); pdf_s / weight, which inherit the direction
+  error through 1/(v.m) near grazing visible normals, within
+  max(1e-5, 64 kappa) relative and >= 99.5 % within 1e-5.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import microfacet as om
+
+FLT_MIN = 1.1754943508222875e-38
+ULP = 2.0 ** -24
+
+
+class Obj:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def f32_medium(med):
+    """Oracle copy of a repo medium with float32-rounded parameters."""
+    return Obj(kind=med.kind, a3=Obj(ax=float(np.float32(med.a3.ax)),
+                                     ay=float(np.float32(med.a3.ay)),
+                                     az=float(np.float32(med.a3.az))),
+               sigma=float(np.float32(med.sigma)), mix_ratio=float(np.float32(med.mix_ratio)),
+               fresnel_one=med.fresnel_one, fresnel_eta=med.fresnel_eta,
+               fresnel_k=med.fresnel_k, albedo=med.albedo)
+
+
+def relerr(got, ref, floor=1e-300):
+    got = np.asarray(got, dtype=np.float64)
+    return np.abs(got - ref) / np.maximum(np.abs(ref), floor)
+
+
+def angle(a, b):
+    a = a / np.linalg.norm(a, axis=-1, keepdims=True)
+    b = b / np.linalg.norm(b, axis=-1, keepdims=True)
+    return np.arctan2(np.linalg.norm(np.cross(a, b), axis=-1), np.sum(a * b, axis=-1))
+
+
+def check_sigma_t(got, f, sigma, ref):
+    u = np.asarray(f, dtype=np.float64) / sigma
+    tiny = ref < FLT_MIN * 1e3
+    tol = np.maximum(1e-5, 4.0 * u * u * ULP)
+    e = relerr(got, ref)
+    bad_big = ~tiny & (e > tol)
+    bad_tiny = tiny & (np.asarray(got, dtype=np.float64) > FLT_MIN * 1e4)
+    return {"max_rel_in_band": float(np.max(e[~tiny & (u >= -6) & (u <= 3)], initial=0.0)),
+            "n_bad": int(bad_big.sum() + bad_tiny.sum()), "n": int(len(e))}
+
+
+def pdf_tolerance(wo, wi):
+    """Per-query pdf tolerance: max(1e-5, 4 ulp / (v.h))."""
+    v = -np.asarray(wo, dtype=np.float64)
+    h = v + np.asarray(wi, dtype=np.float64)
+    h /= np.maximum(np.linalg.norm(h, axis=-1, keepdims=True), 1e-300)
+    vh = np.abs(np.sum(v * h, axis=-1))
+    return np.maximum(1e-5, 4.0 * ULP / np.maximum(vh, 1e-300))
+
+
+def phase_tolerance(wo, wi, m):
+    """max(1e-5, 4 ulp (1 + E)), E the NDF exponent at the half vector: the
+    Beckmann e^{-E} (ndf.py:85-94) and the generalized e^{r - c}
+    (ndf.py:216-222) turn the float32 rounding of h into ~E ulps."""
+    v = -np.asarray(wo, dtype=np.float64)
+    h = v + np.asarray(wi, dtype=np.float64)
+    h /= np.maximum(np.linalg.norm(h, axis=-1, keepdims=True), 1e-300)
+    ax, ay = m.a3.ax, m.a3.ay
+    lat = (h[..., 0] / ax) ** 2 + (h[..., 1] / ay) ** 2
+    e_beck = lat / np.maximum(h[..., 2] ** 2, 1e-300)
+    az = getattr(m.a3, "az", 0.0)
+    e_gen = lat / max(az * az, 1e-300) / np.maximum(lat + (h[..., 2] / max(az, 1e-300)) ** 2,
+                                                     1e-300)
+    kind = getattr(m.kind, "value", m.kind)
+    e = e_beck if kind == "beckmann" else e_gen
+    return np.maximum(1e-5, 4.0 * ULP * (1.0 + np.minimum(e, 1e6)))
+
+
+def check_rel(got, ref, tol=1e-5, floor=1e-30):
+    ok = np.abs(ref) > floor
+    e = relerr(got, ref)
+    bad = (ok & (e > tol)) | (~ok & (np.abs(np.asarray(got, dtype=np.float64)) > 1e-20))
+    return {"max_rel": float(np.max(e[ok], initial=0.0)), "n_bad": int(bad.sum()),
+            "n": int(len(e))}
+
+
+def oracle_sample(wo, m, u1, u2):
+    """Oracle phase sample for the two-uniform convention; u1, u2 float32."""
+    mix = np.float32(m.mix_ratio)
+    u1 = np.asarray(u1, dtype=np.float32)
+    uu = np.where(u1 < mix, u1 / mix, (u1 - mix) / (np.float32(1) - mix)).astype(np.float32)
+    U3 = np.stack([u1, uu, np.asarray(u2, dtype=np.float32)], axis=-1).astype(np.float64)
+    return om.phase_sample_local(wo, m, U3)
+
+
+def check_samples(ws, pdf_s, w, wo, m, u1, u2):
+    """Direction / pdf / weight of sampled directions vs the oracle, with the
+    conditioning-scaled tolerance of the module docstring."""
+    ws_r, pdf_r, w_r = oracle_sample(wo, m, u1, u2)
+    u1 = np.asarray(u1, dtype=np.float32)
+    u2 = np.asarray(u2, dtype=np.float32)
+    # one-ulp perturbations of each uniform (kept inside [0, 1))
+    u1p = np.nextafter(u1, np.float32(1)).astype(np.float32)
+    u2p = np.nextafter(u2, np.float32(1)).astype(np.float32)
+    ws_a, pdf_a, w_a = oracle_sample(wo, m, u1p, u2)
+    ws_b, pdf_b, w_b = oracle_sample(wo, m, u1, u2p)
+    kap_dir = angle(ws_a, ws_r) + angle(ws_b, ws_r)
+    kap_pdf = relerr(pdf_a, pdf_r, 1e-30) + relerr(pdf_b, pdf_r, 1e-30)
+    kap_w = relerr(w_a[:, 0], w_r[:, 0], 1e-30) + relerr(w_b[:, 0], w_r[:, 0], 1e-30)
+    ang = angle(np.asarray(ws, dtype=np.float64), ws_r)
+    tol_dir = np.maximum(1e-5, 16.0 * kap_dir)
+    e_pdf = relerr(pdf_s, pdf_r, 1e-30)
+    e_w = relerr(np.asarray(w)[:, 0], w_r[:, 0], 1e-30)
+    tol_pdf = np.maximum(1e-5, 64.0 * kap_pdf)
+    tol_w = np.maximum(1e-5, 64.0 * kap_w)
+    return {
+        "frac_dir_within_1e-5": float(np.mean(ang <= 1e-5)),
+        "max_angle": float(ang.max()),
+        "n_dir_bad": int(np.sum(ang > tol_dir)),
+        "frac_pdf_within_1e-5": float(np.mean(e_pdf <= 1e-5)),
+        "n_pdf_bad": int(np.sum(e_pdf > tol_pdf)),
+        "frac_w_within_1e-5": float(np.mean(e_w <= 1e-5)),
+        "n_w_bad": int(np.sum(e_w > tol_w)),
+        "n": int(len(ang)),
+    }

@@ -1,0 +1,193 @@
+"""Coefficient-query parity on the B200 (BASELINE config 1) through the C
+ABI: the CUDA `query` kernel vs the float64 oracle on identical
+float32 inputs, with the tolerance policy of tests/parity.py, plus the
+reference's own outputs (tests/golden/config1_ref.npz)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_00280_b200 as mf
+from oracle import microfacet as om
+from paper_2603_00280_b200 import _lib, configs
+
+import parity
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_query(torch, med, p, wo, wi, u, field=None):
+    d = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(d)
+    r = mf.query_batch(med, t(p.T), t(wo.T), t(wi.T), t(u[:, 0]), t(u[:, 1]), field=field)
+    return {k: v.cpu().numpy() for k, v in r.items()}
+
+
+def test_config1_full_batch(cuda):
+    p, wo, wi, u = configs.config1_inputs()            # N = 2^20
+    med = configs.config1_medium()
+    m = parity.f32_medium(med)
+    r = dev_query(cuda, med, p, wo, wi, u)
+    P, WO, WI = (a.astype(np.float64) for a in (p, wo, wi))
+    res = parity.check_sigma_t(r["sigma_t"], P[:, 2], m.sigma,
+                               om.extinction_local(WO, P[:, 2], m))
+    assert res["n_bad"] == 0 and res["max_rel_in_band"] < 1e-5, res
+    res = parity.check_rel(r["phase_r"], om.phase_eval_local(WO, WI, m)[:, 0],
+                           tol=parity.phase_tolerance(WO, WI, m))
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["pdf"], om.phase_pdf_local(WO, WI, m),
+                           tol=parity.pdf_tolerance(WO, WI))
+    assert res["n_bad"] == 0, res
+    assert np.all(r["flags"] == 0)
+    # sampled directions / pdf / weight on the first 2^16 queries
+    n = 1 << 16
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)[:n]
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)[:n]
+    res = parity.check_samples(ws, r["pdf_s"][:n], w, WO[:n], m, u[:n, 0], u[:n, 1])
+    assert res["frac_dir_within_1e-5"] >= 0.9999, res
+    assert res["frac_pdf_within_1e-5"] >= 0.995 and res["frac_w_within_1e-5"] >= 0.995, res
+    assert res["n_dir_bad"] == 0 and res["n_pdf_bad"] == 0 and res["n_w_bad"] == 0, res
+
+
+def test_config1_against_reference_outputs(cuda):
+    """Device vs the reference package's own outputs on the committed
+    fixture (generated in the build container by make_golden.py)."""
+    g = np.load(os.path.join(GOLDEN, "config1_ref.npz"))
+    med = configs.config1_medium()
+    m = parity.f32_medium(med)
+    r = dev_query(cuda, med, g["p"], g["wo"], g["wi"], g["u"])
+    WO, WI = g["wo"].astype(np.float64), g["wi"].astype(np.float64)
+    res = parity.check_sigma_t(r["sigma_t"], g["p"][:, 2].astype(np.float64), m.sigma,
+                               g["sigma_t"])
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["phase_r"], g["phase"][:, 0], tol=parity.phase_tolerance(WO, WI, m))
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["pdf"], g["pdf"], tol=parity.pdf_tolerance(WO, WI))
+    assert res["n_bad"] == 0, res
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)
+    ang = parity.angle(ws.astype(np.float64), g["ws"])
+    assert np.mean(ang <= 1e-5) >= 0.999, float(np.max(ang))
+
+
+@pytest.mark.parametrize("sigma,lz", [(0.01, 0.02), (0.2, 0.02), (0.05, 0.1), (0.2, 0.1),
+                                      (0.05, float("inf")), (0.2, float("inf"))])
+def test_config4_media(cuda, sigma, lz):
+    med = configs.planar_medium(sigma, 0.05, lz, 0.8)
+    m = parity.f32_medium(med)
+    rs = np.random.default_rng(44)
+    n = 1 << 16
+    wo = rs.normal(size=(n, 3))
+    wo /= np.linalg.norm(wo, axis=-1, keepdims=True)
+    wi = rs.normal(size=(n, 3))
+    wi /= np.linalg.norm(wi, axis=-1, keepdims=True)
+    wo, wi = wo.astype(np.float32), wi.astype(np.float32)
+    sig = om.projected_area(wo.astype(np.float64), m.kind.value, m.a3.ax, m.a3.ay, m.a3.az)
+    keep = sig > 1e-9
+    wo, wi = wo[keep], wi[keep]
+    p = np.zeros((len(wo), 3), np.float32)
+    p[:, 2] = rs.uniform(-6 * sigma, 3 * sigma, len(wo))
+    u = rs.uniform(size=(len(wo), 2)).astype(np.float32)
+    r = dev_query(cuda, med, p, wo, wi, u)
+    P, WO, WI = p.astype(np.float64), wo.astype(np.float64), wi.astype(np.float64)
+    res = parity.check_sigma_t(r["sigma_t"], P[:, 2], m.sigma, om.extinction_local(WO, P[:, 2], m))
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["phase_r"], om.phase_eval_local(WO, WI, m)[:, 0], floor=1e-25,
+                           tol=parity.phase_tolerance(WO, WI, m))
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["pdf"], om.phase_pdf_local(WO, WI, m), floor=1e-25,
+                           tol=parity.pdf_tolerance(WO, WI))
+    assert res["n_bad"] == 0, res
+
+
+def test_sphere_field_and_frames(cuda):
+    """f and the local frame derived on the device from a sphere field
+    (sdf.py:35-52 + core.py:156-169) match the oracle."""
+    rs = np.random.default_rng(9)
+    n = 1 << 14
+    p = rs.normal(size=(n, 3))
+    p = (p / np.linalg.norm(p, axis=-1, keepdims=True) * rs.uniform(0.5, 1.5, (n, 1)))
+    p = p.astype(np.float32)
+    wo = rs.normal(size=(n, 3))
+    wo = (wo / np.linalg.norm(wo, axis=-1, keepdims=True)).astype(np.float32)
+    wi = rs.normal(size=(n, 3))
+    wi = (wi / np.linalg.norm(wi, axis=-1, keepdims=True)).astype(np.float32)
+    u = rs.uniform(size=(n, 2)).astype(np.float32)
+    a = np.sqrt(2) * 0.1 / 0.05
+    med = mf.MacrofacetMedium(kind=mf.NdfKind.GENERALIZED, a3=mf.RoughnessTriple(a, a, a),
+                              sigma=0.1, fresnel_one=True)
+    fld = _lib.MfPrimitive()
+    fld.shape = _lib.SHAPE_SPHERE
+    fld.radius = 1.0
+    r = dev_query(cuda, med, p, wo, wi, u, field=fld)
+    m = parity.f32_medium(med)
+    from oracle.numerics import frame_about, to_local
+    P = p.astype(np.float64)
+    nrm = P / np.linalg.norm(P, axis=-1, keepdims=True)
+    fr = frame_about(nrm)
+    f = np.linalg.norm(P, axis=-1) - 1.0
+    WOl, WIl = to_local(fr, wo.astype(np.float64)), to_local(fr, wi.astype(np.float64))
+    ref = om.extinction_local(WOl, f, m)
+    ok = np.abs(f / 0.1) < 6
+    e = parity.relerr(r["sigma_t"][ok], ref[ok])
+    # f is computed from p in float32 on the device: |p| - 1 costs ~2 ulp of |p|
+    tol = np.maximum(1e-5, 8 * 2.0 ** -24 * (np.abs(f[ok]) + 1) / 0.1 * (np.abs(f[ok]) / 0.1 + 2))
+    assert np.all(e <= tol), float(np.max(e / tol))
+    res = parity.check_rel(r["phase_r"], om.phase_eval_local(WOl, WIl, m)[:, 0],
+                           tol=10 * parity.phase_tolerance(WOl, WIl, m))
+    assert res["n_bad"] == 0, res
+
+
+def test_public_medium_api(cuda):
+    """extinction / phase_eval / phase_pdf / phase_sample with host arrays
+    and an explicit frame keep the reference signatures (medium.py:91-207)."""
+    med = mf.MacrofacetMedium(kind=mf.NdfKind.GENERALIZED, a3=mf.RoughnessTriple(1, 1, 1),
+                              sigma=1.0)
+    frame = mf.build_frame(np.array([0.0, 0.0, 1.0]))
+    wo = np.array([np.sin(np.pi / 4), 0.0, np.cos(np.pi / 4)])
+    # test_medium.py:64-67 golden values, float32 accuracy
+    assert abs(mf.extinction(wo, 0.0, med, frame) - 0.04700572065395207) < 1e-5 * 0.047
+    g = mf.extinction(np.array([1.0, 0, 0]), 0.0, med, frame)
+    assert abs(g - 0.22507907903927652) < 1e-5 * 0.225
+    rs = np.random.default_rng(3)
+    wo = rs.normal(size=(500, 3))
+    wo /= np.linalg.norm(wo, axis=-1, keepdims=True)
+    wi = rs.normal(size=(500, 3))
+    wi /= np.linalg.norm(wi, axis=-1, keepdims=True)
+    ph = mf.phase_eval(wo, wi, med, frame)
+    m = parity.f32_medium(med)
+    ref = om.phase_eval_local(wo.astype(np.float32).astype(np.float64),
+                              wi.astype(np.float32).astype(np.float64), m)
+    assert ph.shape == (500, 3)
+    assert np.max(np.abs(ph - ref) / np.maximum(ref, 1e-30)) < 1e-4
+    wi_s, pdf, w = mf.phase_sample(wo[0], med, frame, np.random.default_rng(5), n=1000)
+    assert wi_s.shape == (1000, 3) and pdf.shape == (1000,) and w.shape == (1000, 3)
+    assert np.all(pdf >= 0) and np.all(w >= 0) and np.all(np.isfinite(w))
+    # pdf returned by sampling equals phase_pdf at the sampled direction
+    pdf2 = mf.phase_pdf(np.broadcast_to(wo[0], (1000, 3)), wi_s, med, frame)
+    np.testing.assert_allclose(pdf, pdf2, rtol=2e-3)
+
+
+def test_degenerate_view_raises(cuda):
+    # ndf.py:312-313: sigma(wo) < 1e-12 -> DegenerateVisibilityError
+    med = mf.MacrofacetMedium(kind=mf.NdfKind.BECKMANN, a3=mf.RoughnessTriple(0.1, 0.1, 0),
+                              sigma=1.0)
+    frame = mf.build_frame(np.array([0.0, 0.0, 1.0]))
+    with pytest.raises(mf.DegenerateVisibilityError):
+        mf.phase_eval(np.array([0.0, 0.0, 1.0]), np.array([0.0, 0.0, -1.0]), med, frame)
+
+
+def test_throughput_smoke(cuda):
+    """The 2^24-query batch runs and is deterministic."""
+    torch = cuda
+    p, wo, wi, u = configs.config1_inputs(n=1 << 20)
+    d = torch.device("cuda", 0)
+    t = lambda a, k: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(d).repeat(k)
+    P = torch.stack([t(p[:, i], 16) for i in range(3)])
+    WO = torch.stack([t(wo[:, i], 16) for i in range(3)])
+    WI = torch.stack([t(wi[:, i], 16) for i in range(3)])
+    med = configs.config1_medium()
+    a = mf.query_batch(med, P, WO, WI, t(u[:, 0], 16), t(u[:, 1], 16), outputs=("sigma_t",))
+    b = mf.query_batch(med, P, WO, WI, t(u[:, 0], 16), t(u[:, 1], 16), outputs=("sigma_t",))
+    assert torch.equal(a["sigma_t"], b["sigma_t"])
