@@ -492,7 +492,9 @@ int build_scene(const mf_scene& in, SceneDev* out) {
     sc.media[j] = mk;
     double s = in.media[pk.medium].sigma;
     min_sigma = std::min(min_sigma, s);
-    sc.mx[j].sig_max = (float)sigma_max_host(mk);
+    // exact majorant factor, needed only by the tracking walker (curved shells)
+    bool planar_only = in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE;
+    sc.mx[j].sig_max = planar_only ? mk.sig_bound : (float)sigma_max_host(mk);
     sc.mx[j].lphi_hi = (float)log_ndtr_host(3.0);
     sc.mx[j].lphi_lo_col = (float)log_ndtr_host(-6.0);
     sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);

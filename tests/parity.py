@@ -17,8 +17,10 @@ problem to 1e-5 the tolerance follows the conditioning:
   query within max(1e-5, 16 kappa), kappa the angle the oracle's own
   output moves when its uniforms move by one float32 ulp (the sampler's
   inverse-CDF conditioning); pdf_s / weight, which inherit the direction
-  error through 1/(v.m) near grazing visible normals, within
-  max(1e-5, 64 kappa) relative and >= 99.5 % within 1e-5.
+  error through 1/(v.m) and the NDF exponents near grazing microfacet
+  normals, within max(1e-5, 64 kappa, 4 kappa_m) relative (kappa_m: the
+  change under a 4-ulp tilt of the microfacet normal) and >= 99.5 % within
+  1e-5.
 """
 
 from __future__ import annotations
@@ -112,6 +114,14 @@ def oracle_sample(wo, m, u1, u2):
     return om.phase_sample_local(wo, m, U3)
 
 
+def _f(m):
+    """Grey Fresnel / albedo factor of channel 0 (F == 1 or albedo media)."""
+    alb = getattr(m, "albedo", None)
+    if alb is not None:
+        return float(np.ravel(alb)[0])
+    return 1.0
+
+
 def check_samples(ws, pdf_s, w, wo, m, u1, u2):
     """Direction / pdf / weight of sampled directions vs the oracle, with the
     conditioning-scaled tolerance of the module docstring."""
@@ -126,12 +136,38 @@ def check_samples(ws, pdf_s, w, wo, m, u1, u2):
     kap_dir = angle(ws_a, ws_r) + angle(ws_b, ws_r)
     kap_pdf = relerr(pdf_a, pdf_r, 1e-30) + relerr(pdf_b, pdf_r, 1e-30)
     kap_w = relerr(w_a[:, 0], w_r[:, 0], 1e-30) + relerr(w_b[:, 0], w_r[:, 0], 1e-30)
+    # sensitivity of pdf_s / weight to rounding the microfacet normal itself
+    # (4 ulp tilts along two tangents): grazing normals make the Beckmann /
+    # generalized exponents amplify it
+    kind = getattr(m.kind, "value", m.kind)
+    ax, ay, az = m.a3.ax, m.a3.ay, (m.a3.az if kind == "generalized" else 0.0)
+    v = -np.asarray(wo, dtype=np.float64)
+    wm = v + ws_r
+    wm /= np.linalg.norm(wm, axis=-1, keepdims=True)
+    helper = np.where(np.abs(wm[:, :1]) < 0.9, np.array([[1.0, 0, 0]]), np.array([[0, 1.0, 0]]))
+    t1 = np.cross(wm, helper)
+    t1 /= np.linalg.norm(t1, axis=-1, keepdims=True)
+    t2 = np.cross(wm, t1)
+    kap_pdf_m = np.zeros(len(wm))
+    kap_w_m = np.zeros(len(wm))
+    with np.errstate(all="ignore"):
+        for t in (t1, t2):
+            wp = wm + 4.0 * ULP * t
+            wp /= np.linalg.norm(wp, axis=-1, keepdims=True)
+            pm = om.mixture_pdf(wp, wo, ax, ay, m.mix_ratio)
+            vm = np.sum(v * wp, axis=-1)
+            pdf_p = np.where(vm > 1e-12, pm / (4.0 * vm), 0.0)
+            dv = np.maximum(vm, 0.0) * om.ndf(wp, kind, ax, ay, az) / \
+                om.projected_area(wo, kind, ax, ay, az)
+            w_p = np.where(pm > 0, dv / np.where(pm > 0, pm, 1.0), 0.0)
+            kap_pdf_m += relerr(pdf_p, pdf_r, 1e-30)
+            kap_w_m += relerr(w_p, w_r[:, 0] / np.maximum(_f(m), 1e-300), 1e-30)
     ang = angle(np.asarray(ws, dtype=np.float64), ws_r)
     tol_dir = np.maximum(1e-5, 16.0 * kap_dir)
     e_pdf = relerr(pdf_s, pdf_r, 1e-30)
     e_w = relerr(np.asarray(w)[:, 0], w_r[:, 0], 1e-30)
-    tol_pdf = np.maximum(1e-5, 64.0 * kap_pdf)
-    tol_w = np.maximum(1e-5, 64.0 * kap_w)
+    tol_pdf = np.maximum(1e-5, np.maximum(64.0 * kap_pdf, 4.0 * kap_pdf_m))
+    tol_w = np.maximum(1e-5, np.maximum(64.0 * kap_w, 4.0 * kap_w_m))
     return {
         "frac_dir_within_1e-5": float(np.mean(ang <= 1e-5)),
         "max_angle": float(ang.max()),
