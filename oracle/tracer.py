@@ -78,6 +78,17 @@ def sdf_gradient(s, p):
     raise TypeError(f"oracle has no SDF for {k}")
 
 
+# Root selection for spheres.  "reference" restates transport.py:88-91
+# exactly: t = t1 if t1 > 1e-12 else t2.  A ray that was just skipped onto
+# the level set and whose rounded position sits a hair outside it gets
+# t1 ~ 0 and is sent to the FAR root -- it tunnels through the shell (and the
+# core) and escapes.  "corrected" picks the root by the side of the level
+# sphere the ray is on (c = |p-c|^2 - R^2 > 0: first root, clamped >= 0;
+# inside: second root), which is what the math intends.  Renders of spheres
+# made with "reference" are biased; see DESIGN.md "Reference defect".
+SPHERE_ROOTS = "reference"
+
+
 def level_distance(s, pos, dirn, level):
     """transport.py:70-92: exact for plane/sphere (inf when unreachable),
     Lipschitz lower bound for boxes."""
@@ -92,8 +103,13 @@ def level_distance(s, pos, dirn, level):
             return np.full(pos.shape[:-1], np.inf)
         oc = pos - np.asarray(s.center)
         b = vdot(oc, dirn)
-        disc = b * b - (vdot(oc, oc) - rad * rad)
+        c = vdot(oc, oc) - rad * rad
+        disc = b * b - c
         sq = np.sqrt(np.maximum(disc, 0.0))
+        if SPHERE_ROOTS == "corrected":
+            outside = c > 0.0
+            t_out = np.where((b < 0.0) & (disc >= 0.0), np.maximum(-b - sq, 0.0), np.inf)
+            return np.where(outside, t_out, np.maximum(-b + sq, 0.0))
         t = np.where(-b - sq > 1e-12, -b - sq, -b + sq)
         return np.where((disc >= 0.0) & (t > 1e-12), t, np.inf)
     return np.abs(sdf_value(s, pos) - level)

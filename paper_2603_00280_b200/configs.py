@@ -66,7 +66,9 @@ def planar_scene(medium, width, height, elevation_deg=45.0, light_elev_deg=30.0,
                  film_height=1.0):
     e = math.radians(elevation_deg)
     travel = (math.cos(e), 0.0, -math.sin(e))
-    pos = (-1.0 * travel[0], 0.0, -1.0 * travel[2])  # 1 unit above the plane, looking at 0
+    # film centre 5 units back along the view axis: every ray starts well
+    # above the thickest shell of the sweep (3 sigma <= 0.6)
+    pos = (-5.0 * travel[0], 0.0, -5.0 * travel[2])
     cam = Camera(position=pos, look_at=(0.0, 0.0, 0.0), fov_deg=40.0, width=width,
                  height=height, ortho=True, film_height=film_height)
     le = math.radians(light_elev_deg)

@@ -1,0 +1,127 @@
+// mf_scene_build.h -- host-side flattening of mf_scene into the device
+// SceneDev (shared by the CUDA library and the host test shim).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "mf_prepare.h"
+#include "mf_transport.cuh"
+
+namespace mf {
+
+inline double log_ndtr_host(double u) { return std::log(0.5 * std::erfc(-u / std::sqrt(2.0))); }
+
+// max over directions of sigma(w) in the local frame (exact majorant
+// factor; replaces the direction-free bound of ndf.py:189-194)
+inline double sigma_max_host(const MediumK& m) {
+  double best = 0.0;
+  const int nt = 2048, np = 16;
+  for (int i = 0; i <= nt; ++i) {
+    double th = M_PI * i / nt;
+    for (int j = 0; j <= np; ++j) {
+      double ph = 0.5 * M_PI * j / np;
+      V3 w = v3((float)(std::sin(th) * std::cos(ph)), (float)(std::sin(th) * std::sin(ph)),
+                (float)std::cos(th));
+      best = std::max(best, (double)proj_area(m, w));
+    }
+  }
+  // the grid max of a smooth function under-estimates by O(h^2); pad
+  // generously (a majorant only needs to be an upper bound)
+  return best * 1.01 + 1e-6;
+}
+
+inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
+  if (in.n_prims < 0 || in.n_prims > MF_MAX_PRIMS)
+    return (*err = std::string("n_prims out of range"), MF_ERR_PARAM);
+  if (in.n_media < 0 || in.n_media > MF_MAX_MEDIA)
+    return (*err = std::string("n_media out of range"), MF_ERR_PARAM);
+  SceneDev sc;
+  std::memset(&sc, 0, sizeof(sc));
+  sc.n_prims = in.n_prims;
+  double min_sigma = INFINITY;
+  for (int j = 0; j < in.n_prims; ++j) {
+    PrimK pk;
+    int rc = prepare_primitive(in.prims[j], in.n_media, &pk, err);
+    if (rc) return rc;
+    MediumK mk;
+    rc = prepare_medium(in.media[pk.medium], &mk, err);
+    if (rc) return rc;
+    sc.prims[j].shape = pk.shape;
+    sc.prims[j].medium = j;
+    sc.prims[j].z0 = pk.z0;
+    sc.prims[j].c = v3(pk.cx, pk.cy, pk.cz);
+    sc.prims[j].radius = pk.radius;
+    sc.media[j] = mk;
+    double s = in.media[pk.medium].sigma;
+    min_sigma = std::min(min_sigma, s);
+    // exact majorant factor, needed only by the tracking walker (curved shells)
+    bool planar_only = in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE;
+    sc.mx[j].sig_max = planar_only ? mk.sig_bound : (float)sigma_max_host(mk);
+    sc.mx[j].lphi_hi = (float)log_ndtr_host(3.0);
+    sc.mx[j].lphi_lo_col = (float)log_ndtr_host(-6.0);
+    sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);
+  }
+  sc.min_skip = std::isfinite(min_sigma) ? (float)(1e-7 * min_sigma) : 1e-7f;
+  sc.single_plane = (in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE) ? 1 : 0;
+  // camera basis (scene.py:30-41), in double
+  const mf_camera& cam = in.camera;
+  if (cam.width < 1 || cam.height < 1) return (*err = std::string("camera size must be >= 1"), MF_ERR_PARAM);
+  double f[3] = {cam.look_at[0] - cam.position[0], cam.look_at[1] - cam.position[1],
+                 cam.look_at[2] - cam.position[2]};
+  double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  if (!(fn > 0.0)) return (*err = std::string("camera look_at equals position"), MF_ERR_PARAM);
+  for (double& v : f) v /= fn;
+  double up[3] = {0.0, 0.0, 1.0};
+  if (std::fabs(f[2]) > 0.999) {
+    up[1] = 1.0;
+    up[2] = 0.0;
+  }
+  double r[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2],
+                 f[0] * up[1] - f[1] * up[0]};
+  double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  for (double& v : r) v /= rn;
+  double tu[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+  sc.ortho = cam.ortho;
+  sc.width = cam.width;
+  sc.height = cam.height;
+  sc.cam_pos = v3((float)cam.position[0], (float)cam.position[1], (float)cam.position[2]);
+  sc.cam_fwd = v3((float)f[0], (float)f[1], (float)f[2]);
+  sc.cam_right = v3((float)r[0], (float)r[1], (float)r[2]);
+  sc.cam_up = v3((float)tu[0], (float)tu[1], (float)tu[2]);
+  double hh = cam.ortho ? 0.5 * cam.film_height : std::tan(0.5 * cam.fov_deg * M_PI / 180.0);
+  sc.half_h = (float)hh;
+  sc.half_w = (float)(hh * cam.width / cam.height);
+  sc.env = v3((float)in.env[0], (float)in.env[1], (float)in.env[2]);
+  sc.has_sun = in.has_sun;
+  if (in.has_sun) {
+    double d[3] = {in.sun_dir[0], in.sun_dir[1], in.sun_dir[2]};
+    double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (!(dn > 0.0)) return (*err = std::string("sun direction must be nonzero"), MF_ERR_PARAM);
+    sc.sun_to = v3((float)(-d[0] / dn), (float)(-d[1] / dn), (float)(-d[2] / dn));
+    sc.sun_L = v3((float)in.sun_radiance[0], (float)in.sun_radiance[1], (float)in.sun_radiance[2]);
+  }
+  sc.has_point = in.has_point;
+  if (in.has_point) {
+    sc.point_pos = v3((float)in.point_pos[0], (float)in.point_pos[1], (float)in.point_pos[2]);
+    sc.point_I = v3((float)in.point_intensity[0], (float)in.point_intensity[1],
+                    (float)in.point_intensity[2]);
+    // the light must sit outside every shell (its shadow walk is not clipped
+    // at shells containing it)
+    for (int j = 0; j < in.n_prims; ++j) {
+      const PrimDev& p = sc.prims[j];
+      V3 lp = sc.point_pos;
+      float fv = p.shape == 0 ? lp.z - p.z0
+                              : std::sqrt(dot3(sub3(lp, p.c), sub3(lp, p.c))) - p.radius;
+      if (!(fv > 3.0f * sc.media[j].sigma))
+        return (*err = std::string("point light inside a shell is not supported"), MF_ERR_UNSUPPORTED);
+    }
+  }
+  *out = sc;
+  return MF_OK;
+}
+
+
+}  // namespace mf

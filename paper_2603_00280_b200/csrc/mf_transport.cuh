@@ -94,11 +94,15 @@ MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
 }
 
 // distance along the ray to the level set f = level (transport.py:70-92);
-// +inf when never reached
+// +inf when never reached.  For spheres the side is decided by the sign of
+// c = |p - c|^2 - R^2 (outside: first root, which may round to ~0 on the
+// surface itself; inside: second root), not by a threshold on the first
+// root -- in float32 a ray sitting on the level set must not be sent to the
+// far side.
 MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
   if (p.shape == 0) {
     float t = (level - (pos.z - p.z0)) / dir.z;
-    return (t > 0.0f && t < INFINITY) ? t : INFINITY;
+    return (t >= 0.0f && t < INFINITY) ? t : INFINITY;
   }
   float rad = p.radius + level;
   if (!(rad > 0.0f)) return INFINITY;
@@ -106,11 +110,13 @@ MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
   float b = dot3(oc, dir);
   float cc = dot3(oc, oc) - rad * rad;
   float disc = b * b - cc;
-  if (disc < 0.0f) return INFINITY;
-  float sq = fsqrt(disc);
-  float t1 = -b - sq, t2 = -b + sq;
-  float t = t1 > 1e-7f * fmaxf(1.0f, fabsf(b)) ? t1 : t2;
-  return t > 0.0f ? t : INFINITY;
+  if (cc > 0.0f) {
+    // outside the level sphere: reachable only when moving towards it
+    if (b >= 0.0f || disc < 0.0f) return INFINITY;
+    return fmaxf(-b - fsqrt(disc), 0.0f);
+  }
+  // inside (or on) the level sphere: leave through the second root
+  return fmaxf(-b + fsqrt(fmaxf(disc, 0.0f)), 0.0f);
 }
 
 // ---------------------------------------------------------------------------
@@ -273,7 +279,10 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
         w.pos = pos;
         return w;
       }
-      float skip = fmaxf(gap_min, sc.min_skip);
+      // float32: step past the level set by a few ulps of |pos| so the next
+      // iteration lands inside the band (transport.py:221 uses min_skip)
+      float ulp = 4.8e-7f * (1.0f + fmaxf(fabsf(pos.x), fmaxf(fabsf(pos.y), fabsf(pos.z))));
+      float skip = fmaxf(gap_min, sc.min_skip) + ulp;
       pos = fma3(dir, skip, pos);
       travel += skip;
       continue;

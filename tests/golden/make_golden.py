@@ -14,7 +14,8 @@ Outputs (committed; the GPU box never reads /root/reference):
                      depth 1 / 16, config-4 panel means, furnace mean
   config3_ref.npz    reduced config-3 image (sphere + point light) from the
                      oracle's composed point-light loop (reference functions
-                     + the recorded NEE convention), per-pixel mean and SE
+                     + the recorded NEE convention) with the corrected
+                     sphere-root selection, per-pixel mean and SE
 """
 
 from __future__ import annotations
@@ -219,6 +220,10 @@ def make_anchors(quick=False):
 
 def _c3_job(args):
     from oracle import tracer
+
+    # the reference's sphere root selection tunnels rays through shells
+    # (DESIGN.md "Reference defect"); the fixture uses the corrected roots
+    tracer.SPHERE_ROOTS = "corrected"
 
     ys, xs, spp, tile, w = args
     scene = configs.config3_scene(w, w)

@@ -79,3 +79,35 @@ int mfh_query(const mf_medium* med, const mf_primitive* field, const float* cons
 }
 
 }  // extern "C"
+
+#include "../../paper_2603_00280_b200/csrc/mf_scene_build.h"
+
+extern "C" {
+
+// Host run of the device walker (csrc/mf_transport.cuh walk) for n rays:
+// org/dir SoA [3][n]; path i keyed (pixel = i, sample = 0, segment 0).
+// out: state[n] (0 escaped, 1 absorbed, 2 collided), pos SoA [3][n], weight[n]
+int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t n, uint64_t seed,
+             int ratio, int32_t* state, float* pos, float* weight, float majorant_scale,
+             int64_t* violations) {
+  SceneDev sc;
+  std::string err;
+  if (build_scene(*scene, &sc, &err) != MF_OK) return 1;
+  for (int j = 0; j < sc.n_prims; ++j) sc.mx[j].sig_max *= majorant_scale;
+  *violations = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    PathRng r{(uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)i, 0u};
+    V3 o = v3(org[i], org[n + i], org[2 * n + i]);
+    V3 d = v3(dir[i], dir[n + i], dir[2 * n + i]);
+    WalkResult w = walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY);
+    state[i] = w.outcome;
+    pos[i] = w.pos.x;
+    pos[n + i] = w.pos.y;
+    pos[2 * n + i] = w.pos.z;
+    weight[i] = w.weight;
+    *violations += w.violations;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -7,8 +7,9 @@ consumes exactly those values.  Where float32 cannot represent the
 problem to 1e-5 the tolerance follows the conditioning:
 
 * sigma_t: rounding u = f/sigma costs ~u^2 2^-24 relative, so
-  tol = max(1e-5, 4 u^2 2^-24); values below FLT_MIN * 1e3 in float64 only
-  need to be tiny on the device (underflow policy).
+  tol = max(1e-5, 4 u^2 2^-24) (+ 8 a^2 2^-24 for upward views, a = z/s,
+  through sigma(wo)'s e^{-a^2}); values below FLT_MIN * 1e3 in float64
+  only need to be tiny on the device (underflow policy).
 * phase value: 1e-5 relative.  pdf: 1e-5 relative, loosened to
   4 ulp / (v.h) for near-forward pairs: the pdf carries 1 / (v.h) and
   v.h = (1 + v.wi)/|v + wi| -> 0 cancels in any float32 evaluation (the
@@ -59,10 +60,23 @@ def angle(a, b):
     return np.arctan2(np.linalg.norm(np.cross(a, b), axis=-1), np.sum(a * b, axis=-1))
 
 
-def check_sigma_t(got, f, sigma, ref):
+def area_conditioning(wo_local, m):
+    """Extra relative tolerance of sigma(wo) = s/2 ierfc(a) for upward views:
+    e^{-a^2} turns the float32 rounding of a = z/s into ~2 a^2 ulps."""
+    w = np.asarray(wo_local, dtype=np.float64)
+    kind = getattr(m.kind, "value", m.kind)
+    az = m.a3.az if kind == "generalized" else 0.0
+    s = np.sqrt((m.a3.ax * w[..., 0]) ** 2 + (m.a3.ay * w[..., 1]) ** 2 + (az * w[..., 2]) ** 2)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        a = np.where(s > 0, w[..., 2] / np.maximum(s, 1e-300), 0.0)
+    a = np.where(a > 0, np.minimum(a, 1e3), 0.0)
+    return 8.0 * a * a * ULP
+
+
+def check_sigma_t(got, f, sigma, ref, extra=0.0):
     u = np.asarray(f, dtype=np.float64) / sigma
     tiny = ref < FLT_MIN * 1e3
-    tol = np.maximum(1e-5, 4.0 * u * u * ULP)
+    tol = np.maximum(1e-5, 4.0 * u * u * ULP) + extra
     e = relerr(got, ref)
     bad_big = ~tiny & (e > tol)
     bad_tiny = tiny & (np.asarray(got, dtype=np.float64) > FLT_MIN * 1e4)
