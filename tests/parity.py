@@ -84,13 +84,18 @@ def check_sigma_t(got, f, sigma, ref, extra=0.0):
             "n_bad": int(bad_big.sum() + bad_tiny.sum()), "n": int(len(e))}
 
 
-def pdf_tolerance(wo, wi):
-    """Per-query pdf tolerance: max(1e-5, 4 ulp / (v.h))."""
+def pdf_tolerance(wo, wi, m=None):
+    """Per-query pdf tolerance: max(1e-5, 4 ulp / (v.h)) (+ the Beckmann
+    projected-area conditioning of sigma_b(wo), ndf.py:387-400)."""
     v = -np.asarray(wo, dtype=np.float64)
     h = v + np.asarray(wi, dtype=np.float64)
     h /= np.maximum(np.linalg.norm(h, axis=-1, keepdims=True), 1e-300)
     vh = np.abs(np.sum(v * h, axis=-1))
-    return np.maximum(1e-5, 4.0 * ULP / np.maximum(vh, 1e-300))
+    extra = 0.0
+    if m is not None:
+        beck = Obj(kind="beckmann", a3=Obj(ax=m.a3.ax, ay=m.a3.ay, az=0.0))
+        extra = area_conditioning(wo, beck)
+    return np.maximum(1e-5, 4.0 * ULP / np.maximum(vh, 1e-300)) + extra
 
 
 def phase_tolerance(wo, wi, m):
@@ -108,7 +113,8 @@ def phase_tolerance(wo, wi, m):
                                                      1e-300)
     kind = getattr(m.kind, "value", m.kind)
     e = e_beck if kind == "beckmann" else e_gen
-    return np.maximum(1e-5, 4.0 * ULP * (1.0 + np.minimum(e, 1e6)))
+    # the vNDF divides by sigma(wo) (ndf.py:315), whose e^{-a^2} conditions it
+    return np.maximum(1e-5, 4.0 * ULP * (1.0 + np.minimum(e, 1e6))) + area_conditioning(wo, m)
 
 
 def check_rel(got, ref, tol=1e-5, floor=1e-30):
