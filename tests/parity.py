@@ -99,7 +99,7 @@ def pdf_tolerance(wo, wi, m=None):
 
 
 def phase_tolerance(wo, wi, m):
-    """max(1e-5, 4 ulp (1 + E)), E the NDF exponent at the half vector: the
+    """max(1e-5, 8 ulp (1 + E)), E the NDF exponent at the half vector: the
     Beckmann e^{-E} (ndf.py:85-94) and the generalized e^{r - c}
     (ndf.py:216-222) turn the float32 rounding of h into ~E ulps."""
     v = -np.asarray(wo, dtype=np.float64)
@@ -114,7 +114,7 @@ def phase_tolerance(wo, wi, m):
     kind = getattr(m.kind, "value", m.kind)
     e = e_beck if kind == "beckmann" else e_gen
     # the vNDF divides by sigma(wo) (ndf.py:315), whose e^{-a^2} conditions it
-    return np.maximum(1e-5, 4.0 * ULP * (1.0 + np.minimum(e, 1e6))) + area_conditioning(wo, m)
+    return np.maximum(1e-5, 8.0 * ULP * (1.0 + np.minimum(e, 1e6))) + area_conditioning(wo, m)
 
 
 def check_rel(got, ref, tol=1e-5, floor=1e-30):
