@@ -16,7 +16,8 @@ from .errors import (DegenerateVisibilityError, InternalConsistencyError, Macrof
                      NumericFailureError, ParameterDomainError, UnsupportedGeometryError)
 
 LIB_NAME = "libmacrofacet_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("MF_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 MF_MAX_PRIMS = 8
 MF_MAX_MEDIA = 8

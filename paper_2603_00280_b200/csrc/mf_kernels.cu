@@ -48,6 +48,12 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kBlock = 128;
+// resident blocks per SM the path kernel is compiled for (register cap
+// 65536 / (kBlock * kMinBlocks))
+#ifndef MF_MIN_BLOCKS
+#define MF_MIN_BLOCKS 8
+#endif
+constexpr int kMinBlocks = MF_MIN_BLOCKS;
 
 enum StatIdx {
   kStPaths = 0,
@@ -291,7 +297,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
 }
 
 template <bool kPlanar, bool kCallerRays>
-__global__ void __launch_bounds__(kBlock) path_kernel(const __grid_constant__ SceneDev sc,
+__global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_constant__ SceneDev sc,
                                                        const __grid_constant__ PassDev ps) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;

@@ -1,0 +1,28 @@
+"""Time config-2 / config-3 renders for library variants given as args."""
+import os, subprocess, sys, json
+here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+code = r'''
+import sys, os, json
+sys.path.insert(0, %r)
+import torch, numpy as np
+import paper_2603_00280_b200 as mf
+from paper_2603_00280_b200 import configs
+torch.cuda.set_device(0)
+def tm(scene, spp, seed, mb, reps=10):
+    out = torch.empty((scene.camera.height, scene.camera.width, 3), device="cuda")
+    for _ in range(3): mf.render_device(scene, spp, seed, max_bounces=mb, out=out)
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        s.record(); mf.render_device(scene, spp, seed, max_bounces=mb, out=out); e.record(); torch.cuda.synchronize(); ts.append(s.elapsed_time(e))
+    return min(ts), float(out.mean())
+c2 = configs.config2_scene(); c3 = configs.config3_scene(256, 256)
+t2, m2 = tm(c2, 64, 1, 16); t3, m3 = tm(c3, 64, 2, 32, reps=5)
+_, st = mf.render_device(c2, 64, 1, max_bounces=16, stats=True)
+print(json.dumps({"c2_ms": t2, "c2_Mpaths_s": 256*256*64/t2/1e3, "c2_mean": m2, "c3_ms": t3, "c3_Mpaths_s": 256*256*64/t3/1e3, "c3_mean": m3, "slope_iters_per_path": st["slope_iters"]/st["paths"]}))
+''' % here
+for so in sys.argv[1:]:
+    env = dict(os.environ, MF_LIB_PATH=os.path.abspath(so))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    print(os.path.basename(so), r.stdout.strip() or r.stderr[-2000:], flush=True)
