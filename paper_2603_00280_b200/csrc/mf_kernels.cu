@@ -51,7 +51,7 @@ constexpr int kBlock = 128;
 // resident blocks per SM the path kernel is compiled for (register cap
 // 65536 / (kBlock * kMinBlocks))
 #ifndef MF_MIN_BLOCKS
-#define MF_MIN_BLOCKS 8
+#define MF_MIN_BLOCKS 6
 #endif
 constexpr int kMinBlocks = MF_MIN_BLOCKS;
 
@@ -87,7 +87,13 @@ struct QueryArgs {
 
 __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ QueryArgs a) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+  // every lane of a warp runs the same number of trips (so the sampler's
+  // re-convergence mask is well defined); lanes past n are predicated off
+  int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t w0 = first; w0 < a.n; w0 += stride) {
+    int64_t i = w0 + (threadIdx.x & 31);
+    unsigned qmask = __ballot_sync(0xffffffffu, i < a.n);
+    if (i >= a.n) continue;
     V3 p = v3(__ldg(a.in.px + i), __ldg(a.in.py + i), __ldg(a.in.pz + i));
     V3 wo = v3(__ldg(a.in.wox + i), __ldg(a.in.woy + i), __ldg(a.in.woz + i));
     V3 wi = v3(__ldg(a.in.wix + i), __ldg(a.in.wiy + i), __ldg(a.in.wiz + i));
@@ -102,7 +108,8 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Quer
     } else {
       fr = frame_about(fp.n);
     }
-    QueryResult q = query_local(a.m, fp.f, fr, wo, wi, __ldg(a.in.u1 + i), __ldg(a.in.u2 + i));
+    QueryResult q = query_local(a.m, fp.f, fr, wo, wi, __ldg(a.in.u1 + i), __ldg(a.in.u2 + i),
+                                qmask);
     const mf_query_out& o = a.out;
     if (o.sigma_t) o.sigma_t[i] = q.sigma_t;
     if (o.phase_r) o.phase_r[i] = q.phase.x;
@@ -196,73 +203,82 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
 
 // One free-flight segment plus the scattering event at its end.
 // Returns true when the path has terminated.
+//
+// SIMT structure: a single exit and explicit warp re-convergence
+// (__syncwarp over the lanes that entered, `amask`) after each stage --
+// flight, NEE, phase sampling.  Without it the lanes that escape / take
+// the other mixture branch are not re-joined until the function ends and
+// every later stage runs once per lane group (measured: 5.6 active lanes
+// per warp instruction).  Finished lanes stay predicated off inside the
+// stages but still pass every barrier.
 template <bool kPlanar>
 __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& ps, PathState& st,
-                                             Counters& cn) {
+                                             Counters& cn, unsigned amask) {
   cn.v[kStSegments]++;
   U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
   float u_fl = u01(b.x), u_br = u01(b.y), u_s2 = u01(b.z), u_rr = u01(b.w);
-  int k;
-  V3 pos;
+  int k = 0;
+  V3 pos = st.pos;
+  bool done = false;
+  // ---- stage 1: free flight (transport.py:144-297)
   if (kPlanar) {
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl);
-    if (fl.outcome == kEscaped) {
-      st.L = fma3(v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z), 1.0f, st.L);
-      cn.v[kStEscaped]++;
-      return true;
-    }
-    if (fl.outcome == kAbsorbed) {
-      cn.v[kStAbsorbed]++;
-      return true;
-    }
-    k = 0;
     pos = fl.pos;
+    if (fl.outcome == kEscaped) {
+      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
+      cn.v[kStEscaped]++;
+      done = true;
+    } else if (fl.outcome == kAbsorbed) {
+      cn.v[kStAbsorbed]++;
+      done = true;
+    }
   } else {
     WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false, INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
+    pos = w.pos;
+    k = max(w.prim, 0);
     if (w.steps < 0) {
       cn.v[kStCapped]++;
-      return true;
-    }
-    if (w.outcome == kEscaped) {
+      done = true;
+    } else if (w.outcome == kEscaped) {
       st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
       cn.v[kStEscaped]++;
-      return true;
-    }
-    if (w.outcome == kAbsorbed) {
+      done = true;
+    } else if (w.outcome == kAbsorbed) {
       cn.v[kStAbsorbed]++;
-      return true;
+      done = true;
     }
-    k = w.prim;
-    pos = w.pos;
   }
-  cn.v[kStScatters]++;
+  __syncwarp(amask);
   const PrimDev& pr = sc.prims[k];
   const MediumK& m = sc.media[k];
   Frame fr = frame_about(kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(pr, pos));
   V3 wo = to_local(fr, st.dir);
   float sig_o = proj_area(m, wo);
-  if (!(sig_o >= 1e-12f)) {
-    cn.v[kStDegenerate]++;
-    return true;
+  if (!done) {
+    cn.v[kStScatters]++;
+    if (!(sig_o >= 1e-12f)) {
+      cn.v[kStDegenerate]++;
+      done = true;
+    }
   }
-  // next-event estimation (render.py:71-82; point light: BASELINE extension)
-  if (sc.has_sun) {
+  // ---- stage 2: next-event estimation (render.py:71-82; point light:
+  //      BASELINE extension)
+  if (!done && sc.has_sun) {
     V3 wl = to_local(fr, sc.sun_to);
     V3 ph = phase_eval(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr(sc, st, pos, sc.sun_to, INFINITY,
                            sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn);
-      float s = tr;
-      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * s, st.T.y * ph.y * sc.sun_L.y * s,
-                           st.T.z * ph.z * sc.sun_L.z * s));
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
+                           st.T.z * ph.z * sc.sun_L.z * tr));
     }
   }
-  if (sc.has_point) {
+  if (!done && sc.has_point) {
     V3 d = sub3(sc.point_pos, pos);
     float r2 = dot3(d, d);
     float ir = frsqrt(r2);
@@ -277,23 +293,31 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
                            st.T.z * ph.z * sc.point_I.z * s));
     }
   }
-  // phase sampling (render.py:84-90), two-uniform branch convention
-  float sig_b = proj_area_erf(wo, m.ax, m.ay, 0.0f);
-  float uu = remap_branch_uniform(u_br, m.mix);
-  PhaseSample s = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2);
-  cn.v[kStSlopeIters] += (uint32_t)s.iters;
-  st.dir = to_world(fr, s.wi);
-  st.T = v3(st.T.x * s.weight.x, st.T.y * s.weight.y, st.T.z * s.weight.z);
-  st.pos = pos;
-  st.bounce++;
-  if (st.bounce >= ps.max_bounces) return true;  // render.py:92-94
-  if (st.bounce > 8) {                            // render.py:96-105
-    float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
-    if (u_rr >= q) return true;
-    float iq = 1.0f / q;
-    st.T = mul3(st.T, iq);
+  __syncwarp(amask);
+  // ---- stage 3: phase sampling (render.py:84-90), two-uniform convention
+  unsigned smask = __ballot_sync(amask, !done);
+  if (!done) {
+    float sig_b = proj_area_erf(wo, m.ax, m.ay, 0.0f);
+    float uu = remap_branch_uniform(u_br, m.mix);
+    PhaseSample smp = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2, smask);
+    cn.v[kStSlopeIters] += (uint32_t)smp.iters;
+    st.dir = to_world(fr, smp.wi);
+    st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
+    st.pos = pos;
+    st.bounce++;
+    if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+      done = true;
+    } else if (st.bounce > 8) {                    // render.py:96-105
+      float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+      if (u_rr >= q) {
+        done = true;
+      } else {
+        st.T = mul3(st.T, 1.0f / q);
+      }
+    }
   }
-  return false;
+  __syncwarp(amask);
+  return done;
 }
 
 template <bool kPlanar, bool kCallerRays>
@@ -354,8 +378,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
       if (__ballot_sync(full, !exhausted) == 0) break;
       continue;
     }
+    unsigned amask = __ballot_sync(full, active);
     if (active) {
-      if (path_segment<kPlanar>(sc, ps, st, cn)) {
+      if (path_segment<kPlanar>(sc, ps, st, cn, amask)) {
         float r = st.L.x, g = st.L.y, bl = st.L.z;
         if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
           cn.v[kStNonfinite]++;

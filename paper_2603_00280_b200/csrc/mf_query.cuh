@@ -67,7 +67,7 @@ struct QueryResult {
 };
 
 MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo, V3 wi, float u1,
-                              float u2);
+                              float u2, unsigned mask = 0xffffffffu);
 
 MF_HD QueryResult query_point(const MediumK& m, int shape, float z0, V3 c, float radius, V3 p,
                               V3 wo, V3 wi, float u1, float u2) {
@@ -76,7 +76,7 @@ MF_HD QueryResult query_point(const MediumK& m, int shape, float z0, V3 c, float
 }
 
 MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo, V3 wi, float u1,
-                              float u2) {
+                              float u2, unsigned mask) {
   QueryResult q;
   V3 wol = to_local(fr, wo);
   V3 wil = to_local(fr, wi);
@@ -85,24 +85,27 @@ MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo,
   float sig_b = proj_area_erf(wol, m.ax, m.ay, 0.0f);
   q.flags = 0;
   q.iters = 0;
-  if (!(sig_o >= 1e-12f)) {
-    // the reference raises DegenerateVisibilityError here (ndf.py:312-313)
+  // the reference raises DegenerateVisibilityError where sigma(wo) < 1e-12
+  // (ndf.py:312-313): flagged, outputs zero.  Evaluated branch-free so the
+  // sampler's warp mask stays the full set of lanes that entered.
+  bool degenerate = !(sig_o >= 1e-12f);
+  float sig_safe = degenerate ? 1.0f : sig_o;
+  q.phase = phase_eval(m, wol, wil, sig_safe);
+  q.pdf = phase_pdf(m, wol, wil, sig_b);
+  float uu = remap_branch_uniform(u1, m.mix);
+  PhaseSample s = phase_sample(m, wol, sig_safe, sig_b, u1, uu, u2, mask);
+  q.ws = to_world(fr, s.wi);
+  q.pdf_s = s.pdf;
+  q.w = s.weight;
+  q.iters = s.iters;
+  if (degenerate) {
     q.flags = 1;
     q.phase = v3(0.0f, 0.0f, 0.0f);
     q.pdf = 0.0f;
     q.ws = wo;
     q.pdf_s = 0.0f;
     q.w = v3(0.0f, 0.0f, 0.0f);
-    return q;
   }
-  q.phase = phase_eval(m, wol, wil, sig_o);
-  q.pdf = phase_pdf(m, wol, wil, sig_b);
-  float uu = remap_branch_uniform(u1, m.mix);
-  PhaseSample s = phase_sample(m, wol, sig_o, sig_b, u1, uu, u2);
-  q.ws = to_world(fr, s.wi);
-  q.pdf_s = s.pdf;
-  q.w = s.weight;
-  q.iters = s.iters;
   return q;
 }
 
