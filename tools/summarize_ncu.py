@@ -1,0 +1,114 @@
+"""Summarise ncu captures into profiles/ (tracked).
+
+    python tools/summarize_ncu.py <round_tag> <full.ncu-rep> [launches.csv] [sass_lines_dis]
+
+Writes profiles/<tag>_path_kernel.json (key metrics of the top kernel, DRAM
+bytes per launch, pipe utilisation), profiles/<tag>_launches.json (per-kernel
+share of the step from the gpu__time_duration launch list) and refreshes
+profiles/ncu_path_kernel.json (read by bench.py for roofline.traffic)."""
+
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "smsp__inst_executed.sum", "smsp__thread_inst_executed.sum",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed_pipe_fma.sum", "smsp__inst_executed_pipe_xu.sum",
+    "smsp__inst_executed_pipe_alu.sum",
+    "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
+]
+
+
+def raw_metrics(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6,
+             "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        k = {"kernel": d.get("Kernel Name", "")}
+        for m in METRICS:
+            if m not in d:
+                continue
+            v = to_num(d[m])
+            u = units.get(m, "")
+            if isinstance(v, float) and u in scale:
+                v *= scale[u]
+                m = m + (" [ms]" if "second" in u else " [bytes]")
+            k[m] = v
+        res.append(k)
+    return res
+
+
+def to_num(v):
+    try:
+        return float(str(v).replace(",", ""))
+    except (TypeError, ValueError):
+        return v
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, mi, mn = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    agg = {}
+    for r in rows[1:]:
+        if r[mn] != "gpu__time_duration.sum":
+            continue
+        k = r[ki].split("(")[0]
+        a = agg.setdefault(k, [0, 0.0])
+        a[0] += 1
+        a[1] += to_num(r[mi])
+    tot = sum(a[1] for a in agg.values())
+    return {k: {"launches": a[0], "total_ns": a[1], "mean_ns": a[1] / a[0], "share": a[1] / tot}
+            for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
+
+
+def main():
+    tag, rep = sys.argv[1], sys.argv[2]
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    kernels = raw_metrics(rep)
+    summ = []
+    for k in kernels:
+        d = {m: to_num(v) for m, v in k.items()}
+        if d.get("dram__bytes_read.sum [bytes]") is not None:
+            d["dram_bytes_per_launch"] = (d.get("dram__bytes_read.sum [bytes]") or 0) + \
+                (d.get("dram__bytes_write.sum [bytes]") or 0)
+        summ.append(d)
+    out = {"source": os.path.basename(rep), "kernels": summ}
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    path_k = [d for d in summ if "path_kernel" in d["kernel"]]
+    if path_k:
+        with open(os.path.join(ROOT, "profiles", "ncu_path_kernel.json"), "w") as fh:
+            json.dump({"round": tag, **path_k[0]}, fh, indent=1)
+    if len(sys.argv) > 3 and os.path.exists(sys.argv[3]):
+        with open(os.path.join(ROOT, "profiles", f"{tag}_launches.json"), "w") as fh:
+            json.dump(launches(sys.argv[3]), fh, indent=1)
+    print(json.dumps(out, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main()
