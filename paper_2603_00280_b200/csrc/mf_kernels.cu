@@ -444,6 +444,14 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
 }
 
 // ---------------------------------------------------------------------------
+// visible-slope guess table (built once per device by the solver itself)
+
+__global__ void __launch_bounds__(128) slope_table_kernel(float* tab) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < kTabNT * kTabNU) tab[k] = slope_table_node(k / kTabNU, k % kTabNU);
+}
+
+// ---------------------------------------------------------------------------
 // roofline microbenchmarks: 8 independent FFMA chains / 4 MUFU.EX2 chains
 
 __global__ void __launch_bounds__(256) peak_ffma_kernel(float* out, int iters, float a, float b) {
@@ -477,6 +485,35 @@ __global__ void __launch_bounds__(256) peak_mufu_kernel(float* out, int iters) {
 
 // ---------------------------------------------------------------------------
 // host side
+
+// device pointer of this device's slope table (built on first use)
+int slope_table(const float** out, cudaStream_t st) {
+  static std::mutex mu;
+  static float* tabs[64] = {nullptr};
+  int dev = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 64) return fail(MF_ERR_CUDA, "device index out of range");
+  if (!tabs[dev]) {
+    float* t = nullptr;
+    MF_CUDA(cudaMalloc((void**)&t, (size_t)kTabNT * kTabNU * sizeof(float)));
+    slope_table_kernel<<<(kTabNT * kTabNU + 127) / 128, 128, 0, st>>>(t);
+    g_launches++;
+    MF_CUDA(cudaGetLastError());
+    MF_CUDA(cudaStreamSynchronize(st));
+    tabs[dev] = t;
+  }
+  *out = tabs[dev];
+  return MF_OK;
+}
+
+int attach_slope_table(SceneDev* sc, cudaStream_t st) {
+  const float* tab = nullptr;
+  int rc = slope_table(&tab, st);
+  if (rc) return rc;
+  for (int j = 0; j < kMaxPrims; ++j) sc->media[j].slope_tab = tab;
+  return MF_OK;
+}
 
 struct Occupancy {
   int sms = 0;
@@ -657,6 +694,12 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
   a.out = *d_out;
   a.n = n;
   if (n == 0) return MF_OK;
+  {
+    const float* tab = nullptr;
+    rc = slope_table(&tab, (cudaStream_t)stream);
+    if (rc) return rc;
+    a.m.slope_tab = tab;
+  }
   const float* req[] = {a.in.px, a.in.py, a.in.pz, a.in.wox, a.in.woy, a.in.woz,
                         a.in.wix, a.in.wiy, a.in.wiz, a.in.u1, a.in.u2};
   for (const float* p : req)
@@ -688,6 +731,8 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   std::string berr;
   int rc = build_scene(*scene, &sc, &berr);
   if (rc) return fail(rc, berr);
+  rc = attach_slope_table(&sc, (cudaStream_t)stream);
+  if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   size_t npix = (size_t)sc.width * sc.height;
   if (!p.accumulate) MF_CUDA(cudaMemsetAsync(d_accum, 0, npix * 3 * sizeof(float), st));
@@ -788,6 +833,8 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
   std::string berr;
   int rc = build_scene(*scene, &sc, &berr);
   if (rc) return fail(rc, berr);
+  rc = attach_slope_table(&sc, (cudaStream_t)stream);
+  if (rc) return rc;
   if (n == 0) {
     if (stats) std::memset(stats, 0, sizeof(*stats));
     return MF_OK;
@@ -833,6 +880,8 @@ int mf_transmittance(const mf_scene* scene, const double origin[3], const double
   std::string berr;
   int rc = build_scene(*scene, &sc, &berr);
   if (rc) return fail(rc, berr);
+  rc = attach_slope_table(&sc, (cudaStream_t)stream);
+  if (rc) return rc;
   double dn = std::sqrt(direction[0] * direction[0] + direction[1] * direction[1] +
                         direction[2] * direction[2]);
   if (!(dn > 0.0)) return fail(MF_ERR_PARAM, "direction must be nonzero");

@@ -10,6 +10,19 @@
 
 using namespace mf;
 
+#include <vector>
+
+// host copy of the device slope table (built on first use, same code)
+static const float* host_slope_table() {
+  static std::vector<float> tab;
+  if (tab.empty()) {
+    tab.resize((size_t)kTabNT * kTabNU);
+    for (int i = 0; i < kTabNT; ++i)
+      for (int j = 0; j < kTabNU; ++j) tab[(size_t)i * kTabNU + j] = slope_table_node(i, j);
+  }
+  return tab.data();
+}
+
 extern "C" {
 
 // which: 0 erfcx, 1 ierfcx, 2 bterm, 3 erfc, 4 ndtri, 5 mills, 6 log_ndtr,
@@ -35,9 +48,10 @@ int mfh_special(int which, const float* x, float* out, int64_t n) {
 }
 
 int mfh_slope(const float* nu, const float* u1, float* x, int32_t* iters, int64_t n) {
+  const float* tab = host_slope_table();
   for (int64_t i = 0; i < n; ++i) {
     int it = 0;
-    x[i] = visible_slope_x(nu[i], u1[i], &it);
+    x[i] = visible_slope_x(nu[i], u1[i], &it, tab, atan2f(1.0f, nu[i]));
     iters[i] = it;
   }
   return 0;
@@ -51,6 +65,7 @@ int mfh_query(const mf_medium* med, const mf_primitive* field, const float* cons
   MediumK m;
   std::string err;
   if (prepare_medium(*med, &m, &err) != MF_OK) return 1;
+  m.slope_tab = host_slope_table();
   V3 c = v3((float)field->center[0], (float)field->center[1], (float)field->center[2]);
   for (int64_t i = 0; i < n; ++i) {
     V3 p = v3(in[0][i], in[1][i], in[2][i]);
@@ -93,6 +108,7 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
   SceneDev sc;
   std::string err;
   if (build_scene(*scene, &sc, &err) != MF_OK) return 1;
+  for (int j = 0; j < kMaxPrims; ++j) sc.media[j].slope_tab = host_slope_table();
   for (int j = 0; j < sc.n_prims; ++j) sc.mx[j].sig_max *= majorant_scale;
   *violations = 0;
   for (int64_t i = 0; i < n; ++i) {
