@@ -189,10 +189,11 @@ __device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t pixel, f
 
 // shadow transmittance from pos towards unit direction wl over distance t_max
 __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& st, V3 pos, V3 wl,
-                                           float t_max, float h_end, Counters& cn) {
+                                           float t_max, float h_end, Counters& cn,
+                                           float sig_known = -1.0f) {
   if (sc.single_plane) {
     const MediumK& m = sc.media[0];
-    float sig = proj_area(m, wl);
+    float sig = sig_known >= 0.0f ? sig_known : proj_area(m, wl);
     return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig);
   }
   WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max);
@@ -220,10 +221,12 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
   int k = 0;
   V3 pos = st.pos;
   bool done = false;
+  float sig_dir = 0.0f;   // sigma(dir): in the plane frame this is sigma(wo)
   // ---- stage 1: free flight (transport.py:144-297)
   if (kPlanar) {
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
+    sig_dir = sig;
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl);
     pos = fl.pos;
     if (fl.outcome == kEscaped) {
@@ -257,7 +260,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
   const MediumK& m = sc.media[k];
   Frame fr = frame_about(kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(pr, pos));
   V3 wo = to_local(fr, st.dir);
-  float sig_o = proj_area(m, wo);
+  float sig_o = kPlanar ? sig_dir : proj_area(m, wo);
   if (!done) {
     cn.v[kStScatters]++;
     if (!(sig_o >= 1e-12f)) {
@@ -273,7 +276,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr(sc, st, pos, sc.sun_to, INFINITY,
-                           sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn);
+                           sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
     }
@@ -297,7 +300,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
   // ---- stage 3: phase sampling (render.py:84-90), two-uniform convention
   unsigned smask = __ballot_sync(amask, !done);
   if (!done) {
-    float sig_b = proj_area_erf(wo, m.ax, m.ay, 0.0f);
+    float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
     float uu = remap_branch_uniform(u_br, m.mix);
     PhaseSample smp = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2, smask);
     cn.v[kStSlopeIters] += (uint32_t)smp.iters;

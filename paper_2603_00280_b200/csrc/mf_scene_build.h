@@ -102,6 +102,7 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     if (!(dn > 0.0)) return (*err = std::string("sun direction must be nonzero"), MF_ERR_PARAM);
     sc.sun_to = v3((float)(-d[0] / dn), (float)(-d[1] / dn), (float)(-d[2] / dn));
     sc.sun_L = v3((float)in.sun_radiance[0], (float)in.sun_radiance[1], (float)in.sun_radiance[2]);
+    if (sc.n_prims > 0) sc.sun_sig = proj_area(sc.media[0], sc.sun_to);
   }
   sc.has_point = in.has_point;
   if (in.has_point) {

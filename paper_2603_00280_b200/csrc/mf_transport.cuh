@@ -53,6 +53,7 @@ struct SceneDev {
   int has_sun;
   V3 sun_to;           // unit direction towards the sun (= -DirectionalLight.direction)
   V3 sun_L;
+  float sun_sig;       // sigma(sun_to) in the plane frame (single-plane scenes)
   int has_point;
   V3 point_pos;
   V3 point_I;
