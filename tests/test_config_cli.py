@@ -1,0 +1,54 @@
+"""Config schema and CLI (CPU only; rendering itself is covered on the GPU)."""
+
+import math
+
+import pytest
+
+import paper_2603_00280_b200 as mf
+from paper_2603_00280_b200 import cli, configs
+from paper_2603_00280_b200.config import (config_hash, parse_config, scene_from_config,
+                                          serialize_config)
+
+from conftest import ROOT
+
+
+def test_config_round_trip_and_errors():
+    text = open(f"{ROOT}/configs/config2.cfg").read()
+    v = parse_config(text)
+    assert parse_config(serialize_config(v)) == v
+    assert len(config_hash(v)) == 16
+    with pytest.raises(mf.ConfigError):
+        parse_config("[kernel]\nsigma = 1\nlx = 1\nax = 1\n")      # config.py:102-106
+    with pytest.raises(mf.ConfigError):
+        parse_config("[nope]\n")
+    with pytest.raises(mf.ConfigError):
+        parse_config("[render]\nwidth = 1\nwidth = 2\n")
+    with pytest.raises(mf.ConfigError):
+        parse_config("[scene]\nprimitive0_colour = red\n")
+
+
+def test_configs_match_the_baseline_scenes():
+    s2 = scene_from_config(parse_config(open(f"{ROOT}/configs/config2.cfg").read()))
+    ref2 = configs.config2_scene()
+    assert s2.camera.ortho and s2.camera.width == 256
+    for a, b in zip(s2.camera.position, ref2.camera.position):
+        assert abs(a - b) < 1e-12
+    m2, r2 = s2.primitives[0].medium, ref2.primitives[0].medium
+    assert m2.kind == r2.kind and abs(m2.a3.ax - r2.a3.ax) < 1e-15 and m2.albedo == r2.albedo
+    for a, b in zip(s2.sun.direction, ref2.sun.direction):
+        assert abs(a - b) < 1e-12
+    s3 = scene_from_config(parse_config(open(f"{ROOT}/configs/config3.cfg").read()))
+    assert isinstance(s3.primitives[0].sdf, mf.Sphere) and s3.point.intensity == (10.0,) * 3
+    lz_inf = parse_config("[kernel]\nsigma = 0.05\nlx = 0.05\nly = 0.05\nlz = inf\n")
+    m = scene_from_config(lz_inf).primitives[0].medium
+    assert m.kind is mf.NdfKind.BECKMANN and m.a3.az == 0.0
+    assert abs(m.a3.ax - math.sqrt(2)) < 1e-12
+
+
+def test_cli_exit_codes(tmp_path, capsys):
+    # cli.py:324-343 exit codes: config error 1, I/O error 3
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("[kernel]\nnonsense = 1\n")
+    assert cli.main(["render", str(bad), "--out", str(tmp_path / "x.pfm")]) == 1
+    assert cli.main(["render", str(tmp_path / "missing.cfg"), "--out", "x.pfm"]) == 3
+    assert cli.main(["bogus"]) == 1
