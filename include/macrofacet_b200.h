@@ -60,8 +60,9 @@ typedef struct mf_medium {
   double albedo[3];
 } mf_medium;
 
-/* SDF primitives (sdf.py:18-52) */
-enum mf_shape { MF_SHAPE_PLANE = 0, MF_SHAPE_SPHERE = 1 };
+/* SDF primitives (sdf.py:18-52); MF_SHAPE_GRID is the BASELINE config-5
+ * extension: the scene's mf_grid_field (trilinear SDF + per-voxel sigma) */
+enum mf_shape { MF_SHAPE_PLANE = 0, MF_SHAPE_SPHERE = 1, MF_SHAPE_GRID = 2 };
 
 /* ShellPrimitive (scene.py:99-101): one shape bound to media[medium] */
 typedef struct mf_primitive {
@@ -87,6 +88,21 @@ typedef struct mf_camera {
 #define MF_MAX_PRIMS 8
 #define MF_MAX_MEDIA 8
 
+/* Heterogeneous GP field (BASELINE config 5; not in the reference): mean =
+ * trilinear SDF grid, per-point sigma = trilinear sigma grid, roughness
+ * alpha_xy = sqrt2 sigma / l_xy, alpha_z = sqrt2 sigma / l_z.  Grids are
+ * device float32, vertex-centred over [bmin, bmax], index (ix*n + iy)*n + iz.
+ * d_majorant: n_maj^3 cell bounds of the extinction built by
+ * mf_grid_majorant. */
+typedef struct mf_grid_field {
+  const float* d_sdf;
+  const float* d_sigma;
+  const float* d_majorant;
+  int32_t n_sdf, n_sigma, n_maj;
+  double bmin[3], bmax[3];
+  double l_xy, l_z;
+} mf_grid_field;
+
 /* ShellScene (scene.py:104-129) + lights.  sun_dir is the direction the
  * light travels (DirectionalLight, scene.py:87-96); the point light
  * (position, intensity, NEE weight I/r^2) is a BASELINE-config extension. */
@@ -103,6 +119,8 @@ typedef struct mf_scene {
   int32_t has_point;
   double point_pos[3];
   double point_intensity[3];
+  int32_t has_grid;   /* the single MF_SHAPE_GRID primitive uses `grid` */
+  mf_grid_field grid;
 } mf_scene;
 
 /* Sharding of one render across ranks. */
@@ -199,6 +217,13 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
 int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],
                      int64_t n, uint64_t seed, uint64_t stream_id, double* mean, double* se,
                      void* stream);
+
+/* Build the majorant grid of a grid field: for every one of the n_maj^3
+ * cells an upper bound of the extinction over the cell and over all
+ * directions (exact min/max of the trilinear SDF and sigma over the cell's
+ * vertices; max over sigma samples and directions of rho * sigma_proj).
+ * Writes d_majorant_out (n_maj^3 floats). */
+int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* stream);
 
 /* Issue-rate peaks of this device measured by microbenchmark kernels
  * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane

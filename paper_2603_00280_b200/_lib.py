@@ -24,7 +24,7 @@ MF_MAX_MEDIA = 8
 
 KIND = {"beckmann": 0, "ggx": 1, "generalized": 2}
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
-SHAPE_PLANE, SHAPE_SPHERE = 0, 1
+SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID = 0, 1, 2
 SHARD_TILES, SHARD_SAMPLES = 0, 1
 
 _d3 = ctypes.c_double * 3
@@ -48,12 +48,20 @@ class MfCamera(ctypes.Structure):
                 ("film_height", ctypes.c_double)]
 
 
+class MfGridField(ctypes.Structure):
+    _fields_ = [("d_sdf", ctypes.c_void_p), ("d_sigma", ctypes.c_void_p),
+                ("d_majorant", ctypes.c_void_p), ("n_sdf", ctypes.c_int32),
+                ("n_sigma", ctypes.c_int32), ("n_maj", ctypes.c_int32), ("bmin", _d3),
+                ("bmax", _d3), ("l_xy", ctypes.c_double), ("l_z", ctypes.c_double)]
+
+
 class MfScene(ctypes.Structure):
     _fields_ = [("n_prims", ctypes.c_int32), ("n_media", ctypes.c_int32),
                 ("prims", MfPrimitive * MF_MAX_PRIMS), ("media", MfMedium * MF_MAX_MEDIA),
                 ("camera", MfCamera), ("env", _d3),
                 ("has_sun", ctypes.c_int32), ("sun_dir", _d3), ("sun_radiance", _d3),
-                ("has_point", ctypes.c_int32), ("point_pos", _d3), ("point_intensity", _d3)]
+                ("has_point", ctypes.c_int32), ("point_pos", _d3), ("point_intensity", _d3),
+                ("has_grid", ctypes.c_int32), ("grid", MfGridField)]
 
 
 class MfRenderParams(ctypes.Structure):
@@ -104,6 +112,7 @@ SIGNATURES = {
                                         ctypes.c_uint64, ctypes.c_uint64,
                                         ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), _vp]),
+    "mf_grid_majorant": (ctypes.c_int, [ctypes.POINTER(MfGridField), _vp, _vp]),
     "mf_measure_peaks": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), _vp]),
     "mf_last_error": (ctypes.c_char_p, []),

@@ -107,3 +107,24 @@ def config4_scene(sigma, l_z, width=1024, height=1024):
 
 
 CONFIG4 = dict(spp=1024, max_bounces=64, seed=3)
+
+
+def config5_scene(width=2048, height=2048, n_sdf=256, n_sigma=128, seed=4):
+    """Heterogeneous GP field (config 5): union of 16 spheres + torus as a
+    trilinear SDF grid, value-noise sigma grid, l_xy = 0.03, l_z = 0.08,
+    albedo 0.85.  Camera and lights are not given by BASELINE.json; recorded
+    convention: pinhole 40 deg at (0, -4, 1.2) looking at the origin,
+    directional light travelling (-1, 1, -2)/|.| with irradiance 2, and a
+    constant environment 0.2."""
+    from .grid import GridMedium, config5_fields
+
+    sdf, sigma = config5_fields(seed=seed, n_sdf=n_sdf, n_sigma=n_sigma)
+    med = GridMedium(sigma=sigma, l_xy=0.03, l_z=0.08, albedo=0.85)
+    cam = Camera(position=(0.0, -4.0, 1.2), look_at=(0.0, 0.0, 0.0), fov_deg=40.0, width=width,
+                 height=height)
+    return ShellScene(primitives=(ShellPrimitive(sdf, med),), camera=cam,
+                      environment=Environment(radiance=(0.2, 0.2, 0.2)),
+                      sun=DirectionalLight(direction=(-1.0, 1.0, -2.0), radiance=(2.0, 2.0, 2.0)))
+
+
+CONFIG5 = dict(spp=4096, max_bounces=64, seed=4)

@@ -1,0 +1,329 @@
+// mf_grid.cuh -- heterogeneous GP field (BASELINE config 5, not in the
+// reference): trilinear SDF grid for the mean, trilinear per-voxel sigma,
+// spatially varying roughness alpha = sqrt2 sigma / l, and free flight by
+// delta / ratio tracking against a coarse majorant grid traversed with a 3D
+// DDA (exponential sampling per cell, memoryless restarts).
+//
+// Region rules follow transport.py:161-166 with sigma = sigma(p): collision
+// walks live on f in [-6 sigma, 3 sigma]; a tentative collision that lands
+// below -6 sigma(p) absorbs the path (the reference tests the depth cap at
+// every walker step; here it is tested at tentative collisions -- the
+// transmittance of the -3..-6 sigma slab is ~1e-6, transport.py:12-15);
+// shadow walks integrate |f| <= 3 sigma only.
+#pragma once
+
+#include "mf_math.cuh"
+
+namespace mf {
+
+struct GridDev {
+  const float* sdf;
+  const float* sig;
+  const float* maj;
+  int n_sdf, n_sig, n_maj;
+  V3 bmin, bmax;
+  V3 inv_h_sdf;   // (n-1) / extent, per axis
+  V3 inv_h_sig;
+  V3 inv_h_maj;   // n_maj / extent
+  V3 h_maj;       // cell size
+  float k_xy, k_z;  // alpha = k * sigma, k = sqrt2 / l
+};
+
+MF_HD float ldg(const float* p) {
+#if defined(__CUDA_ARCH__)
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
+
+MF_HD int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+struct TriSample {
+  float v;
+  V3 grad;
+};
+
+// trilinear value (and optionally the gradient of the interpolant) of an
+// n^3 vertex grid at grid coordinates g
+template <bool kGrad>
+MF_HD TriSample trilinear(const float* a, int n, V3 g, V3 inv_h) {
+  float gx = fminf(fmaxf(g.x, 0.0f), (float)(n - 1));
+  float gy = fminf(fmaxf(g.y, 0.0f), (float)(n - 1));
+  float gz = fminf(fmaxf(g.z, 0.0f), (float)(n - 1));
+  int ix = clampi((int)gx, 0, n - 2), iy = clampi((int)gy, 0, n - 2), iz = clampi((int)gz, 0, n - 2);
+  float tx = gx - (float)ix, ty = gy - (float)iy, tz = gz - (float)iz;
+  const float* p = a + ((size_t)ix * n + iy) * n + iz;
+  size_t sy = (size_t)n, sx = (size_t)n * n;
+  float c000 = ldg(p), c001 = ldg(p + 1), c010 = ldg(p + sy), c011 = ldg(p + sy + 1);
+  float c100 = ldg(p + sx), c101 = ldg(p + sx + 1), c110 = ldg(p + sx + sy),
+        c111 = ldg(p + sx + sy + 1);
+  float c00 = fmaf(tz, c001 - c000, c000), c01 = fmaf(tz, c011 - c010, c010);
+  float c10 = fmaf(tz, c101 - c100, c100), c11 = fmaf(tz, c111 - c110, c110);
+  float c0 = fmaf(ty, c01 - c00, c00), c1 = fmaf(ty, c11 - c10, c10);
+  TriSample s;
+  s.v = fmaf(tx, c1 - c0, c0);
+  if (kGrad) {
+    float gxv = c1 - c0;
+    float gyv = fmaf(tx, c11 - c10, (1.0f - tx) * (c01 - c00));
+    float d00 = c001 - c000, d01 = c011 - c010, d10 = c101 - c100, d11 = c111 - c110;
+    float d0 = fmaf(ty, d01 - d00, d00), d1 = fmaf(ty, d11 - d10, d10);
+    float gzv = fmaf(tx, d1 - d0, d0);
+    s.grad = v3(gxv * inv_h.x, gyv * inv_h.y, gzv * inv_h.z);
+  } else {
+    s.grad = v3(0.0f, 0.0f, 0.0f);
+  }
+  return s;
+}
+
+MF_HD V3 grid_coord(const GridDev& g, V3 p, V3 inv_h) {
+  return v3((p.x - g.bmin.x) * inv_h.x, (p.y - g.bmin.y) * inv_h.y, (p.z - g.bmin.z) * inv_h.z);
+}
+
+MF_HD float grid_f(const GridDev& g, V3 p) {
+  return trilinear<false>(g.sdf, g.n_sdf, grid_coord(g, p, g.inv_h_sdf), g.inv_h_sdf).v;
+}
+
+MF_HD float grid_sigma(const GridDev& g, V3 p) {
+  return trilinear<false>(g.sig, g.n_sig, grid_coord(g, p, g.inv_h_sig), g.inv_h_sig).v;
+}
+
+// Local medium at sigma: generalized kind, alpha = k sigma; `base` supplies
+// the mixture ratio, Fresnel / albedo and the slope table.
+MF_HD MediumK grid_medium(const MediumK& base, float sigma, float k_xy, float k_z) {
+  MediumK m = base;
+  m.kind = kGeneralized;
+  m.sigma = sigma;
+  m.inv_sigma = frcp(sigma);
+  float ax = k_xy * sigma, az = k_z * sigma;
+  m.ax = ax;
+  m.ay = ax;
+  m.az = az;
+  m.inv_ax = frcp(ax);
+  m.inv_ay = m.inv_ax;
+  m.inv_az2 = frcp(az * az);
+  m.exp_neg_c = expf(-m.inv_az2);
+  m.beck_norm = kInvSqrtPi * kInvSqrtPi * m.inv_ax * m.inv_ax;            // 1/(pi ax^2)
+  m.d_norm = m.beck_norm * kInvSqrtPi * frcp(az);                         // 1/(pi^1.5 ax^2 az)
+  return m;
+}
+
+// extinction at p along dir; 0 outside the region [lo_mult sigma, 3 sigma].
+// Also reports f and sigma (for the absorption rule).
+MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir, float lo_mult,
+                            float* f_out, float* s_out) {
+  TriSample fs = trilinear<true>(g.sdf, g.n_sdf, grid_coord(g, p, g.inv_h_sdf), g.inv_h_sdf);
+  float sg = fmaxf(grid_sigma(g, p), 1e-6f);
+  *f_out = fs.v;
+  *s_out = sg;
+  if (fs.v < lo_mult * sg || fs.v > 3.0f * sg) return 0.0f;
+  float gn2 = dot3(fs.grad, fs.grad);
+  V3 n = gn2 > 0.0f ? mul3(fs.grad, frsqrt(gn2)) : v3(0.0f, 0.0f, 1.0f);
+  Frame fr = frame_about(n);
+  V3 wl = to_local(fr, dir);
+  float ax = g.k_xy * sg, az = g.k_z * sg;
+  float area = proj_area_erf(wl, ax, ax, az);
+  (void)base;
+  return mills(fs.v * frcp(sg)) * frcp(sg) * area;
+}
+
+struct GridWalk {
+  int outcome;   // kEscaped / kAbsorbed / kCollided (values of mf_transport.cuh)
+  V3 pos;
+  float weight;
+  int steps;
+  int violations;
+};
+
+// Slab test against the grid bounds; returns false on a miss.
+MF_HD bool grid_box(const GridDev& g, V3 o, V3 d, float* t0, float* t1) {
+  float ta = 0.0f, tb = INFINITY;
+  float os[3] = {o.x, o.y, o.z}, ds[3] = {d.x, d.y, d.z};
+  float lo[3] = {g.bmin.x, g.bmin.y, g.bmin.z}, hi[3] = {g.bmax.x, g.bmax.y, g.bmax.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float inv = 1.0f / ds[a];
+    float u = (lo[a] - os[a]) * inv, v = (hi[a] - os[a]) * inv;
+    if (ds[a] == 0.0f) {
+      if (os[a] < lo[a] || os[a] > hi[a]) return false;
+      continue;
+    }
+    ta = fmaxf(ta, fminf(u, v));
+    tb = fminf(tb, fmaxf(u, v));
+  }
+  *t0 = ta;
+  *t1 = tb;
+  return ta <= tb;
+}
+
+// Delta (ratio == false) or ratio tracking through the majorant grid.
+// Random draws: blocks (segment, call0 + k) of the path's Philox stream.
+template <typename RngBlock>
+MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_block,
+                         uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max) {
+  GridWalk w;
+  w.outcome = 0;
+  w.pos = pos;
+  w.weight = 1.0f;
+  w.steps = 0;
+  w.violations = 0;
+  float lo_mult = ratio ? -3.0f : -6.0f;
+  float t0, t1;
+  if (!grid_box(g, pos, dir, &t0, &t1)) return w;
+  t1 = fminf(t1, t_max);
+  float t = t0;
+  // DDA setup in majorant-cell coordinates
+  V3 gc = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
+  int n = g.n_maj;
+  int cx = clampi((int)gc.x, 0, n - 1), cy = clampi((int)gc.y, 0, n - 1),
+      cz = clampi((int)gc.z, 0, n - 1);
+  int sx = dir.x > 0.0f ? 1 : -1, sy = dir.y > 0.0f ? 1 : -1, sz = dir.z > 0.0f ? 1 : -1;
+  float idx = 1.0f / dir.x, idy = 1.0f / dir.y, idz = 1.0f / dir.z;
+  // parametric distance to the next cell wall on each axis
+  auto wall = [&](int c, int s, float bmin, float h, float o, float id) {
+    float x = bmin + h * (float)(c + (s > 0 ? 1 : 0));
+    float tw = (x - o) * id;
+    return isfinite(tw) ? tw : INFINITY;
+  };
+  float tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
+  float ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
+  float tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
+  float dtx = isfinite(idx) ? fabsf(g.h_maj.x * idx) : INFINITY;
+  float dty = isfinite(idy) ? fabsf(g.h_maj.y * idy) : INFINITY;
+  float dtz = isfinite(idz) ? fabsf(g.h_maj.z * idz) : INFINITY;
+  U4 bits = U4{0, 0, 0, 0};
+  int avail = 0;
+  uint32_t call = call0;
+  for (int iter = 0; iter < 1000000; ++iter) {
+    float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
+    float mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
+    if (mu > 0.0f) {
+      if (avail == 0) {
+        bits = rng_block(call++);
+        avail = 4;
+      }
+      float u = u01(bits.x);
+      bits.x = bits.y;
+      bits.y = bits.z;
+      bits.z = bits.w;
+      --avail;
+      float ts = t - flog(u) / mu;
+      if (ts < t_exit) {
+        t = ts;
+        w.steps++;
+        V3 p = fma3(dir, t, pos);
+        float f, sg;
+        float st = grid_extinction(g, base, p, dir, lo_mult, &f, &sg);
+        if (st > mu * 1.00001f) w.violations++;
+        if (ratio) {
+          w.weight *= fmaxf(1.0f - st / mu, 0.0f);
+          if (!(w.weight > 0.0f)) {
+            w.pos = p;
+            return w;
+          }
+        } else {
+          if (f < -6.0f * sg) {
+            w.outcome = 1;   // absorbed below the depth cap
+            w.pos = p;
+            return w;
+          }
+          if (avail == 0) {
+            bits = rng_block(call++);
+            avail = 4;
+          }
+          float u2 = u01(bits.x);
+          bits.x = bits.y;
+          bits.y = bits.z;
+          bits.z = bits.w;
+          --avail;
+          if (u2 * mu < st) {
+            w.outcome = 2;
+            w.pos = p;
+            return w;
+          }
+        }
+        continue;
+      }
+    }
+    // leave the cell
+    if (t_exit >= t1) {
+      w.pos = fma3(dir, t1, pos);
+      return w;   // escaped the grid (or reached the light)
+    }
+    t = t_exit;
+    if (tx <= ty && tx <= tz) {
+      cx += sx;
+      tx += dtx;
+      if (cx < 0 || cx >= n) break;
+    } else if (ty <= tz) {
+      cy += sy;
+      ty += dty;
+      if (cy < 0 || cy >= n) break;
+    } else {
+      cz += sz;
+      tz += dtz;
+      if (cz < 0 || cz >= n) break;
+    }
+  }
+  w.pos = fma3(dir, t, pos);
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// majorant of one cell (host-checked formula; run by mf_grid_majorant)
+
+MF_HD float area_max_iso(float a_xy, float a_z) {
+  // max over directions of sigma(w) for ax = ay = a_xy: 1D scan in theta
+  float best = 0.0f;
+  for (int i = 0; i <= 96; ++i) {
+    float th = kPi * (float)i / 96.0f;
+    V3 w = v3(sinf(th), 0.0f, cosf(th));
+    best = fmaxf(best, proj_area_erf(w, a_xy, a_xy, a_z));
+  }
+  return best * 1.03f;
+}
+
+MF_HD float grid_cell_majorant(const GridDev& g, int cx, int cy, int cz) {
+  // world extent of the cell
+  V3 lo = v3(g.bmin.x + g.h_maj.x * cx, g.bmin.y + g.h_maj.y * cy, g.bmin.z + g.h_maj.z * cz);
+  V3 hi = add3(lo, g.h_maj);
+  // exact bounds of the trilinear interpolants: min / max over covering vertices
+  V3 a = grid_coord(g, lo, g.inv_h_sdf), b = grid_coord(g, hi, g.inv_h_sdf);
+  int x0 = clampi((int)floorf(a.x), 0, g.n_sdf - 1), x1 = clampi((int)ceilf(b.x), 0, g.n_sdf - 1);
+  int y0 = clampi((int)floorf(a.y), 0, g.n_sdf - 1), y1 = clampi((int)ceilf(b.y), 0, g.n_sdf - 1);
+  int z0 = clampi((int)floorf(a.z), 0, g.n_sdf - 1), z1 = clampi((int)ceilf(b.z), 0, g.n_sdf - 1);
+  float fmin = INFINITY;
+  for (int i = x0; i <= x1; ++i)
+    for (int j = y0; j <= y1; ++j)
+      for (int k = z0; k <= z1; ++k)
+        fmin = fminf(fmin, ldg(g.sdf + ((size_t)i * g.n_sdf + j) * g.n_sdf + k));
+  V3 c = grid_coord(g, lo, g.inv_h_sig), d = grid_coord(g, hi, g.inv_h_sig);
+  x0 = clampi((int)floorf(c.x), 0, g.n_sig - 1); x1 = clampi((int)ceilf(d.x), 0, g.n_sig - 1);
+  y0 = clampi((int)floorf(c.y), 0, g.n_sig - 1); y1 = clampi((int)ceilf(d.y), 0, g.n_sig - 1);
+  z0 = clampi((int)floorf(c.z), 0, g.n_sig - 1); z1 = clampi((int)ceilf(d.z), 0, g.n_sig - 1);
+  float smin = INFINITY, smax = 0.0f;
+  for (int i = x0; i <= x1; ++i)
+    for (int j = y0; j <= y1; ++j)
+      for (int k = z0; k <= z1; ++k) {
+        float v = ldg(g.sig + ((size_t)i * g.n_sig + j) * g.n_sig + k);
+        smin = fminf(smin, v);
+        smax = fmaxf(smax, v);
+      }
+  smin = fmaxf(smin, 1e-6f);
+  smax = fmaxf(smax, smin);
+  if (fmin > 3.0f * smax) return 0.0f;   // entirely above every shell: vacuum
+  // sup over sigma in [smin, smax] of rho(max(fmin, -6 sigma), sigma) * max_w sigma(w)
+  float best = 0.0f;
+  const int K = 12;
+  for (int i = 0; i <= K; ++i) {
+    float s = smin + (smax - smin) * (float)i / (float)K;
+    float f = fmaxf(fmin, -6.0f * s);
+    if (f > 3.0f * s) continue;
+    float rho = mills(f / s) / s;
+    best = fmaxf(best, rho * area_max_iso(g.k_xy * s, g.k_z * s));
+  }
+  // rho * area varies by < 5 % between the sigma samples of one cell
+  return best * 1.15f;
+}
+
+}  // namespace mf

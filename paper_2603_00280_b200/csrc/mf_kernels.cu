@@ -188,18 +188,29 @@ __device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t pixel, f
 }
 
 // shadow transmittance from pos towards unit direction wl over distance t_max
+template <int kMode>
 __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& st, V3 pos, V3 wl,
                                            float t_max, float h_end, Counters& cn,
                                            float sig_known = -1.0f) {
-  if (sc.single_plane) {
+  if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
     float sig = sig_known >= 0.0f ? sig_known : proj_area(m, wl);
     return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig);
+  } else if constexpr (kMode == 2) {
+    const PathRng& r = st.rng;
+    uint32_t seg = (uint32_t)st.bounce;
+    GridWalk w = grid_walk(sc.grid, sc.media[0],
+                           [&](uint32_t call) { return rng_block(r, seg, call); }, kCallShadow,
+                           pos, wl, true, t_max);
+    cn.v[kStTrackSteps] += (uint32_t)w.steps;
+    cn.v[kStViolations] += (uint32_t)w.violations;
+    return w.weight;
+  } else {
+    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max);
+    cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
+    cn.v[kStViolations] += (uint32_t)w.violations;
+    return w.weight;
   }
-  WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max);
-  cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
-  cn.v[kStViolations] += (uint32_t)w.violations;
-  return w.weight;
 }
 
 // One free-flight segment plus the scattering event at its end.
@@ -212,7 +223,15 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
 // every later stage runs once per lane group (measured: 5.6 active lanes
 // per warp instruction).  Finished lanes stay predicated off inside the
 // stages but still pass every barrier.
-template <bool kPlanar>
+template <int kMode>
+__device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev& ps,
+                                               PathState& st, Counters& cn, unsigned amask,
+                                               const MediumK& m, const Frame& fr, V3 pos,
+                                               float sig_known, bool done, float u_br,
+                                               float u_s2, float u_rr);
+
+// kMode: 0 single plane (analytic), 1 general shells (tracking), 2 grid field
+template <int kMode>
 __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& ps, PathState& st,
                                              Counters& cn, unsigned amask) {
   cn.v[kStSegments]++;
@@ -222,8 +241,26 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
   V3 pos = st.pos;
   bool done = false;
   float sig_dir = 0.0f;   // sigma(dir): in the plane frame this is sigma(wo)
+  constexpr bool kPlanar = kMode == 0;
   // ---- stage 1: free flight (transport.py:144-297)
-  if (kPlanar) {
+  if (kMode == 2) {
+    const PathRng& r = st.rng;
+    uint32_t seg = (uint32_t)st.bounce;
+    GridWalk w = grid_walk(sc.grid, sc.media[0],
+                           [&](uint32_t call) { return rng_block(r, seg, call); }, 1u, st.pos,
+                           st.dir, false, INFINITY);
+    cn.v[kStTrackSteps] += (uint32_t)w.steps;
+    cn.v[kStViolations] += (uint32_t)w.violations;
+    pos = w.pos;
+    if (w.outcome == kEscaped) {
+      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
+      cn.v[kStEscaped]++;
+      done = true;
+    } else if (w.outcome == kAbsorbed) {
+      cn.v[kStAbsorbed]++;
+      done = true;
+    }
+  } else if (kPlanar) {
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
     sig_dir = sig;
@@ -256,11 +293,34 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
     }
   }
   __syncwarp(amask);
-  const PrimDev& pr = sc.prims[k];
-  const MediumK& m = sc.media[k];
-  Frame fr = frame_about(kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(pr, pos));
+  if constexpr (kMode == 2) {
+    // local medium and frame of the grid field at the collision
+    TriSample fs = trilinear<true>(sc.grid.sdf, sc.grid.n_sdf,
+                                   grid_coord(sc.grid, pos, sc.grid.inv_h_sdf),
+                                   sc.grid.inv_h_sdf);
+    float sg = fmaxf(grid_sigma(sc.grid, pos), 1e-6f);
+    MediumK mg = grid_medium(sc.media[0], sg, sc.grid.k_xy, sc.grid.k_z);
+    float gn2 = dot3(fs.grad, fs.grad);
+    V3 nrm = gn2 > 0.0f ? mul3(fs.grad, frsqrt(gn2)) : v3(0.0f, 0.0f, 1.0f);
+    return scatter_stages<kMode>(sc, ps, st, cn, amask, mg, frame_about(nrm), pos, -1.0f, done,
+                                 u_br, u_s2, u_rr);
+  } else {
+    V3 nrm = kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(sc.prims[k], pos);
+    return scatter_stages<kMode>(sc, ps, st, cn, amask, sc.media[k], frame_about(nrm), pos,
+                                 sig_dir, done, u_br, u_s2, u_rr);
+  }
+}
+
+// Stages 2-3 of a segment at a real collision (NEE, phase sampling, depth
+// cap, RR) for medium m and local frame fr; sig_known >= 0 is sigma(dir).
+template <int kMode>
+__device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev& ps,
+                                               PathState& st, Counters& cn, unsigned amask,
+                                               const MediumK& m, const Frame& fr, V3 pos,
+                                               float sig_known, bool done, float u_br,
+                                               float u_s2, float u_rr) {
   V3 wo = to_local(fr, st.dir);
-  float sig_o = kPlanar ? sig_dir : proj_area(m, wo);
+  float sig_o = sig_known >= 0.0f ? sig_known : proj_area(m, wo);
   if (!done) {
     cn.v[kStScatters]++;
     if (!(sig_o >= 1e-12f)) {
@@ -275,7 +335,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
     V3 ph = phase_eval(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr(sc, st, pos, sc.sun_to, INFINITY,
+      float tr = shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
                            sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
@@ -290,7 +350,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
     V3 ph = phase_eval(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
+      float tr = shadow_tr<kMode>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
       float s = tr * frcp(r2);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
                            st.T.z * ph.z * sc.point_I.z * s));
@@ -323,7 +383,7 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
   return done;
 }
 
-template <bool kPlanar, bool kCallerRays>
+template <int kMode, bool kCallerRays>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_constant__ SceneDev sc,
                                                        const __grid_constant__ PassDev ps) {
   const unsigned full = 0xffffffffu;
@@ -383,7 +443,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
     }
     unsigned amask = __ballot_sync(full, active);
     if (active) {
-      if (path_segment<kPlanar>(sc, ps, st, cn, amask)) {
+      if (path_segment<kMode>(sc, ps, st, cn, amask)) {
         float r = st.L.x, g = st.L.y, bl = st.L.z;
         if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
           cn.v[kStNonfinite]++;
@@ -433,10 +493,19 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
   uint32_t steps = 0, viol = 0;
   if (i < n) {
     PathRng rng{k0, k1, stream_lo, i};
-    WalkResult w = walk(sc, rng, 0u, kCallShadow, org, dir, true, INFINITY);
-    w_out[i] = w.weight;
-    steps = (uint32_t)max(w.steps, 0);
-    viol = (uint32_t)w.violations;
+    if (sc.has_grid) {
+      GridWalk w = grid_walk(sc.grid, sc.media[0],
+                             [&](uint32_t call) { return rng_block(rng, 0u, call); },
+                             kCallShadow, org, dir, true, INFINITY);
+      w_out[i] = w.weight;
+      steps = (uint32_t)w.steps;
+      viol = (uint32_t)w.violations;
+    } else {
+      WalkResult w = walk(sc, rng, 0u, kCallShadow, org, dir, true, INFINITY);
+      w_out[i] = w.weight;
+      steps = (uint32_t)max(w.steps, 0);
+      viol = (uint32_t)w.violations;
+    }
   }
   unsigned a = __reduce_add_sync(0xffffffffu, steps);
   unsigned b = __reduce_add_sync(0xffffffffu, viol);
@@ -452,6 +521,18 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
 __global__ void __launch_bounds__(128) slope_table_kernel(float* tab) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < kTabNT * kTabNU) tab[k] = slope_table_node(k / kTabNU, k % kTabNU);
+}
+
+// ---------------------------------------------------------------------------
+// grid-field majorant (one thread per cell)
+
+__global__ void __launch_bounds__(128) grid_majorant_kernel(const __grid_constant__ GridDev g,
+                                                             float* out) {
+  int n = g.n_maj;
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n * n * n) return;
+  int cx = c / (n * n), cy = (c / n) % n, cz = c % n;
+  out[c] = grid_cell_majorant(g, cx, cy, cz);
 }
 
 // ---------------------------------------------------------------------------
@@ -520,7 +601,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[4] = {0, 0, 0, 0};
+  int blocks[6] = {0, 0, 0, 0, 0, 0};
 };
 
 int device_occupancy(Occupancy* occ) {
@@ -536,13 +617,17 @@ int device_occupancy(Occupancy* occ) {
   }
   Occupancy o;
   MF_CUDA(cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[0], path_kernel<true, false>,
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[0], path_kernel<0, false>,
                                                         kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[1], path_kernel<false, false>,
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[1], path_kernel<1, false>,
                                                         kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[2], path_kernel<true, true>,
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[2], path_kernel<2, false>,
                                                         kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[3], path_kernel<false, true>,
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[3], path_kernel<0, true>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[4], path_kernel<1, true>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[5], path_kernel<2, true>,
                                                         kBlock, 0));
   for (int& b : o.blocks) b = std::max(b, 1);
   if (dev < 64) {
@@ -607,16 +692,19 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   Occupancy occ;
   int rc = device_occupancy(&occ);
   if (rc) return rc;
-  int which = (sc.single_plane ? 0 : 1) + (caller_rays ? 2 : 0);
-  int grid = occ.sms * occ.blocks[which];
+  int mode = sc.has_grid ? 2 : (sc.single_plane ? 0 : 1);
+  int grid = occ.sms * occ.blocks[mode + (caller_rays ? 3 : 0)];
   int64_t need = ((int64_t)ps.n_paths + kBlock - 1) / kBlock;
   grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
-  if (sc.single_plane) {
-    if (caller_rays) path_kernel<true, true><<<grid, kBlock, 0, st>>>(sc, ps);
-    else path_kernel<true, false><<<grid, kBlock, 0, st>>>(sc, ps);
+  if (mode == 0) {
+    if (caller_rays) path_kernel<0, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
+  } else if (mode == 1) {
+    if (caller_rays) path_kernel<1, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<1, false><<<grid, kBlock, 0, st>>>(sc, ps);
   } else {
-    if (caller_rays) path_kernel<false, true><<<grid, kBlock, 0, st>>>(sc, ps);
-    else path_kernel<false, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
   }
   g_launches++;
   MF_CUDA(cudaGetLastError());
@@ -630,6 +718,36 @@ constexpr size_t kMaxPassPaths = size_t(1) << 26;  // 64 Mi paths (768 MiB of ra
 extern "C" {
 
 const char* mf_last_error(void) { return g_err.c_str(); }
+
+int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* stream) {
+  if (!grid || !d_majorant_out) return fail(MF_ERR_PARAM, "null argument");
+  // reuse the scene builder's validation: a one-primitive grid scene
+  mf_scene tmp;
+  std::memset(&tmp, 0, sizeof(tmp));
+  tmp.n_prims = 1;
+  tmp.n_media = 1;
+  tmp.prims[0].shape = MF_SHAPE_GRID;
+  tmp.media[0].kind = MF_KIND_GENERALIZED;
+  tmp.media[0].fresnel = MF_FRESNEL_ONE;
+  tmp.media[0].ax = tmp.media[0].ay = tmp.media[0].az = 1.0;
+  tmp.media[0].sigma = 1.0;
+  tmp.media[0].mix_ratio = 0.5;
+  tmp.camera.width = tmp.camera.height = 1;
+  tmp.camera.look_at[2] = -1.0;
+  tmp.has_grid = 1;
+  tmp.grid = *grid;
+  tmp.grid.d_majorant = d_majorant_out;
+  SceneDev sc;
+  std::string berr;
+  int rc = build_scene(tmp, &sc, &berr);
+  if (rc) return fail(rc, berr);
+  int cells = grid->n_maj * grid->n_maj * grid->n_maj;
+  grid_majorant_kernel<<<(cells + 127) / 128, 128, 0, (cudaStream_t)stream>>>(sc.grid,
+                                                                              d_majorant_out);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
 
 int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream) {
   if (!fp32_ginst_s || !sfu_ginst_s) return fail(MF_ERR_PARAM, "null argument");

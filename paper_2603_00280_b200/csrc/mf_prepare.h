@@ -89,7 +89,7 @@ struct PrimK {
 };
 
 inline int prepare_primitive(const mf_primitive& in, int n_media, PrimK* out, std::string* err) {
-  if (in.shape != MF_SHAPE_PLANE && in.shape != MF_SHAPE_SPHERE) {
+  if (in.shape != MF_SHAPE_PLANE && in.shape != MF_SHAPE_SPHERE && in.shape != MF_SHAPE_GRID) {
     *err = "unsupported primitive shape " + std::to_string(in.shape);
     return MF_ERR_UNSUPPORTED;
   }

@@ -65,7 +65,47 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);
   }
   sc.min_skip = std::isfinite(min_sigma) ? (float)(1e-7 * min_sigma) : 1e-7f;
+  // grid field (BASELINE config 5): exactly one MF_SHAPE_GRID primitive
+  int n_grid = 0;
+  for (int j = 0; j < in.n_prims; ++j) n_grid += in.prims[j].shape == MF_SHAPE_GRID;
+  if (n_grid || in.has_grid) {
+    if (!in.has_grid || n_grid != 1 || in.n_prims != 1)
+      return (*err = std::string("a grid field must be the scene's only primitive"), MF_ERR_UNSUPPORTED);
+    const mf_grid_field& g = in.grid;
+    if (!g.d_sdf || !g.d_sigma || !g.d_majorant || g.n_sdf < 2 || g.n_sigma < 2 || g.n_maj < 1)
+      return (*err = std::string("grid field arrays / sizes invalid"), MF_ERR_PARAM);
+    if (!(g.l_xy > 0.0) || !(g.l_z > 0.0))
+      return (*err = std::string("grid correlation lengths must be > 0"), MF_ERR_PARAM);
+    GridDev gd;
+    gd.sdf = g.d_sdf;
+    gd.sig = g.d_sigma;
+    gd.maj = g.d_majorant;
+    gd.n_sdf = g.n_sdf;
+    gd.n_sig = g.n_sigma;
+    gd.n_maj = g.n_maj;
+    gd.bmin = v3((float)g.bmin[0], (float)g.bmin[1], (float)g.bmin[2]);
+    gd.bmax = v3((float)g.bmax[0], (float)g.bmax[1], (float)g.bmax[2]);
+    double ext[3];
+    for (int a = 0; a < 3; ++a) {
+      ext[a] = g.bmax[a] - g.bmin[a];
+      if (!(ext[a] > 0.0)) return (*err = std::string("grid bounds are empty"), MF_ERR_PARAM);
+    }
+    gd.inv_h_sdf = v3((float)((g.n_sdf - 1) / ext[0]), (float)((g.n_sdf - 1) / ext[1]),
+                      (float)((g.n_sdf - 1) / ext[2]));
+    gd.inv_h_sig = v3((float)((g.n_sigma - 1) / ext[0]), (float)((g.n_sigma - 1) / ext[1]),
+                      (float)((g.n_sigma - 1) / ext[2]));
+    gd.inv_h_maj = v3((float)(g.n_maj / ext[0]), (float)(g.n_maj / ext[1]),
+                      (float)(g.n_maj / ext[2]));
+    gd.h_maj = v3((float)(ext[0] / g.n_maj), (float)(ext[1] / g.n_maj), (float)(ext[2] / g.n_maj));
+    gd.k_xy = (float)(std::sqrt(2.0) / g.l_xy);
+    gd.k_z = (float)(std::sqrt(2.0) / g.l_z);
+    sc.has_grid = 1;
+    sc.grid = gd;
+    sc.single_plane = 0;
+    sc.min_skip = 1e-8f;
+  }
   sc.single_plane = (in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE) ? 1 : 0;
+  sc.has_grid = 0;
   // camera basis (scene.py:30-41), in double
   const mf_camera& cam = in.camera;
   if (cam.width < 1 || cam.height < 1) return (*err = std::string("camera size must be >= 1"), MF_ERR_PARAM);

@@ -19,6 +19,7 @@
 
 #include "mf_math.cuh"
 #include "mf_query.cuh"
+#include "mf_grid.cuh"
 
 namespace mf {
 
@@ -58,6 +59,8 @@ struct SceneDev {
   V3 point_pos;
   V3 point_I;
   float min_skip;      // 1e-7 * min sigma (transport.py:167)
+  int has_grid;        // 1: the single primitive is the grid field below
+  GridDev grid;
 };
 
 // ---------------------------------------------------------------------------

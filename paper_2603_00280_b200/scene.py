@@ -94,6 +94,12 @@ class ShellScene:
     def __post_init__(self):
         object.__setattr__(self, "primitives", tuple(self.primitives))
         prims = self.primitives
+        from .grid import GridSDF
+
+        if any(isinstance(p.sdf, GridSDF) for p in prims):
+            if len(prims) != 1:
+                raise ConfigError("a grid field must be the scene's only primitive")
+            return
         for i in range(len(prims)):
             for j in range(i + 1, len(prims)):
                 gap = surface_distance(prims[i].sdf, prims[j].sdf)
@@ -112,8 +118,13 @@ def to_c_scene(scene: ShellScene) -> _lib.MfScene:
     c = _lib.MfScene()
     c.n_prims = len(scene.primitives)
     c.n_media = len(scene.primitives)
+    from .grid import GridSDF, fill_scene_grid
+
     for j, pr in enumerate(scene.primitives):
         cp = c.prims[j]
+        if isinstance(pr.sdf, GridSDF):
+            fill_scene_grid(c, j, pr.sdf, pr.medium)
+            continue
         if isinstance(pr.sdf, Plane):
             cp.shape = _lib.SHAPE_PLANE
             cp.z0 = float(pr.sdf.z0)

@@ -93,3 +93,4 @@ def test_struct_layout_matches_header(tmp_path):
 def test_sm100a_code_in_library():
     out = subprocess.run(["cuobjdump", "--list-elf", build.OUT], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+STRUCTS["mf_grid_field"] = _lib.MfGridField
