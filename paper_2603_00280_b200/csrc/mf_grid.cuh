@@ -197,6 +197,9 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   for (int iter = 0; iter < 1000000; ++iter) {
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
     float mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
+#if defined(MF_GRID_DEBUG) && !defined(__CUDA_ARCH__)
+    printf("it %d t %g cell %d %d %d mu %g tx %g ty %g tz %g t1 %g\n", iter, t, cx, cy, cz, mu, tx, ty, tz, t1);
+#endif
     if (mu > 0.0f) {
       if (avail == 0) {
         bits = rng_block(call++);

@@ -65,6 +65,8 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);
   }
   sc.min_skip = std::isfinite(min_sigma) ? (float)(1e-7 * min_sigma) : 1e-7f;
+  sc.single_plane = (in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE) ? 1 : 0;
+  sc.has_grid = 0;
   // grid field (BASELINE config 5): exactly one MF_SHAPE_GRID primitive
   int n_grid = 0;
   for (int j = 0; j < in.n_prims; ++j) n_grid += in.prims[j].shape == MF_SHAPE_GRID;
@@ -104,8 +106,7 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     sc.single_plane = 0;
     sc.min_skip = 1e-8f;
   }
-  sc.single_plane = (in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE) ? 1 : 0;
-  sc.has_grid = 0;
+
   // camera basis (scene.py:30-41), in double
   const mf_camera& cam = in.camera;
   if (cam.width < 1 || cam.height < 1) return (*err = std::string("camera size must be >= 1"), MF_ERR_PARAM);

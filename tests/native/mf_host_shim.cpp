@@ -3,6 +3,7 @@
 // against the float64 oracle without a GPU.  Not part of the product (the
 // package never loads this library; there is no CPU fallback).
 #include <cstdint>
+#include <cstring>
 #include <string>
 
 #include "../../paper_2603_00280_b200/csrc/mf_prepare.h"
@@ -115,6 +116,18 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
     PathRng r{(uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)i, 0u};
     V3 o = v3(org[i], org[n + i], org[2 * n + i]);
     V3 d = v3(dir[i], dir[n + i], dir[2 * n + i]);
+    if (sc.has_grid) {
+      GridWalk w = grid_walk(sc.grid, sc.media[0],
+                             [&](uint32_t call) { return rng_block(r, 0u, call); },
+                             ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY);
+      state[i] = w.outcome;
+      pos[i] = w.pos.x;
+      pos[n + i] = w.pos.y;
+      pos[2 * n + i] = w.pos.z;
+      weight[i] = w.weight;
+      *violations += w.violations;
+      continue;
+    }
     WalkResult w = walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY);
     state[i] = w.outcome;
     pos[i] = w.pos.x;
@@ -126,4 +139,53 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
   return 0;
 }
 
+}  // extern "C"
+
+extern "C" {
+
+// host build of the majorant grid (same per-cell code as the device)
+int mfh_grid_majorant(const mf_grid_field* grid, float* out) {
+  mf_scene tmp;
+  std::memset(&tmp, 0, sizeof(tmp));
+  tmp.n_prims = 1;
+  tmp.n_media = 1;
+  tmp.prims[0].shape = MF_SHAPE_GRID;
+  tmp.media[0].kind = MF_KIND_GENERALIZED;
+  tmp.media[0].fresnel = MF_FRESNEL_ONE;
+  tmp.media[0].ax = tmp.media[0].ay = tmp.media[0].az = 1.0;
+  tmp.media[0].sigma = 1.0;
+  tmp.media[0].mix_ratio = 0.5;
+  tmp.camera.width = tmp.camera.height = 1;
+  tmp.camera.look_at[2] = -1.0;
+  tmp.has_grid = 1;
+  tmp.grid = *grid;
+  tmp.grid.d_majorant = out;
+  SceneDev sc;
+  std::string err;
+  if (build_scene(tmp, &sc, &err) != MF_OK) return 1;
+  int n = grid->n_maj;
+  for (int c = 0; c < n * n * n; ++c) out[c] = grid_cell_majorant(sc.grid, c / (n * n), (c / n) % n, c % n);
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" {
+// grid field probes (f, sigma, extinction along dir) at points, host build
+int mfh_grid_probe(const mf_scene* scene, const float* p, const float* dir, int64_t n,
+                   float* out) {
+  SceneDev sc;
+  std::string err;
+  if (build_scene(*scene, &sc, &err) != MF_OK) return 1;
+  for (int64_t i = 0; i < n; ++i) {
+    V3 x = v3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+    V3 d = v3(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]);
+    float f, s;
+    float e = grid_extinction(sc.grid, sc.media[0], x, d, -6.0f, &f, &s);
+    out[3 * i] = f;
+    out[3 * i + 1] = s;
+    out[3 * i + 2] = e;
+  }
+  return 0;
+}
 }  // extern "C"
