@@ -306,8 +306,9 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
                                  u_br, u_s2, u_rr);
   } else {
     V3 nrm = kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(sc.prims[k], pos);
+    // sigma(dir) from the flight is sigma(wo) only in the (identity) plane frame
     return scatter_stages<kMode>(sc, ps, st, cn, amask, sc.media[k], frame_about(nrm), pos,
-                                 sig_dir, done, u_br, u_s2, u_rr);
+                                 kPlanar ? sig_dir : -1.0f, done, u_br, u_s2, u_rr);
   }
 }
 
