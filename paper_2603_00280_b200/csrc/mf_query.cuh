@@ -78,6 +78,11 @@ MF_HD QueryResult query_point(const MediumK& m, int shape, float z0, V3 c, float
 MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo, V3 wi, float u1,
                               float u2, unsigned mask) {
   QueryResult q;
+  // caller uniforms are clamped into the open interval: u = 0 or 1 (e.g. a
+  // float64 draw rounded to float32) make the inverse CDFs infinite, also in
+  // the reference (ndf.py:353 erfinv(+-1))
+  u1 = fminf(fmaxf(u1, 5.9604644775390625e-08f), 0.99999994f);
+  u2 = fminf(fmaxf(u2, 5.9604644775390625e-08f), 0.99999994f);
   V3 wol = to_local(fr, wo);
   V3 wil = to_local(fr, wi);
   float sig_o = proj_area(m, wol);

@@ -189,3 +189,7 @@ int mfh_grid_probe(const mf_scene* scene, const float* p, const float* dir, int6
   return 0;
 }
 }  // extern "C"
+
+extern "C" {
+float mfh_u01(uint32_t bits) { return u01(bits); }
+}

@@ -149,3 +149,23 @@ def test_config4_media_host(host_math, sigma, lz):
     assert r["n_bad"] == 0, r
     r = parity.check_rel(o[0], om.extinction_local(WO, np.zeros(len(WO)), m), floor=1e-25)
     assert r["n_bad"] == 0, r
+
+
+def test_uniforms_strictly_inside_unit_interval(host_math):
+    """The device uniform u01 never returns 0 or 1 (1.0f made erfinv(2u-1)
+    infinite and stalled the walker on NaN directions)."""
+    host_math.mfh_u01.restype = ctypes.c_float
+    host_math.mfh_u01.argtypes = [ctypes.c_uint32]
+    lo = host_math.mfh_u01(0)
+    hi = host_math.mfh_u01(0xFFFFFFFF)
+    assert 0.0 < lo < 1e-6 and 1.0 - 1e-6 < hi < 1.0
+
+
+def test_query_clamps_boundary_uniforms(host_math):
+    med = configs.config1_medium()
+    p = np.zeros((4, 3), np.float32)
+    wo = np.tile(np.array([0.6, 0.0, -0.8], np.float32), (4, 1))
+    u = np.array([[0.0, 0.0], [1.0, 1.0], [0.25, 1.0], [0.75, 0.0]], np.float32)
+    o = run_query(host_math, med, p, wo, wo, u)
+    for k in (5, 6, 7, 8, 9):
+        assert np.all(np.isfinite(o[k]))
