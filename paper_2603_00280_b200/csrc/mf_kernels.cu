@@ -136,6 +136,7 @@ struct PassDev {
   uint32_t n_paths;      // paths in this pass
   uint32_t S;            // samples per local pixel in this pass
   uint32_t sample_begin; // global sample index of the pass's first sample
+  uint32_t n_local;      // local pixels of this rank (render mode)
   int shard, rank, nranks, tile, tiles_x;
   float* rad;            // SoA [3][n_paths]
   unsigned int* counter;
@@ -163,8 +164,12 @@ __device__ __forceinline__ int local_to_pixel(const SceneDev& sc, const PassDev&
 
 struct PathState {
   V3 pos, dir, T, L;
+  V3 cpos;               // pending collision (flight -> scatter stage)
+  int ck;                // primitive of the pending collision
+  float csig;            // sigma(dir) when known in the collision frame, else -1
+  float u_br, u_s2, u_rr;  // the segment's branch / slope / RR uniforms
   int bounce;
-  uint32_t pid;
+  uint32_t pid;          // result slot: caller-ray index, or s * n_local + lp (render)
   PathRng rng;
 };
 
@@ -213,16 +218,6 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
   }
 }
 
-// One free-flight segment plus the scattering event at its end.
-// Returns true when the path has terminated.
-//
-// SIMT structure: a single exit and explicit warp re-convergence
-// (__syncwarp over the lanes that entered, `amask`) after each stage --
-// flight, NEE, phase sampling.  Without it the lanes that escape / take
-// the other mixture branch are not re-joined until the function ends and
-// every later stage runs once per lane group (measured: 5.6 active lanes
-// per warp instruction).  Finished lanes stay predicated off inside the
-// stages but still pass every barrier.
 template <int kMode>
 __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev& ps,
                                                PathState& st, Counters& cn, unsigned amask,
@@ -230,20 +225,23 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
                                                float sig_known, bool done, float u_br,
                                                float u_s2, float u_rr);
 
+// Stage 1 of a segment: draw the segment's uniforms and fly to the next real
+// collision (transport.py:144-297).  Returns true on a collision (state kept
+// in st.cpos / st.ck / st.csig for the scatter stage); on escape / absorption
+// the environment term is added and false is returned (path finished).
 // kMode: 0 single plane (analytic), 1 general shells (tracking), 2 grid field
 template <int kMode>
-__device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& ps, PathState& st,
-                                             Counters& cn, unsigned amask) {
+__device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, Counters& cn) {
   cn.v[kStSegments]++;
   U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
-  float u_fl = u01(b.x), u_br = u01(b.y), u_s2 = u01(b.z), u_rr = u01(b.w);
-  int k = 0;
-  V3 pos = st.pos;
-  bool done = false;
-  float sig_dir = 0.0f;   // sigma(dir): in the plane frame this is sigma(wo)
-  constexpr bool kPlanar = kMode == 0;
-  // ---- stage 1: free flight (transport.py:144-297)
-  if (kMode == 2) {
+  float u_fl = u01(b.x);
+  st.u_br = u01(b.y);
+  st.u_s2 = u01(b.z);
+  st.u_rr = u01(b.w);
+  st.ck = 0;
+  st.csig = -1.0f;
+  int outcome;
+  if constexpr (kMode == 2) {
     const PathRng& r = st.rng;
     uint32_t seg = (uint32_t)st.bounce;
     GridWalk w = grid_walk(sc.grid, sc.media[0],
@@ -251,50 +249,52 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
                            st.dir, false, INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)w.steps;
     cn.v[kStViolations] += (uint32_t)w.violations;
-    pos = w.pos;
-    if (w.outcome == kEscaped) {
-      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
-      cn.v[kStEscaped]++;
-      done = true;
-    } else if (w.outcome == kAbsorbed) {
-      cn.v[kStAbsorbed]++;
-      done = true;
-    }
-  } else if (kPlanar) {
+    st.cpos = w.pos;
+    outcome = w.outcome;
+  } else if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
-    sig_dir = sig;
+    st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl);
-    pos = fl.pos;
-    if (fl.outcome == kEscaped) {
-      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
-      cn.v[kStEscaped]++;
-      done = true;
-    } else if (fl.outcome == kAbsorbed) {
-      cn.v[kStAbsorbed]++;
-      done = true;
-    }
+    st.cpos = fl.pos;
+    outcome = fl.outcome;
   } else {
     WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false, INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
-    pos = w.pos;
-    k = max(w.prim, 0);
-    if (w.steps < 0) {
-      cn.v[kStCapped]++;
-      done = true;
-    } else if (w.outcome == kEscaped) {
-      st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
-      cn.v[kStEscaped]++;
-      done = true;
-    } else if (w.outcome == kAbsorbed) {
-      cn.v[kStAbsorbed]++;
-      done = true;
-    }
+    st.cpos = w.pos;
+    st.ck = max(w.prim, 0);
+    outcome = w.steps < 0 ? -1 : w.outcome;
   }
-  __syncwarp(amask);
+  if (outcome == kEscaped) {
+    st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
+    cn.v[kStEscaped]++;
+    return false;
+  }
+  if (outcome == kAbsorbed) {
+    cn.v[kStAbsorbed]++;
+    return false;
+  }
+  if (outcome < 0) {
+    cn.v[kStCapped]++;
+    return false;
+  }
+  return true;
+}
+
+// Stages 2-3 at the collision found by flight_stage: local medium / frame,
+// then NEE, phase sampling, depth cap, RR.  Returns true when the path ends.
+//
+// SIMT structure: single exits and explicit warp re-convergence
+// (__syncwarp over the participating lanes) between stages.  Without it the
+// lanes that escape / take the other mixture branch are not re-joined until
+// the function ends and every later stage runs once per lane group
+// (measured: 5.6 active lanes per warp instruction).
+template <int kMode>
+__device__ __forceinline__ bool scatter_stage(const SceneDev& sc, const PassDev& ps,
+                                              PathState& st, Counters& cn, unsigned amask) {
+  V3 pos = st.cpos;
   if constexpr (kMode == 2) {
-    // local medium and frame of the grid field at the collision
     TriSample fs = trilinear<true>(sc.grid.sdf, sc.grid.n_sdf,
                                    grid_coord(sc.grid, pos, sc.grid.inv_h_sdf),
                                    sc.grid.inv_h_sdf);
@@ -302,13 +302,13 @@ __device__ __forceinline__ bool path_segment(const SceneDev& sc, const PassDev& 
     MediumK mg = grid_medium(sc.media[0], sg, sc.grid.k_xy, sc.grid.k_z);
     float gn2 = dot3(fs.grad, fs.grad);
     V3 nrm = gn2 > 0.0f ? mul3(fs.grad, frsqrt(gn2)) : v3(0.0f, 0.0f, 1.0f);
-    return scatter_stages<kMode>(sc, ps, st, cn, amask, mg, frame_about(nrm), pos, -1.0f, done,
-                                 u_br, u_s2, u_rr);
+    return scatter_stages<kMode>(sc, ps, st, cn, amask, mg, frame_about(nrm), pos, -1.0f, false,
+                                 st.u_br, st.u_s2, st.u_rr);
   } else {
-    V3 nrm = kPlanar ? v3(0.0f, 0.0f, 1.0f) : prim_normal(sc.prims[k], pos);
-    // sigma(dir) from the flight is sigma(wo) only in the (identity) plane frame
-    return scatter_stages<kMode>(sc, ps, st, cn, amask, sc.media[k], frame_about(nrm), pos,
-                                 kPlanar ? sig_dir : -1.0f, done, u_br, u_s2, u_rr);
+    V3 nrm = kMode == 0 ? v3(0.0f, 0.0f, 1.0f) : prim_normal(sc.prims[st.ck], pos);
+    return scatter_stages<kMode>(sc, ps, st, cn, amask, sc.media[st.ck], frame_about(nrm), pos,
+                                 kMode == 0 ? st.csig : -1.0f, false, st.u_br, st.u_s2,
+                                 st.u_rr);
   }
 }
 
@@ -384,6 +384,76 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
   return done;
 }
 
+// Start the path with index `my` in lane state st (raygen, render.py:149-160
+// keying); returns false for tile padding (no path).
+template <bool kCallerRays>
+__device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps, PathState& st,
+                                           uint32_t my) {
+  st.pid = my;
+  st.rng.k0 = ps.k0;
+  st.rng.k1 = ps.k1;
+  st.T = v3(1.0f, 1.0f, 1.0f);
+  st.L = v3(0.0f, 0.0f, 0.0f);
+  st.bounce = 0;
+  if (kCallerRays) {
+    st.rng.pixel = ps.pix[my];
+    st.rng.sample = ps.smp[my];
+    st.pos = v3(ps.org[my], ps.org[ps.n_paths + my], ps.org[2u * ps.n_paths + my]);
+    st.dir = v3(ps.dir[my], ps.dir[ps.n_paths + my], ps.dir[2u * ps.n_paths + my]);
+    return true;
+  }
+  uint32_t lp = my / ps.S;
+  uint32_t s = my - lp * ps.S;
+  // sample-major result slots: accumulate_kernel reads them coalesced
+  st.pid = s * ps.n_local + lp;
+  int pixel = local_to_pixel(sc, ps, lp);
+  if (pixel < 0) {
+    ps.rad[st.pid] = 0.0f;
+    ps.rad[ps.n_paths + st.pid] = 0.0f;
+    ps.rad[2u * ps.n_paths + st.pid] = 0.0f;
+    return false;
+  }
+  st.rng.pixel = (uint32_t)pixel;
+  st.rng.sample = ps.sample_begin + s;
+  U4 jb = rng_block(st.rng, kSegCamera, 0u);
+  camera_ray(sc, (uint32_t)pixel, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
+  return true;
+}
+
+__device__ __forceinline__ void finish_path(const PassDev& ps, const PathState& st, Counters& cn) {
+  float r = st.L.x, g = st.L.y, bl = st.L.z;
+  if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
+    cn.v[kStNonfinite]++;
+  }
+  ps.rad[st.pid] = r;
+  ps.rad[ps.n_paths + st.pid] = g;
+  ps.rad[2u * ps.n_paths + st.pid] = bl;
+}
+
+// Warp-level regeneration: the dead lanes of the warp take popc(dead) path
+// indices with one atomicAdd and start them.  Every lane must call this.
+template <bool kCallerRays>
+__device__ __forceinline__ void refill(const SceneDev& sc, const PassDev& ps, PathState& st,
+                                       bool& active, bool& exhausted, Counters& cn) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  unsigned need = __ballot_sync(full, !active && !exhausted);
+  if (!need) return;
+  int leader = __ffs(need) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(ps.counter, (unsigned)__popc(need));
+  base = __shfl_sync(full, base, leader);
+  if (!active && !exhausted) {
+    uint32_t my = base + (uint32_t)__popc(need & ((1u << lane) - 1u));
+    if (my < ps.n_paths) {
+      active = start_path<kCallerRays>(sc, ps, st, my);
+      if (active) cn.v[kStPaths]++;
+    } else {
+      exhausted = true;
+    }
+  }
+}
+
 template <int kMode, bool kCallerRays>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_constant__ SceneDev sc,
                                                        const __grid_constant__ PassDev ps) {
@@ -395,63 +465,36 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
   PathState st;
   bool active = false, exhausted = false;
   while (true) {
-    unsigned need = __ballot_sync(full, !active && !exhausted);
-    if (need) {
-      int leader = __ffs(need) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(ps.counter, (unsigned)__popc(need));
-      base = __shfl_sync(full, base, leader);
-      if (!active && !exhausted) {
-        uint32_t my = base + (uint32_t)__popc(need & ((1u << lane) - 1u));
-        if (my < ps.n_paths) {
-          st.pid = my;
-          st.rng.k0 = ps.k0;
-          st.rng.k1 = ps.k1;
-          st.T = v3(1.0f, 1.0f, 1.0f);
-          st.L = v3(0.0f, 0.0f, 0.0f);
-          st.bounce = 0;
-          if (kCallerRays) {
-            st.rng.pixel = ps.pix[my];
-            st.rng.sample = ps.smp[my];
-            st.pos = v3(ps.org[my], ps.org[ps.n_paths + my], ps.org[2u * ps.n_paths + my]);
-            st.dir = v3(ps.dir[my], ps.dir[ps.n_paths + my], ps.dir[2u * ps.n_paths + my]);
-            active = true;
-          } else {
-            uint32_t lp = my / ps.S;
-            uint32_t s = my - lp * ps.S;
-            int pixel = local_to_pixel(sc, ps, lp);
-            if (pixel < 0) {
-              ps.rad[my] = 0.0f;
-              ps.rad[ps.n_paths + my] = 0.0f;
-              ps.rad[2u * ps.n_paths + my] = 0.0f;
-            } else {
-              st.rng.pixel = (uint32_t)pixel;
-              st.rng.sample = ps.sample_begin + s;
-              U4 jb = rng_block(st.rng, kSegCamera, 0u);
-              camera_ray(sc, (uint32_t)pixel, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
-              active = true;
-            }
-          }
-          if (active) cn.v[kStPaths]++;
-        } else {
-          exhausted = true;
-        }
-      }
-    }
+    refill<kCallerRays>(sc, ps, st, active, exhausted, cn);
     if (__ballot_sync(full, active) == 0) {
       if (__ballot_sync(full, !exhausted) == 0) break;
       continue;
     }
-    unsigned amask = __ballot_sync(full, active);
+    bool coll = false;
     if (active) {
-      if (path_segment<kMode>(sc, ps, st, cn, amask)) {
-        float r = st.L.x, g = st.L.y, bl = st.L.z;
-        if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
-          cn.v[kStNonfinite]++;
-        }
-        ps.rad[st.pid] = r;
-        ps.rad[ps.n_paths + st.pid] = g;
-        ps.rad[2u * ps.n_paths + st.pid] = bl;
+      coll = flight_stage<kMode>(sc, st, cn);
+      if (!coll) {
+        finish_path(ps, st, cn);
+        active = false;
+      }
+    }
+    __syncwarp(full);
+    // second chance: lanes whose path just ended start the next one and fly
+    // it now, so the (expensive) scatter stage runs with as many lanes as
+    // possible
+    refill<kCallerRays>(sc, ps, st, active, exhausted, cn);
+    bool fresh = active && !coll;
+    if (fresh) {
+      coll = flight_stage<kMode>(sc, st, cn);
+      if (!coll) {
+        finish_path(ps, st, cn);
+        active = false;
+      }
+    }
+    unsigned smask = __ballot_sync(full, active && coll);
+    if (active && coll) {
+      if (scatter_stage<kMode>(sc, ps, st, cn, smask)) {
+        finish_path(ps, st, cn);
         active = false;
       }
     }
@@ -472,12 +515,15 @@ __global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__
   if (lp >= n_local) return;
   int pixel = local_to_pixel(sc, ps, lp);
   if (pixel < 0) return;
-  const float* r = ps.rad + (size_t)lp * ps.S;
+  // fixed sample order; slot s * n_local + lp makes each sample's loads
+  // coalesced across the warp's pixels
+  const float* r = ps.rad + lp;
   float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
   for (uint32_t s = 0; s < ps.S; ++s) {
-    s0 += r[s];
-    s1 += r[ps.n_paths + s];
-    s2 += r[2u * ps.n_paths + s];
+    size_t o = (size_t)s * n_local;
+    s0 += __ldg(r + o);
+    s1 += __ldg(r + ps.n_paths + o);
+    s2 += __ldg(r + 2u * ps.n_paths + o);
   }
   float* a = accum + (size_t)pixel * 3;
   a[0] += s0 * inv_spp;
@@ -908,6 +954,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.S = S;
     ps.sample_begin = s_begin + s0;
     ps.n_paths = (uint32_t)(n_local * S);
+    ps.n_local = (uint32_t)n_local;
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
     if (stats) MF_CUDA(cudaEventRecord(ev[0], st));
     rc = launch_paths(sc, ps, false, st);
