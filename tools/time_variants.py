@@ -9,13 +9,13 @@ import paper_2603_00280_b200 as mf
 from paper_2603_00280_b200 import configs
 torch.cuda.set_device(0)
 def tm(scene, spp, seed, mb, reps=10):
+    # path-kernel time from the library's own CUDA events (mf_stats)
     out = torch.empty((scene.camera.height, scene.camera.width, 3), device="cuda")
     for _ in range(3): mf.render_device(scene, spp, seed, max_bounces=mb, out=out)
-    torch.cuda.synchronize()
-    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(reps):
-        s.record(); mf.render_device(scene, spp, seed, max_bounces=mb, out=out); e.record(); torch.cuda.synchronize(); ts.append(s.elapsed_time(e))
+        _, st = mf.render_device(scene, spp, seed, max_bounces=mb, out=out, stats=True)
+        ts.append(st["path_kernel_ms"])
     return min(ts), float(out.mean())
 c2 = configs.config2_scene(); c3 = configs.config3_scene(256, 256)
 t2, m2 = tm(c2, 64, 1, 16); t3, m3 = tm(c3, 64, 2, 32, reps=5)
