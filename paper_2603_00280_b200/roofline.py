@@ -48,12 +48,13 @@ EVENTS = {
     # (log(u), log_ndtr, division, inv_log_ndtr, position update)
     "segments": (212, 12.5),
     # real scatter: frame + sigma(wo) + phase sample (sigma_b, branch remap,
-    # mixture pdf, vNDF weight, 50/50 Beckmann (55 + 110 base) / hemisphere
-    # (43) proposal, rotation, throughput, RR)
-    "scatters": (275, 26),
+    # mixture pdf, vNDF weight, 50/50 Beckmann (55 + 110 base + one residual
+    # evaluation 57 from the table guess) / hemisphere (43) proposal,
+    # rotation, throughput, RR)
+    "scatters": (304, 28),
     # next-event estimation: phase_eval + sigma(wl) + closed-form / walk Tr
     "nee": (157, 15),
-    # one Newton iteration of the visible-slope inversion
+    # each further Newton iteration of the visible-slope inversion
     "slope_iters": (57, 3.5),
     # one delta / ratio tracking step on a curved shell (majorant, sample,
     # tentative extinction)
