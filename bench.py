@@ -252,7 +252,7 @@ def run_ours(args):
                                         _lib.stream_handle(torch, dev)))
         _, st = mf.render_device(scene, spp_total, 1, max_bounces=16, rank=0, nranks=n,
                                  shard=shard, out=out, stats=True, c_scene=cs)
-        rl = roofline.roofline(st, st["path_kernel_ms"], fpk.value, spk.value)
+        rl = roofline.roofline(st, st["path_kernel_ms"], fpk.value, spk.value, planar=True)
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_path_kernel.json")
         if os.path.exists(prof):

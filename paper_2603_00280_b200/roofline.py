@@ -62,19 +62,28 @@ EVENTS = {
 }
 
 
-def algorithmic_ops(stats):
+# single-plane scenes reuse sigma(dir) of the flight as sigma(wo) at the
+# scatter (identity frame) and precompute sigma(w_sun) once per render: that
+# work is not repeated per event
+PLANAR_DISCOUNT = {"scatters": PRIMS["proj_area"], "nee": PRIMS["proj_area"]}
+
+
+def algorithmic_ops(stats, planar=False):
     """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters."""
     f = s = 0.0
     for ev, (cf, cs) in EVENTS.items():
+        if planar and ev in PLANAR_DISCOUNT:
+            cf -= PLANAR_DISCOUNT[ev][0]
+            cs -= PLANAR_DISCOUNT[ev][1]
         n = float(stats.get(ev, 0))
         f += n * cf
         s += n * cs
     return f, s
 
 
-def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst):
+def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, planar=False):
     """Achieved issue rates and the roofline fraction of the path kernel."""
-    f, s = algorithmic_ops(stats)
+    f, s = algorithmic_ops(stats, planar)
     t = kernel_ms * 1e-3
     af = f / t / 1e9
     asf = s / t / 1e9
