@@ -16,6 +16,20 @@ inline double log_ndtr_host(double u) { return std::log(0.5 * std::erfc(-u / std
 
 // max over directions of sigma(w) in the local frame (exact majorant
 // factor; replaces the direction-free bound of ndf.py:189-194)
+// sigma(w) depends on cos(theta) only (ax == ay) and is non-increasing in
+// it: then the direction factor of a chord majorant is its start value
+inline int area_monotone_host(const MediumK& m) {
+  if (m.ax != m.ay) return 0;
+  float prev = INFINITY;
+  for (int i = 0; i <= 4096; ++i) {
+    float c = -1.0f + 2.0f * (float)i / 4096.0f;
+    float v = proj_area(m, v3(std::sqrt(std::max(0.0f, 1.0f - c * c)), 0.0f, c));
+    if (v > prev * (1.0f + 1e-6f)) return 0;
+    prev = v;
+  }
+  return 1;
+}
+
 inline double sigma_max_host(const MediumK& m) {
   double best = 0.0;
   const int nt = 2048, np = 16;
@@ -60,6 +74,7 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     // exact majorant factor, needed only by the tracking walker (curved shells)
     bool planar_only = in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE;
     sc.mx[j].sig_max = planar_only ? mk.sig_bound : (float)sigma_max_host(mk);
+    sc.mx[j].area_monotone = area_monotone_host(mk);
     sc.mx[j].lphi_hi = (float)log_ndtr_host(3.0);
     sc.mx[j].lphi_lo_col = (float)log_ndtr_host(-6.0);
     sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);

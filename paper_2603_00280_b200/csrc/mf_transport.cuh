@@ -33,8 +33,18 @@ struct PrimDev {
   float radius;
 };
 
+// Tracking-step length inside a band, in units of the medium's sigma.  The
+// per-step majorant is exact over [0, step] whatever the length; shorter
+// steps tighten it (fewer null collisions) but cost more majorant
+// evaluations.  Measured on config 3 (B200): 0.5 -> 16.0 ms, 1 -> 12.9,
+// 2 -> 11.9, 3 -> 12.2, 4.5 -> 13.2 ms.
+#ifndef MF_STEP_FRAC
+#define MF_STEP_FRAC 2.0f
+#endif
+
 struct MediumExtra {
   float sig_max;       // max_w sigma(w), majorant factor for curved shells
+  int area_monotone;   // sigma(w) depends on cos(theta) only and decreases with it
   float lphi_hi;       // log Phi(3)   (collision / ratio upper edge)
   float lphi_lo_col;   // log Phi(-6)  (collision absorption edge)
   float lphi_lo_rat;   // log Phi(-3)  (ratio lower edge)
@@ -254,10 +264,12 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
     bool all_done = true;
     float maj = 0.0f;
     float cap = INFINITY;
+    float fs[kMaxPrims];
     for (int j = 0; j < sc.n_prims; ++j) {
       const PrimDev& p = sc.prims[j];
       const MediumK& m = sc.media[j];
       float f = prim_field(p, pos);
+      fs[j] = f;
       float lo = lo_mult * m.sigma, hi = 3.0f * m.sigma;
       if (!ratio && f < lo) {
         w.outcome = kAbsorbed;
@@ -266,16 +278,44 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
       }
       if (f >= lo && f <= hi) {
         any_band = true;
-        float half = 0.5f * m.sigma;
-        float fb = fmaxf(f - half, lo);
-        maj += mills(fb * m.inv_sigma) * m.inv_sigma * sc.mx[j].sig_max;
-        cap = fminf(cap, half);
+        cap = fminf(cap, MF_STEP_FRAC * m.sigma);
       } else {
         float g = level_distance(p, pos, dir, f > hi ? hi : lo);
         gap_min = fminf(gap_min, g);
         if (g < INFINITY) all_done = false;
         cap = fminf(cap, fmaxf(g, sc.min_skip));
       }
+    }
+    // majorant over the step [0, cap] (transport.py:226-231 with exact
+    // geometry): min of f along the step (planes: linear; spheres: closest
+    // approach) and, for media whose sigma(w) decreases with cos(theta), the
+    // direction factor at the step start (cos(theta) grows along a chord)
+    for (int j = 0; j < sc.n_prims; ++j) {
+      const PrimDev& p = sc.prims[j];
+      const MediumK& m = sc.media[j];
+      float f = fs[j];
+      float lo = lo_mult * m.sigma, hi = 3.0f * m.sigma;
+      if (!(f >= lo && f <= hi)) continue;
+      float fmin, dirf;
+      if (p.shape == 0) {
+        fmin = f + cap * fminf(dir.z, 0.0f);
+        dirf = proj_area(m, dir);
+      } else {
+        V3 oc = sub3(pos, p.c);
+        float b = dot3(oc, dir);
+        float r2 = dot3(oc, oc);
+        float ts = fminf(fmaxf(-b, 0.0f), cap);
+        fmin = fsqrt(fmaxf(fmaf(ts, ts + 2.0f * b, r2), 0.0f)) - p.radius;
+        if (sc.mx[j].area_monotone) {
+          float c = b * frsqrt(fmaxf(r2, 1e-30f));
+          c = fminf(fmaxf(c, -1.0f), 1.0f);
+          dirf = proj_area(m, v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c)) * 1.0001f;
+        } else {
+          dirf = sc.mx[j].sig_max;
+        }
+      }
+      float fb = fmaxf(fmin - 1e-6f * (1.0f + fabsf(f)), lo);
+      maj += mills(fb * m.inv_sigma) * m.inv_sigma * dirf;
     }
     if (!any_band) {
       if (all_done || travel + gap_min >= t_max) {
