@@ -229,8 +229,8 @@ def run_ours(args):
     if n > 1:
         dist.barrier()
     e2e_steps = max(1, min(args.steps, 10))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+
+    def e2e_step():
         if n == 1:
             mf.render(scene, 64, 1, max_bounces=16)
         else:
@@ -238,6 +238,15 @@ def run_ours(args):
             if rank == 0:
                 img.cpu()
             torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if n > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
     e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if n > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

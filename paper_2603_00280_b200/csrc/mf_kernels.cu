@@ -708,7 +708,27 @@ struct Scratch {
   unsigned long long* stats = nullptr;
 };
 
+// The device's default stream-ordered pool releases freed memory back to the
+// driver at every synchronisation unless told otherwise; re-mapping the
+// ~50 MB of per-path scratch then costs milliseconds per render.  Keep it.
+int retain_pool_memory() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && done[dev]) return MF_OK;
+  cudaMemPool_t pool;
+  MF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  MF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  if (dev < 64) done[dev] = true;
+  return MF_OK;
+}
+
 int scratch_alloc(Scratch* s, size_t n_paths, cudaStream_t st) {
+  int rc = retain_pool_memory();
+  if (rc) return rc;
   MF_CUDA(cudaMallocAsync((void**)&s->rad, std::max<size_t>(n_paths, 1) * 3 * sizeof(float), st));
   MF_CUDA(cudaMallocAsync((void**)&s->counter, 64 * sizeof(unsigned int), st));
   MF_CUDA(cudaMallocAsync((void**)&s->stats, kStCount * sizeof(unsigned long long), st));

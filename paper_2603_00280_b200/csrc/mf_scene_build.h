@@ -5,7 +5,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "mf_prepare.h"
 #include "mf_transport.cuh"
@@ -47,6 +50,30 @@ inline double sigma_max_host(const MediumK& m) {
   return best * 1.01 + 1e-6;
 }
 
+// (sig_max, area_monotone) of a roughness triple, memoised: the dense
+// direction scans above cost milliseconds and scenes are rebuilt per call
+inline void direction_factors(const MediumK& m, float* sig_max, int* monotone) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, float, float, float>, std::pair<float, int>> memo;
+  auto key = std::make_tuple(m.kind, m.ax, m.ay, m.az);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) {
+      *sig_max = it->second.first;
+      *monotone = it->second.second;
+      return;
+    }
+  }
+  float sm = (float)sigma_max_host(m);
+  int mono = area_monotone_host(m);
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() > 4096) memo.clear();
+  memo[key] = std::make_pair(sm, mono);
+  *sig_max = sm;
+  *monotone = mono;
+}
+
 inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
   if (in.n_prims < 0 || in.n_prims > MF_MAX_PRIMS)
     return (*err = std::string("n_prims out of range"), MF_ERR_PARAM);
@@ -73,8 +100,12 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     min_sigma = std::min(min_sigma, s);
     // exact majorant factor, needed only by the tracking walker (curved shells)
     bool planar_only = in.n_prims == 1 && in.prims[0].shape == MF_SHAPE_PLANE;
-    sc.mx[j].sig_max = planar_only ? mk.sig_bound : (float)sigma_max_host(mk);
-    sc.mx[j].area_monotone = area_monotone_host(mk);
+    if (planar_only) {
+      sc.mx[j].sig_max = mk.sig_bound;
+      sc.mx[j].area_monotone = 0;
+    } else {
+      direction_factors(mk, &sc.mx[j].sig_max, &sc.mx[j].area_monotone);
+    }
     sc.mx[j].lphi_hi = (float)log_ndtr_host(3.0);
     sc.mx[j].lphi_lo_col = (float)log_ndtr_host(-6.0);
     sc.mx[j].lphi_lo_rat = (float)log_ndtr_host(-3.0);

@@ -82,7 +82,13 @@ def launches(path):
         a[0] += 1
         a[1] += to_num(r[mi])
     tot = sum(a[1] for a in agg.values())
-    return {k: {"launches": a[0], "total_ns": a[1], "mean_ns": a[1] / a[0], "share": a[1] / tot}
+    # the render step proper: our kernels minus the one-off peak
+    # microbenchmarks (roofline denominators) and torch's L2-flush fills
+    step = {k: a for k, a in agg.items() if not k.startswith("at::") and "peak_" not in k
+            and "slope_table" not in k}
+    st = sum(a[1] for a in step.values()) or 1.0
+    return {k: {"launches": a[0], "total_ns": a[1], "mean_ns": a[1] / a[0], "share": a[1] / tot,
+                "step_share": (a[1] / st) if k in step else None}
             for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1])}
 
 
