@@ -3,6 +3,7 @@ without a GPU).  `python -m paper_2603_00280_b200.build`"""
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -12,9 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "mf_kernels.cu")
 OUT = os.path.join(HERE, "libmacrofacet_b200.so")
-DEPS = [os.path.join(HERE, "csrc", f) for f in
-        ("mf_kernels.cu", "mf_math.cuh", "mf_poly.inc", "mf_query.cuh", "mf_transport.cuh",
-         "mf_prepare.h")] + [os.path.join(ROOT, "include", "macrofacet_b200.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [
+    os.path.join(ROOT, "include", "macrofacet_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

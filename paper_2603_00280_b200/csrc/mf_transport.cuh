@@ -213,8 +213,15 @@ MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, f
   float b = fminf(fmaxf(h_end, -s3), s3);
   if (a == b) return 1.0f;
   if (fabsf(c) < 1e-6f) return 0.0f;
-  float la = a >= s3 ? mx.lphi_hi : (a <= -s3 ? mx.lphi_lo_rat : log_ndtr(a * m.inv_sigma));
-  float lb = b >= s3 ? mx.lphi_hi : (b <= -s3 ? mx.lphi_lo_rat : log_ndtr(b * m.inv_sigma));
+  // both ends through one copy of log_ndtr (I-cache)
+  float la = 0.0f, lb = 0.0f, e = a;
+#pragma unroll 1
+  for (int i = 0; i < 2; ++i) {
+    float l = e >= s3 ? mx.lphi_hi : (e <= -s3 ? mx.lphi_lo_rat : log_ndtr(e * m.inv_sigma));
+    la = i == 0 ? l : la;
+    lb = l;
+    e = b;
+  }
   return expf(-sig / fabsf(c) * fabsf(lb - la));
 }
 
