@@ -225,6 +225,33 @@ int mf_transmittance(const mf_scene* scene, const double origin[3], const double
  * Writes d_majorant_out (n_maj^3 floats). */
 int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Multi-GPU exchange: the one collective of a sharded
+ * render, the sum of the per-rank accumulation buffers onto `root`.  The
+ * reference has no multi-process path (its render() joins a thread pool,
+ * render.py:168-176); these calls replace that join across GPUs.
+ *
+ * `comm` is an ncclComm_t.  A caller that owns one passes it directly; the
+ * helpers below create one from a unique id that the caller distributes
+ * (any out-of-band channel, e.g. a torch.distributed broadcast).  NCCL is
+ * loaded at run time (the process's already-loaded libnccl.so.2 when there
+ * is one), so the library itself has no link-time NCCL dependency.
+ *
+ * mode MF_REDUCE_NCCL    : one in-place ncclReduce(sum, fp32) -- exact and
+ *                          order-free under tile sharding (disjoint pixels)
+ * mode MF_REDUCE_ORDERED : root receives every rank's buffer (grouped
+ *                          ncclSend/ncclRecv into a stream-ordered scratch)
+ *                          and sums them in rank order 0..n-1 in one
+ *                          kernel -- bit-reproducible for a fixed rank
+ *                          count under sample sharding too
+ * All calls are stream-ordered on `stream`; d_buf on root holds the sum. */
+enum mf_reduce_mode { MF_REDUCE_NCCL = 0, MF_REDUCE_ORDERED = 1 };
+#define MF_COMM_ID_BYTES 128
+int mf_comm_unique_id(unsigned char id_out[MF_COMM_ID_BYTES]);
+int mf_comm_init(const unsigned char id[MF_COMM_ID_BYTES], int nranks, int rank, void** comm_out);
+int mf_comm_destroy(void* comm);
+int mf_reduce(void* comm, float* d_buf, size_t count, int root, int mode, void* stream);
+
 /* Issue-rate peaks of this device measured by microbenchmark kernels
  * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane
  * instructions per second: the FP32 / SFU roofline denominators. */

@@ -23,6 +23,8 @@ MF_MAX_PRIMS = 8
 MF_MAX_MEDIA = 8
 
 KIND = {"beckmann": 0, "ggx": 1, "generalized": 2}
+REDUCE_NCCL, REDUCE_ORDERED = 0, 1
+COMM_ID_BYTES = 128
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
 SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID = 0, 1, 2
 SHARD_TILES, SHARD_SAMPLES = 0, 1
@@ -115,6 +117,11 @@ SIGNATURES = {
     "mf_grid_majorant": (ctypes.c_int, [ctypes.POINTER(MfGridField), _vp, _vp]),
     "mf_measure_peaks": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), _vp]),
+    "mf_comm_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
+    "mf_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_void_p)]),
+    "mf_comm_destroy": (ctypes.c_int, [_vp]),
+    "mf_reduce": (ctypes.c_int, [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _vp]),
     "mf_last_error": (ctypes.c_char_p, []),
     "mf_abi_version": (ctypes.c_int, []),
     "mf_launch_count": (ctypes.c_uint64, []),

@@ -44,7 +44,7 @@ def needs_build():
 def build(force=False, verbose=False):
     if not force and not needs_build():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")

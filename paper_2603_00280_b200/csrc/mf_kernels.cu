@@ -1097,3 +1097,5 @@ int mf_transmittance(const mf_scene* scene, const double origin[3], const double
 }
 
 }  // extern "C"
+
+#include "mf_comm.cuh"

@@ -83,22 +83,39 @@ def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, 
 
 
 def render_sharded(scene: ShellScene, spp, seed, max_bounces=64, tile=32, shard="tiles",
-                   group=None, stats=False):
+                   group=None, stats=False, comm=None, ordered=False):
     """One rank's share of a multi-GPU render followed by a single NCCL
     sum-reduce of the fp32 accumulation buffers to rank 0.
     The kernel writes straight into the tensor NCCL sends, on the same
     stream.  Tile sharding leaves non-owned pixels at +0.0, so the reduce is
-    exact and the image is bit-identical for any rank count.  Returns the
-    (H, W, 3) tensor (complete on rank 0) and this rank's stats."""
+    exact and the image is bit-identical for any rank count.
+
+    The reduce runs through torch.distributed unless `comm` (a
+    `comm.NcclComm`, the library's own communicator, C ABI `mf_reduce`) is
+    given; `ordered=True` (needs `comm`) sums the ranks' buffers in rank
+    order on the root, which makes sample-sharded images bit-reproducible
+    for a fixed rank count.  Returns the (H, W, 3) tensor (complete on rank
+    0) and this rank's stats."""
     import torch.distributed as dist
 
-    rank = dist.get_rank(group)
-    nranks = dist.get_world_size(group)
+    if ordered and comm is None:
+        raise ParameterDomainError("ordered reduction needs the library communicator (comm=)")
+    rank = dist.get_rank(group) if comm is None else comm.rank
+    nranks = dist.get_world_size(group) if comm is None else comm.nranks
     img, st = render_device(scene, spp, seed, max_bounces=max_bounces, tile=tile, rank=rank,
                             nranks=nranks, shard=shard, stats=stats)
-    if nranks > 1:
-        dist.reduce(img, dst=0, op=dist.ReduceOp.SUM, group=group)
+    if comm is not None:
+        comm.reduce(img, root=0, ordered=ordered)
+    elif nranks > 1:
+        dist.reduce(img, dst=group_root(group), op=dist.ReduceOp.SUM, group=group)
     return img, st
+
+
+def group_root(group):
+    """Global rank of the group's rank 0 (the reduce destination)."""
+    import torch.distributed as dist
+
+    return 0 if group is None else dist.get_global_rank(group, 0)
 
 
 def sample_range(spp, rank, nranks):

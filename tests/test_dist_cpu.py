@@ -31,7 +31,27 @@ def _fake_pixels(w, h):
     return np.stack([np.sin(idx), np.cos(idx) ** 2, idx / (w * h)], axis=-1).astype(np.float32)
 
 
-def _worker(rank, world, port, shard, q):
+class _GlooOrderedComm:
+    """Stand-in for comm.NcclComm with mf_reduce's MF_REDUCE_ORDERED
+    semantics (root sums the ranks' buffers in rank order) over gloo."""
+
+    def __init__(self):
+        self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
+        self.calls = []
+
+    def reduce(self, t, root=0, ordered=False):
+        self.calls.append(ordered)
+        parts = [torch.empty_like(t) for _ in range(self.nranks)]
+        dist.all_gather(parts, t)
+        if self.rank == root:
+            acc = parts[0].clone()
+            for p in parts[1:]:
+                acc += p
+            t.copy_(acc)
+        return t
+
+
+def _worker(rank, world, port, shard, q, ordered=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     scene = configs.config2_scene(40, 24)
@@ -50,19 +70,22 @@ def _worker(rank, world, port, shard, q):
         return torch.from_numpy(img.reshape(h, w, 3)), ({"paths": 1} if stats else None)
 
     R.render_device = fake_render_device
-    img, _ = R.render_sharded(scene, 8, 1, tile=8, shard=shard)
+    comm = _GlooOrderedComm() if ordered else None
+    img, _ = R.render_sharded(scene, 8, 1, tile=8, shard=shard, comm=comm, ordered=ordered)
     if rank == 0:
         q.put(img.numpy().copy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shard", ["tiles", "samples"])
-def test_render_sharded_gloo_world2(shard):
+@pytest.mark.parametrize("shard,ordered", [("tiles", False), ("samples", False),
+                                           ("samples", True)])
+def test_render_sharded_gloo_world2(shard, ordered):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, shard, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shard, q, ordered))
+             for r in range(2)]
     for p in procs:
         p.start()
     img = q.get(timeout=90)
@@ -72,6 +95,12 @@ def test_render_sharded_gloo_world2(shard):
     full = _fake_pixels(40, 24).reshape(24, 40, 3)
     if shard == "tiles":
         assert np.array_equal(img, full)  # disjoint tiles: the reduce is exact
+    elif ordered:
+        # rank-order sum of the two halves, bit for bit
+        b0, e0 = R.sample_range(8, 0, 2)
+        b1, e1 = R.sample_range(8, 1, 2)
+        want = full * np.float32((e0 - b0) / 8) + full * np.float32((e1 - b1) / 8)
+        assert np.array_equal(img, want.astype(np.float32))
     else:
         np.testing.assert_allclose(img, full, rtol=1e-6, atol=1e-7)
 
@@ -82,3 +111,30 @@ def test_sample_ranges_partition():
             rs = [R.sample_range(spp, r, n) for r in range(n)]
             assert rs[0][0] == 0 and rs[-1][1] == spp
             assert all(rs[i][1] == rs[i + 1][0] for i in range(n - 1))
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_00280_b200 import _lib, comm
+
+    uid = comm.exchange_unique_id(_lib.load())
+    q.put((rank, bytes(uid)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_comm_unique_id_exchange_gloo_world2():
+    """NcclComm's unique-id exchange: rank 0 creates it through the C ABI
+    (mf_comm_unique_id, NCCL resolved at run time), both ranks hold it."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=90) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[0] == got[1] and len(got[0]) == 128 and any(got[0])
