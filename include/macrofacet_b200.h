@@ -22,6 +22,7 @@
 #ifndef MACROFACET_B200_H
 #define MACROFACET_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -217,6 +218,30 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
 int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],
                      int64_t n, uint64_t seed, uint64_t stream_id, double* mean, double* se,
                      void* stream);
+
+/* ---------------------------------------------------------------------
+ * Closed-form curves of one medium on the device (the `curves` CLI command,
+ * cli.py:132-175, and the device validation suites, validate.py:57-209).
+ * Directions are SoA float32 device arrays d_x, d_y, d_z (unit vectors,
+ * local frame); params (host doubles) = {wo_x, wo_y, wo_z, z0}.
+ *   MF_CURVE_LAMBDA          Lambda(w) = sigma(w) / w_z   generalized_lambda, ndf.py:120-144
+ *   MF_CURVE_PROJECTED_AREA  sigma(w)                     projected_area_dir, ndf.py:174-186
+ *   MF_CURVE_NDF             D(w)                         generalized_ndf_dir / beckmann / ggx
+ *   MF_CURVE_VNDF            D_wo(w), wo = params[0..2]   vndf_eval, ndf.py:299-315
+ *   MF_CURVE_TRANSMITTANCE   closed-form planar Tr along wo from field value
+ *                            h0 = params[3] to h1 = d_x[i]
+ *                            (planar_transmittance, medium.py:98-124; d_y/d_z unused)
+ * Transmittance raises MF_ERR_UNSUPPORTED for GGX or |wo_z| < 1e-12, as the
+ * reference does. */
+enum mf_curve_kind {
+  MF_CURVE_LAMBDA = 0,
+  MF_CURVE_PROJECTED_AREA = 1,
+  MF_CURVE_NDF = 2,
+  MF_CURVE_VNDF = 3,
+  MF_CURVE_TRANSMITTANCE = 4
+};
+int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d_y,
+             const float* d_z, int64_t n, const double params[4], float* d_out, void* stream);
 
 /* Build the majorant grid of a grid field: for every one of the n_maj^3
  * cells an upper bound of the extinction over the cell and over all

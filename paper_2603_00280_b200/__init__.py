@@ -8,6 +8,9 @@ kernels behind the C ABI in include/macrofacet_b200.h.  No CPU fallback."""
 __version__ = "0.1.0"
 
 from .core import Frame, build_frame, dot, normalize
+from .curves import (generalized_lambda, generalized_lambda_dir, generalized_ndf,
+                     generalized_ndf_dir, planar_transmittance, projected_area,
+                     projected_area_dir, vndf_eval)
 from .errors import (ConfigError, DegenerateVisibilityError, GrazingSingularityError,
                      InternalConsistencyError, IoError, MacrofacetError, NumericFailureError,
                      ParameterDomainError, UnsupportedGeometryError)

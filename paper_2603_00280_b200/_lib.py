@@ -24,6 +24,7 @@ MF_MAX_MEDIA = 8
 
 KIND = {"beckmann": 0, "ggx": 1, "generalized": 2}
 REDUCE_NCCL, REDUCE_ORDERED = 0, 1
+CURVE = {"lambda": 0, "projected-area": 1, "ndf": 2, "vndf": 3, "transmittance": 4}
 COMM_ID_BYTES = 128
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
 SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID = 0, 1, 2
@@ -122,6 +123,8 @@ SIGNATURES = {
                                     ctypes.POINTER(ctypes.c_void_p)]),
     "mf_comm_destroy": (ctypes.c_int, [_vp]),
     "mf_reduce": (ctypes.c_int, [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _vp]),
+    "mf_curve": (ctypes.c_int, [ctypes.POINTER(MfMedium), ctypes.c_int, _vp, _vp, _vp,
+                                ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _vp, _vp]),
     "mf_last_error": (ctypes.c_char_p, []),
     "mf_abi_version": (ctypes.c_int, []),
     "mf_launch_count": (ctypes.c_uint64, []),

@@ -72,6 +72,40 @@ enum StatIdx {
 };
 
 // ---------------------------------------------------------------------------
+// closed-form curves (mf_curve)
+
+struct CurveArgs {
+  MediumK m;
+  int kind;
+  const float *x, *y, *z;
+  int64_t n;
+  V3 wo;
+  float z0;
+  float sig_wo;   // sigma(wo) (VNDF) or Lambda(wo) (transmittance)
+  float* out;
+};
+
+__global__ void __launch_bounds__(256) curve_kernel(const __grid_constant__ CurveArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float r;
+    if (a.kind == MF_CURVE_TRANSMITTANCE) {
+      // planar_transmittance (medium.py:98-124): exp(-Lambda * dlog Phi)
+      float h1 = __ldg(a.x + i);
+      float dl = log_ndtr(h1 * a.m.inv_sigma) - log_ndtr(a.z0 * a.m.inv_sigma);
+      r = expf(-a.sig_wo * dl);
+    } else {
+      V3 w = v3(__ldg(a.x + i), __ldg(a.y + i), __ldg(a.z + i));
+      if (a.kind == MF_CURVE_LAMBDA) r = proj_area(a.m, w) / w.z;
+      else if (a.kind == MF_CURVE_PROJECTED_AREA) r = proj_area(a.m, w);
+      else if (a.kind == MF_CURVE_NDF) r = ndf(a.m, w);
+      else r = vndf_eval(a.m, w, a.wo, a.sig_wo);
+    }
+    a.out[i] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // config-1 query kernel
 
 struct QueryArgs {
@@ -887,6 +921,58 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
   int64_t blocks = (n + 255) / 256;
   int grid = (int)std::min<int64_t>(blocks, (int64_t)sms * 8);
   query_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d_y,
+             const float* d_z, int64_t n, const double params[4], float* d_out, void* stream) {
+  if (!medium || !params || (n > 0 && (!d_x || !d_out))) return fail(MF_ERR_PARAM, "null argument");
+  if (kind < MF_CURVE_LAMBDA || kind > MF_CURVE_TRANSMITTANCE)
+    return fail(MF_ERR_PARAM, "unknown curve kind " + std::to_string(kind));
+  if (kind != MF_CURVE_TRANSMITTANCE && n > 0 && (!d_y || !d_z))
+    return fail(MF_ERR_PARAM, "direction arrays are null");
+  if (n < 0) return fail(MF_ERR_PARAM, "n must be >= 0");
+  CurveArgs a;
+  std::memset(&a, 0, sizeof(a));
+  std::string err;
+  int rc = prepare_medium(*medium, &a.m, &err);
+  if (rc) return fail(rc, err);
+  a.kind = kind;
+  a.x = d_x;
+  a.y = d_y;
+  a.z = d_z;
+  a.n = n;
+  a.out = d_out;
+  double wx = params[0], wy = params[1], wz = params[2];
+  double wn = std::sqrt(wx * wx + wy * wy + wz * wz);
+  if (kind == MF_CURVE_VNDF || kind == MF_CURVE_TRANSMITTANCE) {
+    if (!(wn > 0.0) || !std::isfinite(wn)) return fail(MF_ERR_PARAM, "wo must be a finite non-zero vector");
+    wx /= wn;
+    wy /= wn;
+    wz /= wn;
+  }
+  a.wo = v3((float)wx, (float)wy, (float)wz);
+  a.z0 = (float)params[3];
+  if (kind == MF_CURVE_VNDF) {
+    a.sig_wo = proj_area(a.m, a.wo);
+    if (!(a.sig_wo >= 1e-12f))
+      return fail(MF_ERR_DEGENERATE, "sigma(wo) < 1e-12: visible normals undefined");
+  }
+  if (kind == MF_CURVE_TRANSMITTANCE) {
+    if (std::fabs(wz) < 1e-12)
+      return fail(MF_ERR_UNSUPPORTED, "planar transmittance is undefined at cos(theta) = 0");
+    if (a.m.kind == kGGX)
+      return fail(MF_ERR_UNSUPPORTED, "closed-form transmittance covers the erf-family lambda only");
+    a.sig_wo = proj_area(a.m, a.wo) / a.wo.z;
+  }
+  if (n == 0) return MF_OK;
+  int dev = 0, sms = 148;
+  MF_CUDA(cudaGetDevice(&dev));
+  MF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+  curve_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   g_launches++;
   MF_CUDA(cudaGetLastError());
   return MF_OK;

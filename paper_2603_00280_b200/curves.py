@@ -1,0 +1,148 @@
+"""Closed-form curves of the microflake statistics, evaluated on the GPU
+(C ABI `mf_curve`, `curve_kernel`).
+
+Reference-named functions (same arguments and meaning, float64 numpy in
+and out, fp32 device arithmetic):
+
+    generalized_lambda(theta, phi, a3)            ndf.py:138-144
+    generalized_lambda_dir(w, a3)                 ndf.py:120-135
+    projected_area(theta, phi, a3)                ndf.py:174-177
+    projected_area_dir(wo, kind, a3)              ndf.py:180-186
+    generalized_ndf(theta_m, phi_m, a3)           ndf.py:227-229
+    generalized_ndf_dir(wm, a3)                   ndf.py:209-224
+    ndf_dir(wm, kind, a3)                         ndf.py:85-103 / 209-224 by kind
+    vndf_eval(wm, wo, kind, a3)                   ndf.py:299-315 (one wo per call)
+    planar_transmittance(h0, h1, theta, phi, medium)   medium.py:98-124
+
+The erf-family functions take the roughness triple as given (az = 0 is the
+Beckmann height-field limit), as the reference does.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import GrazingSingularityError, ParameterDomainError, UnsupportedGeometryError
+from .medium import MacrofacetMedium, to_c_medium
+from .ndf import NdfKind, RoughnessTriple
+
+
+def _sph_dir(theta, phi):
+    theta = np.asarray(theta, dtype=np.float64)
+    phi = np.asarray(phi, dtype=np.float64)
+    st = np.sin(theta)
+    return np.stack(np.broadcast_arrays(st * np.cos(phi), st * np.sin(phi), np.cos(theta)),
+                    axis=-1)
+
+
+def _erf_medium(a3: RoughnessTriple):
+    kind = NdfKind.GENERALIZED if a3.az > 0.0 else NdfKind.BECKMANN
+    return MacrofacetMedium(kind=kind, a3=a3, sigma=1.0, fresnel_one=True)
+
+
+def curve_device(medium: MacrofacetMedium, kind, x, y=None, z=None, wo=(0.0, 0.0, 1.0), z0=0.0,
+                 out=None, stream=None):
+    """mf_curve on device float32 tensors (x, y, z: direction components,
+    or x = end field values h1 for "transmittance", from h0 = z0); returns
+    the output tensor."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    if kind not in _lib.CURVE:
+        raise ParameterDomainError(f"unknown curve kind {kind!r}")
+    n = x.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=x.device)
+    prm = (ctypes.c_double * 4)(*(float(v) for v in wo), float(z0))
+    cm = to_c_medium(medium)
+    ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+    s = stream if stream is not None else _lib.stream_handle(torch, x.device)
+    _lib.check(lib.mf_curve(ctypes.byref(cm), _lib.CURVE[kind], ptr(x), ptr(y), ptr(z), n, prm,
+                            ptr(out), s))
+    return out
+
+
+def _curve_host(medium, kind, w=None, t=None, wo=(0.0, 0.0, 1.0), z0=0.0):
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def col(a):
+        return torch.from_numpy(np.ascontiguousarray(np.reshape(a, -1), dtype=np.float32)).to(dev)
+
+    if t is not None:
+        t = np.asarray(t, dtype=np.float64)
+        r = curve_device(medium, kind, col(t), wo=wo, z0=z0)
+        return r.cpu().numpy().astype(np.float64).reshape(t.shape)[()]
+    w = np.asarray(w, dtype=np.float64)
+    shape = w.shape[:-1]
+    r = curve_device(medium, kind, col(w[..., 0]), col(w[..., 1]), col(w[..., 2]), wo=wo)
+    return r.cpu().numpy().astype(np.float64).reshape(shape)[()]
+
+
+def generalized_lambda_dir(w, a3: RoughnessTriple):
+    """Smith Lambda(w) = sigma(w) / cos(theta); GrazingSingularityError at
+    grazing directions, as the reference (ndf.py:120-135)."""
+    w = np.asarray(w, dtype=np.float64)
+    if np.any(np.abs(w[..., 2]) < 1e-9 * np.linalg.norm(w, axis=-1)):
+        raise GrazingSingularityError("Lambda diverges at grazing directions; use projected_area")
+    return _curve_host(_erf_medium(a3), "lambda", w=w)
+
+
+def generalized_lambda(theta, phi, a3: RoughnessTriple):
+    return generalized_lambda_dir(_sph_dir(theta, phi), a3)
+
+
+def projected_area_dir(wo, kind: NdfKind, a3: RoughnessTriple):
+    if kind is NdfKind.GENERALIZED:
+        med = MacrofacetMedium(kind=kind, a3=a3, sigma=1.0, fresnel_one=True)
+    else:
+        med = MacrofacetMedium(kind=kind, a3=RoughnessTriple(a3.ax, a3.ay, 0.0), sigma=1.0,
+                               fresnel_one=True)
+    return _curve_host(med, "projected-area", w=wo)
+
+
+def projected_area(theta, phi, a3: RoughnessTriple):
+    return _curve_host(_erf_medium(a3), "projected-area", w=_sph_dir(theta, phi))
+
+
+def generalized_ndf_dir(wm, a3: RoughnessTriple):
+    if a3.az <= 0.0:
+        raise ParameterDomainError("generalized NDF requires az > 0")
+    return _curve_host(_erf_medium(a3), "ndf", w=wm)
+
+
+def generalized_ndf(theta_m, phi_m, a3: RoughnessTriple):
+    return generalized_ndf_dir(_sph_dir(theta_m, phi_m), a3)
+
+
+def ndf_dir(wm, kind: NdfKind, a3: RoughnessTriple):
+    """D(wm) dispatched on kind (the reference's _ndf_dispatch)."""
+    a = a3 if kind is NdfKind.GENERALIZED else RoughnessTriple(a3.ax, a3.ay, 0.0)
+    return _curve_host(MacrofacetMedium(kind=kind, a3=a, sigma=1.0, fresnel_one=True), "ndf",
+                       w=wm)
+
+
+def vndf_eval(wm, wo, kind: NdfKind, a3: RoughnessTriple):
+    """<-wo, wm>+ D(wm) / sigma(wo) for one propagation direction wo;
+    DegenerateVisibilityError when sigma(wo) < 1e-12 (ndf.py:312-313)."""
+    wo = np.asarray(wo, dtype=np.float64)
+    if wo.ndim != 1:
+        raise ParameterDomainError("vndf_eval on the device takes one wo per call")
+    a = a3 if kind is NdfKind.GENERALIZED else RoughnessTriple(a3.ax, a3.ay, 0.0)
+    med = MacrofacetMedium(kind=kind, a3=a, sigma=1.0, fresnel_one=True)
+    return _curve_host(med, "vndf", w=wm, wo=tuple(wo))
+
+
+def planar_transmittance(h0, h1, theta, phi, medium: MacrofacetMedium):
+    """exp(-Lambda (log Phi(h1/s) - log Phi(h0/s))) (medium.py:98-124), for
+    scalar h0 / theta / phi and scalar or array h1."""
+    theta = float(theta)
+    c = np.cos(theta)
+    if abs(c) < 1e-12:
+        raise UnsupportedGeometryError("planar transmittance is undefined at cos(theta) = 0")
+    if medium.kind is NdfKind.GGX:
+        raise UnsupportedGeometryError("closed-form transmittance covers the erf-family lambda only")
+    wo = tuple(_sph_dir(theta, float(phi)))
+    return _curve_host(medium, "transmittance", t=h1, wo=wo, z0=float(h0))

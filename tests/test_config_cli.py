@@ -52,3 +52,22 @@ def test_cli_exit_codes(tmp_path, capsys):
     assert cli.main(["render", str(bad), "--out", str(tmp_path / "x.pfm")]) == 1
     assert cli.main(["render", str(tmp_path / "missing.cfg"), "--out", "x.pfm"]) == 3
     assert cli.main(["bogus"]) == 1
+
+
+def test_cli_curves_validate_host_paths(tmp_path, capsys):
+    """Argument errors and the CSV layout need no GPU; without a device the
+    compute subcommands fail loudly (no CPU fallback) with exit code 2."""
+    from paper_2603_00280_b200 import cli
+
+    assert cli.main(["validate", "nope"]) == 1
+    assert cli.main(["validate", "all", "--tol", "x"]) == 1
+    assert cli.main(["curves", "bogus", "--out", str(tmp_path / "x.csv")]) == 1
+    out = tmp_path / "t.csv"
+    cli.write_csv(str(out), ["a", "b"], [(0.1, 1.0 / 3.0)], {"z": 1, "k": "lambda"}, seed=7)
+    lines = out.read_text().splitlines()
+    assert lines[1:] == ["# seed = 7", "# params: k=lambda z=1", "a,b",
+                         "0.10000000000000001,0.33333333333333331"]
+    import torch
+
+    if not torch.cuda.is_available():
+        assert cli.main(["curves", "lambda", "--out", str(tmp_path / "l.csv")]) == 2
