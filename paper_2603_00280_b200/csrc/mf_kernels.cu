@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -529,6 +530,255 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Path pool (single-plane renders): decouple paths from lanes.
+//
+// The megakernel above binds one path to one lane, so a warp pays for every
+// stage any of its lanes needs: the costly Beckmann visible-normal sampler
+// runs with the ~half of the lanes whose mixture branch chose it (10 of 32
+// active on config 2, ncu), and raygen with the few lanes whose path just
+// ended (9 of 32).  Here every warp owns kPool path slots in shared memory
+// (SoA, one tag per slot) and each iteration runs ONE stage on 32 slots that
+// wait for it:
+//   R  raygen into 32 empty slots (while path indices last);
+//   A  flight and, on a collision, NEE and the mixture branch: the cheap
+//      hemisphere branch samples in place (phase tail, depth cap, RR), the
+//      Beckmann branch parks the path for B;
+//   B  Beckmann visible-normal sample + phase tail + depth cap / RR.
+// B and R run only as full warps (until the work runs out); with 96 slots
+// and fewer than 32 in each of B and R, A always has more than 32.
+// Each path runs exactly the arithmetic of path_kernel<0> with the same
+// random stream (pixel, sample, segment, call), so the image is bit-identical
+// to it (tests/test_gpu_render.py); only the order in which paths advance
+// changes.
+
+#ifndef MF_POOL
+#define MF_POOL 96
+#endif
+constexpr int kPool = MF_POOL;
+static_assert(kPool % 32 == 0 && kPool <= 128, "pool size: whole warps of slots");
+constexpr int kPoolWords = kPool / 32;
+constexpr int kPoolF = 17;   // pos3 dir3 T3 L3 sig_o sig_b u_br u_s2 u_rr
+constexpr int kPoolU = 4;    // pid pixel sample bounce
+constexpr int kWarpsPerBlock = kBlock / 32;
+
+enum PoolStage : int { kStageFlight = 0, kStageBeck = 1, kStageRaygen = 2 };
+constexpr uint8_t kTagEmpty = 0, kTagFlight = 1, kTagBeck = 2;
+
+struct PoolSlots {
+  float f[kPoolF][kPool];
+  uint32_t u[kPoolU][kPool];
+  uint8_t tag[kPool];
+  uint8_t list[32];   // this iteration's slot of each lane
+};
+
+__device__ __forceinline__ void pool_store(PoolSlots& P, int s, const PathState& st, float sig_o,
+                                           float sig_b) {
+  P.f[0][s] = st.pos.x; P.f[1][s] = st.pos.y; P.f[2][s] = st.pos.z;
+  P.f[3][s] = st.dir.x; P.f[4][s] = st.dir.y; P.f[5][s] = st.dir.z;
+  P.f[6][s] = st.T.x;   P.f[7][s] = st.T.y;   P.f[8][s] = st.T.z;
+  P.f[9][s] = st.L.x;   P.f[10][s] = st.L.y;  P.f[11][s] = st.L.z;
+  P.f[12][s] = sig_o;   P.f[13][s] = sig_b;
+  P.f[14][s] = st.u_br; P.f[15][s] = st.u_s2; P.f[16][s] = st.u_rr;
+  P.u[0][s] = st.pid;   P.u[1][s] = st.rng.pixel; P.u[2][s] = st.rng.sample;
+  P.u[3][s] = (uint32_t)st.bounce;
+}
+
+__device__ __forceinline__ void pool_load(const PoolSlots& P, int s, const PassDev& ps,
+                                          PathState& st, float& sig_o, float& sig_b) {
+  st.pos = v3(P.f[0][s], P.f[1][s], P.f[2][s]);
+  st.dir = v3(P.f[3][s], P.f[4][s], P.f[5][s]);
+  st.T = v3(P.f[6][s], P.f[7][s], P.f[8][s]);
+  st.L = v3(P.f[9][s], P.f[10][s], P.f[11][s]);
+  sig_o = P.f[12][s];
+  sig_b = P.f[13][s];
+  st.u_br = P.f[14][s]; st.u_s2 = P.f[15][s]; st.u_rr = P.f[16][s];
+  st.pid = P.u[0][s];
+  st.rng.k0 = ps.k0;
+  st.rng.k1 = ps.k1;
+  st.rng.pixel = P.u[1][s];
+  st.rng.sample = P.u[2][s];
+  st.bounce = (int)P.u[3][s];
+}
+
+// next-event estimation at a collision of the single plane (the stage-2
+// block of scatter_stages<0>, same arithmetic); kPoint: the scene has a point
+// light (its code is compiled out otherwise)
+template <bool kPoint>
+__device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Counters& cn,
+                                           const Frame& fr, V3 wo, float sig_o, V3 pos) {
+  const MediumK& m = sc.media[0];
+  if (sc.has_sun) {
+    V3 wl = to_local(fr, sc.sun_to);
+    V3 ph = phase_eval(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr<0>(sc, st, pos, sc.sun_to, INFINITY,
+                              sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
+                           st.T.z * ph.z * sc.sun_L.z * tr));
+    }
+  }
+  if (kPoint && sc.has_point) {
+    V3 d = sub3(sc.point_pos, pos);
+    float r2 = dot3(d, d);
+    float ir = frsqrt(r2);
+    V3 wlw = mul3(d, ir);
+    V3 wl = to_local(fr, wlw);
+    V3 ph = phase_eval(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr<0>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
+      float s = tr * frcp(r2);
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
+                           st.T.z * ph.z * sc.point_I.z * s));
+    }
+  }
+}
+
+template <bool kPoint>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
+                                                                  const __grid_constant__ PassDev ps) {
+  __shared__ PoolSlots pools[kWarpsPerBlock];
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  PoolSlots& P = pools[threadIdx.x >> 5];
+  const MediumK& m = sc.media[0];
+  Counters cn;
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
+#pragma unroll
+  for (int w = 0; w < kPoolWords; ++w) P.tag[w * 32 + lane] = kTagEmpty;
+  __syncwarp();
+  bool exhausted = false;    // warp-uniform
+  while (true) {
+    // per-stage slot masks from the tags (lane l reads slots l, l+32, ...)
+    unsigned qa[kPoolWords], qb[kPoolWords], qe[kPoolWords];
+    int na = 0, nb = 0, ne = 0;
+#pragma unroll
+    for (int w = 0; w < kPoolWords; ++w) {
+      uint8_t t = P.tag[w * 32 + lane];
+      qa[w] = __ballot_sync(full, t == kTagFlight);
+      qb[w] = __ballot_sync(full, t == kTagBeck);
+      qe[w] = exhausted ? 0u : __ballot_sync(full, t == kTagEmpty);
+      na += __popc(qa[w]);
+      nb += __popc(qb[w]);
+      ne += __popc(qe[w]);
+    }
+    int stage;
+    if (nb >= 32) stage = kStageBeck;
+    else if (ne >= 32) stage = kStageRaygen;
+    else if (na > 0) stage = kStageFlight;
+    else if (nb > 0) stage = kStageBeck;
+    else if (ne > 0) stage = kStageRaygen;
+    else break;
+    // compaction: the i-th candidate slot goes to lane i (through smem)
+    int n = 0;
+#pragma unroll
+    for (int w = 0; w < kPoolWords; ++w) {
+      unsigned c = stage == kStageFlight ? qa[w] : (stage == kStageBeck ? qb[w] : qe[w]);
+      int r = n + __popc(c & lt);
+      if (((c >> lane) & 1u) && r < 32) P.list[r] = (uint8_t)(w * 32 + lane);
+      n += __popc(c);
+    }
+    __syncwarp();
+    int slot = lane < n ? (int)P.list[lane] : -1;
+    __syncwarp();
+
+    uint8_t tag = kTagEmpty;
+    PathState st;
+    float sig_o = 0.0f, sig_b = 0.0f;
+    bool sample = false;
+    Frame fr = frame_about(v3(0.0f, 0.0f, 1.0f));
+    if (stage == kStageRaygen) {
+      // raygen, full width: path indices with one atomicAdd
+      unsigned need = __ballot_sync(full, slot >= 0);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(ps.counter, (unsigned)__popc(need));
+      base = __shfl_sync(full, base, 0);
+      if (base + (unsigned)__popc(need) >= ps.n_paths) exhausted = true;
+      uint32_t my = base + (uint32_t)lane;
+      if (slot >= 0 && my < ps.n_paths && start_path<false>(sc, ps, st, my)) {
+        cn.v[kStPaths]++;
+        tag = kTagFlight;
+      }
+    } else if (slot >= 0) {
+      pool_load(P, slot, ps, st, sig_o, sig_b);
+      if (stage == kStageFlight) {
+        if (!flight_stage<0>(sc, st, cn)) {
+          finish_path(ps, st, cn);
+        } else {
+          // scatter_stages<0> up to the mixture branch
+          V3 pos = st.cpos;
+          V3 wo = to_local(fr, st.dir);
+          sig_o = st.csig;
+          cn.v[kStScatters]++;
+          if (!(sig_o >= 1e-12f)) {
+            cn.v[kStDegenerate]++;
+            finish_path(ps, st, cn);
+          } else {
+            planar_nee<kPoint>(sc, st, cn, fr, wo, sig_o, pos);
+            st.pos = pos;
+            sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
+            // the cheap hemisphere branch samples right here; the Beckmann
+            // branch waits for a full warp of Beckmann samples
+            if (sig_b > 1e-12f && st.u_br < m.mix) tag = kTagBeck;
+            else sample = true;
+          }
+        }
+      } else {
+        sample = true;
+      }
+    }
+    __syncwarp();
+    if (sample) {
+      // stage 3 of scatter_stages<0>: phase sample, depth cap, RR
+      V3 wo = to_local(fr, st.dir);
+      V3 v = neg3(wo);
+      float uu = remap_branch_uniform(st.u_br, m.mix);
+      V3 wm;
+      float vm;
+      int iters = 0;
+      if (stage == kStageBeck) {
+        wm = beckmann_visible_normal(m, v, uu, st.u_s2, &iters);
+        vm = dot3(v, wm);
+      } else {
+        wm = hemisphere_about(v, uu, st.u_s2);
+        vm = uu;
+      }
+      PhaseSample smp = phase_sample_tail(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
+      cn.v[kStSlopeIters] += (uint32_t)iters;
+      st.dir = to_world(fr, smp.wi);
+      st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
+      st.bounce++;
+      bool done = false;
+      if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+        done = true;
+      } else if (st.bounce > 8) {                    // render.py:96-105
+        float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+        if (st.u_rr >= q) {
+          done = true;
+        } else {
+          st.T = mul3(st.T, 1.0f / q);
+        }
+      }
+      if (done) finish_path(ps, st, cn);
+      else tag = kTagFlight;
+    }
+    if (slot >= 0) {
+      if (tag != kTagEmpty) pool_store(P, slot, st, sig_o, sig_b);
+      P.tag[slot] = tag;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) {
+    unsigned v = __reduce_add_sync(full, cn.v[i]);
+    if (lane == 0 && v) atomicAdd(ps.stats + i, (unsigned long long)v);
+  }
+}
+
 // per-pixel fixed-order sum of a pass (render.py:150,165-166)
 __global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__ SceneDev sc,
                                                           const __grid_constant__ PassDev ps,
@@ -671,7 +921,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[6] = {0, 0, 0, 0, 0, 0};
+  int blocks[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 int device_occupancy(Occupancy* occ) {
@@ -699,6 +949,10 @@ int device_occupancy(Occupancy* occ) {
                                                         kBlock, 0));
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[5], path_kernel<2, true>,
                                                         kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[6], pool_kernel<false>, kBlock,
+                                                        0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[7], pool_kernel<true>, kBlock,
+                                                        0));
   for (int& b : o.blocks) b = std::max(b, 1);
   if (dev < 64) {
     cache[dev] = o;
@@ -778,6 +1032,11 @@ int scratch_free(Scratch* s, cudaStream_t st) {
   return MF_OK;
 }
 
+bool megakernel_requested() {
+  const char* e = std::getenv("MF_MEGAKERNEL");
+  return e && e[0] == '1';
+}
+
 int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaStream_t st) {
   Occupancy occ;
   int rc = device_occupancy(&occ);
@@ -788,7 +1047,19 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
   if (mode == 0) {
     if (caller_rays) path_kernel<0, true><<<grid, kBlock, 0, st>>>(sc, ps);
+#ifndef MF_NO_POOL
+    // MF_MEGAKERNEL=1 selects the lane-per-path megakernel instead (the
+    // pool's bit-exactness test compares the two)
+    else if (megakernel_requested()) path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    else {
+      int pk = sc.has_point ? 7 : 6;
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>(occ.sms * occ.blocks[pk], need));
+      if (sc.has_point) pool_kernel<true><<<grid, kBlock, 0, st>>>(sc, ps);
+      else pool_kernel<false><<<grid, kBlock, 0, st>>>(sc, ps);
+    }
+#else
     else path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
+#endif
   } else if (mode == 1) {
     if (caller_rays) path_kernel<1, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else path_kernel<1, false><<<grid, kBlock, 0, st>>>(sc, ps);

@@ -59,7 +59,8 @@ for l in dis[start + 1:]:
         fresh = True
 
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                      "-k", "regex:" + kname.split("ILi")[0]], capture_output=True, text=True).stdout
+                      "-k", "regex:" + re.split(r"I[LN]", kname)[0]], capture_output=True,
+                     text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
 hdr, data = rows[hi], rows[hi + 1:]
