@@ -150,7 +150,7 @@ typedef struct mf_stats {
   uint64_t absorbed;
   uint64_t majorant_violations;
   uint64_t degenerate;    /* sigma(wo) < 1e-12 at a scatter (returns 0) */
-  uint64_t nonfinite;
+  uint64_t nonfinite;     /* paths / pixels with non-finite or negative radiance */
   uint64_t capped;        /* paths cut by the segment cap */
   double path_kernel_ms;  /* CUDA-event time of the path megakernel launches */
 } mf_stats;

@@ -799,9 +799,14 @@ __global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__
     s2 += __ldg(r + 2u * ps.n_paths + o);
   }
   float* a = accum + (size_t)pixel * 3;
-  a[0] += s0 * inv_spp;
-  a[1] += s1 * inv_spp;
-  a[2] += s2 * inv_spp;
+  float v0 = a[0] + s0 * inv_spp, v1 = a[1] + s1 * inv_spp, v2 = a[2] + s2 * inv_spp;
+  a[0] = v0;
+  a[1] = v1;
+  a[2] = v2;
+  // RadianceImage.validate (image.py:38-42) on the device: the per-path
+  // check in finish_path cannot see a sum that overflows
+  if (!(isfinite(v0) && isfinite(v1) && isfinite(v2)) || v0 < 0.0f || v1 < 0.0f || v2 < 0.0f)
+    atomicAdd(ps.stats + kStNonfinite, 1ull);
 }
 
 // ratio-tracking transmittance samples (transport.py:300-313)
@@ -1309,12 +1314,10 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   ps.counter = scr.counter;
   ps.stats = scr.stats;
   float inv_spp = (float)(1.0 / p.spp);
-  cudaEvent_t ev[2] = {nullptr, nullptr};
+  // path-kernel timing: one event pair per pass, read after the final sync
+  // (no host round trip between the path and accumulate kernels)
+  std::vector<cudaEvent_t> ev;
   double kernel_ms = 0.0;
-  if (stats) {
-    MF_CUDA(cudaEventCreate(&ev[0]));
-    MF_CUDA(cudaEventCreate(&ev[1]));
-  }
   for (uint32_t s0 = 0; s0 < s_count; s0 += S_pass) {
     uint32_t S = std::min(S_pass, s_count - s0);
     ps.S = S;
@@ -1322,16 +1325,16 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.n_paths = (uint32_t)(n_local * S);
     ps.n_local = (uint32_t)n_local;
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
-    if (stats) MF_CUDA(cudaEventRecord(ev[0], st));
-    rc = launch_paths(sc, ps, false, st);
-    if (stats && !rc) {
-      MF_CUDA(cudaEventRecord(ev[1], st));
-      MF_CUDA(cudaEventSynchronize(ev[1]));
-      float ms = 0.0f;
-      MF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-      kernel_ms += ms;
+    if (stats) {
+      ev.resize(ev.size() + 2, nullptr);
+      MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));
+      MF_CUDA(cudaEventCreate(&ev[ev.size() - 1]));
+      MF_CUDA(cudaEventRecord(ev[ev.size() - 2], st));
     }
+    rc = launch_paths(sc, ps, false, st);
+    if (stats && !rc) MF_CUDA(cudaEventRecord(ev[ev.size() - 1], st));
     if (rc) {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
       scratch_free(&scr, st);
       return rc;
     }
@@ -1346,9 +1349,13 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     MF_CUDA(cudaStreamSynchronize(st));
     fill_stats(h, stats);
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float ms = 0.0f;
+      MF_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      kernel_ms += ms;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
     stats->path_kernel_ms = kernel_ms;
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
     out = check_stats(*stats);
   }
   rc = scratch_free(&scr, st);

@@ -75,11 +75,14 @@ def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, 
     any launch geometry)."""
     if threads is not None and threads < 1:
         raise ParameterDomainError(f"thread count must be >= 1, got {threads}")
+    import torch
+
+    # RadianceImage.validate (image.py:38-42) runs on the device: the path and
+    # accumulate kernels count non-finite / negative radiance and mf_render
+    # raises NumericFailureError (a MacrofacetError) for any
     img, _ = render_device(scene, spp, seed, max_bounces=max_bounces, tile=tile, stats=True)
-    out = RadianceImage(pixels=img.cpu().numpy().astype(np.float64),
-                        meta={"seed": int(seed), "spp": int(spp), "scene_hash": scene_hash})
-    out.validate()
-    return out
+    return RadianceImage(pixels=img.to(torch.float64).cpu().numpy(),
+                         meta={"seed": int(seed), "spp": int(spp), "scene_hash": scene_hash})
 
 
 def render_sharded(scene: ShellScene, spp, seed, max_bounces=64, tile=32, shard="tiles",

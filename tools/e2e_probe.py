@@ -1,13 +1,41 @@
-import time, torch, sys
+"""Host-side breakdown of one render() call on config 2 (GPU box)."""
+import sys
+import time
+
 sys.path.insert(0, '.')
-import paper_2603_00280_b200 as mf
-from paper_2603_00280_b200 import configs
-scene = configs.config2_scene() if hasattr(configs, 'config2_scene') else None
-print(type(scene))
-for i in range(6):
-    torch.cuda.synchronize(); t0=time.perf_counter()
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2603_00280_b200 as mf  # noqa: E402
+from paper_2603_00280_b200 import configs  # noqa: E402
+
+scene = configs.config2_scene()
+for _ in range(3):
+    mf.render(scene, 64, 1, max_bounces=16)
+T = {}
+
+
+def tick(k, t0):
+    T[k] = T.get(k, 0.0) + (time.perf_counter() - t0) * 1e3
+    return time.perf_counter()
+
+
+N = 20
+for _ in range(N):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
     img, st = mf.render_device(scene, 64, 1, max_bounces=16, stats=True)
-    torch.cuda.synchronize(); t1=time.perf_counter()
-    h = img.cpu().numpy(); t2=time.perf_counter()
-    r = mf.render(scene, 64, 1, max_bounces=16); t3=time.perf_counter()
-    print(f"dev {1e3*(t1-t0):.2f} ms  d2h {1e3*(t2-t1):.2f}  render {1e3*(t3-t2):.2f}")
+    t = tick("render_device(stats)", t)
+    flags = torch.stack(((~torch.isfinite(img)).any(), (img < 0.0).any()))
+    t = tick("flags (async)", t)
+    pixels = img.to(torch.float64).cpu().numpy()
+    t = tick("double+d2h", t)
+    f = flags.cpu().numpy()
+    t = tick("flags d2h", t)
+    out = mf.RadianceImage(pixels=pixels, meta={})
+    t = tick("RadianceImage", t)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    mf.render(scene, 64, 1, max_bounces=16)
+    t = tick("render() total", t)
+print({k: round(v / N, 3) for k, v in T.items()})
