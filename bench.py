@@ -276,7 +276,7 @@ def run_ours(args):
                                "issue microbenchmarks)",
                 "fp32_frac": rl["fp32_frac"], "sfu_frac": rl["sfu_frac"],
                 "fp32_per_path": rl["fp32_per_path"], "sfu_per_path": rl["sfu_per_path"],
-                "kernel_ms": st["path_kernel_ms"], "kernel": "path_kernel<planar>"}
+                "kernel_ms": st["path_kernel_ms"], "kernel": "pool_kernel (single-plane path pool)"}
         cpu = None
         if n == 1 and not args.no_cpu:
             cpu = cpu_baseline(args.cpu_seconds)
@@ -294,7 +294,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": METRIC,
                     "h2d_bytes_per_step": _lib.ctypes.sizeof(_lib.MfScene)
                     + _lib.ctypes.sizeof(_lib.MfRenderParams),
-                    "d2h_bytes_per_step": 256 * 256 * 3 * 4,
+                    "d2h_bytes_per_step": 256 * 256 * 3 * 8,   # float64 image
                     "api": "paper_2603_00280_b200.render()" if n == 1 else "render_sharded()"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

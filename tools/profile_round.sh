@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 \
     > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"pool_kernel|path_kernel" -s 3 -c 1 \
     -o gpurun_out/path_full -f python bench.py --steps 3 --warmup 3 \
     > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"

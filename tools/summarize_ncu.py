@@ -106,7 +106,7 @@ def main():
     out = {"source": os.path.basename(rep), "kernels": summ}
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.json"), "w") as fh:
         json.dump(out, fh, indent=1)
-    path_k = [d for d in summ if "path_kernel" in d["kernel"]]
+    path_k = [d for d in summ if "pool_kernel" in d["kernel"] or "path_kernel" in d["kernel"]]
     if path_k:
         with open(os.path.join(ROOT, "profiles", "ncu_path_kernel.json"), "w") as fh:
             json.dump({"round": tag, **path_k[0]}, fh, indent=1)
