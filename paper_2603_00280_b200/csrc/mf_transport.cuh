@@ -228,6 +228,12 @@ MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, f
 // ---------------------------------------------------------------------------
 // general walker (delta / ratio tracking), any number of plane / sphere shells
 
+// sigma(w) for the walker, out of line: three call sites in the tracking
+// loop share one copy in the instruction stream (config 3: 11.07 -> 10.56 ms)
+MF_COLD float proj_area_outlined(int kind, float ax, float ay, float az, V3 w) {
+  return kind == kGGX ? proj_area_ggx(w, ax, ay) : proj_area_erf(w, ax, ay, az);
+}
+
 struct WalkResult {
   int outcome;
   int prim;
@@ -244,7 +250,7 @@ MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mu
   float f = prim_field(p, x);
   if (f < lo_mult * m.sigma || f > 3.0f * m.sigma) return 0.0f;
   Frame fr = frame_about(prim_normal(p, x));
-  float sg = proj_area(m, to_local(fr, dir));
+  float sg = proj_area_outlined(m.kind, m.ax, m.ay, m.az, to_local(fr, dir));
   return mills(f * m.inv_sigma) * m.inv_sigma * sg;
 }
 
@@ -306,7 +312,7 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
       float fmin, dirf;
       if (p.shape == 0) {
         fmin = f + cap * fminf(dir.z, 0.0f);
-        dirf = proj_area(m, dir);
+        dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az, dir);
       } else {
         V3 oc = sub3(pos, p.c);
         float b = dot3(oc, dir);
@@ -316,7 +322,8 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
         if (sc.mx[j].area_monotone) {
           float c = b * frsqrt(fmaxf(r2, 1e-30f));
           c = fminf(fmaxf(c, -1.0f), 1.0f);
-          dirf = proj_area(m, v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c)) * 1.0001f;
+          dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az,
+                                    v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c)) * 1.0001f;
         } else {
           dirf = sc.mx[j].sig_max;
         }
