@@ -203,6 +203,7 @@ struct PathState {
   int ck;                // primitive of the pending collision
   float csig;            // sigma(dir) when known in the collision frame, else -1
   float u_br, u_s2, u_rr;  // the segment's branch / slope / RR uniforms
+  float lphi;            // single plane: log Phi(f / sigma) at pos, NaN when unknown
   int bounce;
   uint32_t pid;          // result slot: caller-ray index, or s * n_local + lp (render)
   PathRng rng;
@@ -235,7 +236,7 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
   if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
     float sig = sig_known >= 0.0f ? sig_known : proj_area(m, wl);
-    return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig);
+    return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig, st.lphi);
   } else if constexpr (kMode == 2) {
     const PathRng& r = st.rng;
     uint32_t seg = (uint32_t)st.bounce;
@@ -290,8 +291,9 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
     st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
-    Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl);
+    Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi);
     st.cpos = fl.pos;
+    st.lphi = fl.lphi;
     outcome = fl.outcome;
   } else {
     WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false, INFINITY);
@@ -429,6 +431,7 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   st.rng.k1 = ps.k1;
   st.T = v3(1.0f, 1.0f, 1.0f);
   st.L = v3(0.0f, 0.0f, 0.0f);
+  st.lphi = NAN;
   st.bounce = 0;
   if (kCallerRays) {
     st.rng.pixel = ps.pix[my];
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 constexpr int kPool = MF_POOL;
 static_assert(kPool % 32 == 0 && kPool <= 128, "pool size: whole warps of slots");
 constexpr int kPoolWords = kPool / 32;
-constexpr int kPoolF = 17;   // pos3 dir3 T3 L3 sig_o sig_b u_br u_s2 u_rr
+constexpr int kPoolF = 18;   // pos3 dir3 T3 L3 sig_o sig_b u_br u_s2 u_rr lphi
 constexpr int kPoolU = 4;    // pid pixel sample bounce
 constexpr int kWarpsPerBlock = kBlock / 32;
 
@@ -580,6 +583,7 @@ __device__ __forceinline__ void pool_store(PoolSlots& P, int s, const PathState&
   P.f[9][s] = st.L.x;   P.f[10][s] = st.L.y;  P.f[11][s] = st.L.z;
   P.f[12][s] = sig_o;   P.f[13][s] = sig_b;
   P.f[14][s] = st.u_br; P.f[15][s] = st.u_s2; P.f[16][s] = st.u_rr;
+  P.f[17][s] = st.lphi;
   P.u[0][s] = st.pid;   P.u[1][s] = st.rng.pixel; P.u[2][s] = st.rng.sample;
   P.u[3][s] = (uint32_t)st.bounce;
 }
@@ -593,6 +597,7 @@ __device__ __forceinline__ void pool_load(const PoolSlots& P, int s, const PassD
   sig_o = P.f[12][s];
   sig_b = P.f[13][s];
   st.u_br = P.f[14][s]; st.u_s2 = P.f[15][s]; st.u_rr = P.f[16][s];
+  st.lphi = P.f[17][s];
   st.pid = P.u[0][s];
   st.rng.k0 = ps.k0;
   st.rng.k1 = ps.k1;

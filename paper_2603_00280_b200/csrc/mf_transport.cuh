@@ -141,13 +141,19 @@ enum FlightOutcome : int { kEscaped = 0, kAbsorbed = 1, kCollided = 2 };
 struct Flight {
   int outcome;
   V3 pos;
+  float lphi;   // log Phi(f / sigma) at pos after a collision, NaN otherwise
 };
 
 // One collision-mode flight from pos along dir through the shell of a
 // single plane, given u in (0,1).  sig = sigma(dir) in the plane frame.
+// lphi = log Phi(f / sigma) at pos when known (the previous collision's
+// inverted value), NaN otherwise: the flight is sampled in log-Phi space,
+// so a collision's l1 is carried to the next segment and to its shadow ray
+// instead of being re-derived from the rounded height.
 MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtra& mx, V3 pos,
-                           V3 dir, float sig, float u) {
+                           V3 dir, float sig, float u, float lphi) {
   Flight fl;
+  fl.lphi = NAN;
   float s3 = 3.0f * m.sigma;
   float h = pos.z - pr.z0;
   float c = dir.z;
@@ -159,6 +165,7 @@ MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtr
     }
     pos = fma3(dir, (s3 - h) / c, pos);
     h = s3;
+    lphi = mx.lphi_hi;
   }
   if (h < -6.0f * m.sigma) {
     fl.outcome = kAbsorbed;
@@ -177,7 +184,7 @@ MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtr
     fl.pos = fma3(dir, tau / st, pos);
     return fl;
   }
-  float l0 = log_ndtr(h * m.inv_sigma);
+  float l0 = lphi == lphi ? lphi : log_ndtr(h * m.inv_sigma);
   float dl = tau * fabsf(c) / sig;          // change of log Phi along the flight
   float l1;
   if (c > 0.0f) {
@@ -201,13 +208,15 @@ MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtr
   fl.outcome = kCollided;
   fl.pos = fma3(dir, (h1 - h) / c, pos);
   fl.pos.z = pr.z0 + h1;
+  fl.lphi = l1;
   return fl;
 }
 
 // closed-form shadow transmittance of a single plane over |f| <= 3 sigma
-// between field values h (start) and h_end (light; +/-inf for the sun)
+// between field values h (start) and h_end (light; +/-inf for the sun);
+// lphi = log Phi(h / sigma) when known (NaN otherwise)
 MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, float h_end,
-                             float c, float sig) {
+                             float c, float sig, float lphi) {
   float s3 = 3.0f * m.sigma;
   float a = fminf(fmaxf(h, -s3), s3);
   float b = fminf(fmaxf(h_end, -s3), s3);
@@ -215,12 +224,16 @@ MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, f
   if (fabsf(c) < 1e-6f) return 0.0f;
   // both ends through one copy of log_ndtr (I-cache)
   float la = 0.0f, lb = 0.0f, e = a;
+  float known = lphi;
 #pragma unroll 1
   for (int i = 0; i < 2; ++i) {
-    float l = e >= s3 ? mx.lphi_hi : (e <= -s3 ? mx.lphi_lo_rat : log_ndtr(e * m.inv_sigma));
+    float l = e >= s3 ? mx.lphi_hi
+                      : (e <= -s3 ? mx.lphi_lo_rat
+                                  : (known == known ? known : log_ndtr(e * m.inv_sigma)));
     la = i == 0 ? l : la;
     lb = l;
     e = b;
+    known = NAN;
   }
   return expf(-sig / fabsf(c) * fabsf(lb - la));
 }
