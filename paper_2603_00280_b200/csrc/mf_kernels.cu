@@ -291,7 +291,9 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
     const MediumK& m = sc.media[0];
     float sig = proj_area(m, st.dir);
     st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
-    Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi);
+    // positions matter only to a point light
+    Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi,
+                              sc.has_point != 0);
     st.cpos = fl.pos;
     st.lphi = fl.lphi;
     outcome = fl.outcome;

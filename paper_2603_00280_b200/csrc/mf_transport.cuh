@@ -146,95 +146,107 @@ struct Flight {
 
 // One collision-mode flight from pos along dir through the shell of a
 // single plane, given u in (0,1).  sig = sigma(dir) in the plane frame.
-// lphi = log Phi(f / sigma) at pos when known (the previous collision's
-// inverted value), NaN otherwise: the flight is sampled in log-Phi space,
-// so a collision's l1 is carried to the next segment and to its shadow ray
-// instead of being re-derived from the rounded height.
+// The flight is sampled in log-Phi space: lphi = log Phi(f / sigma) at pos
+// when known (the previous collision's l1), NaN otherwise (first flight,
+// after a grazing one).  A collision returns its l1, which the next flight
+// and the shadow ray use instead of re-deriving it from the height; the
+// height h1 = sigma Phi^-1(e^l1) (and so the position) is then needed only
+// when something reads positions (a point light): need_pos.  Without it
+// fl.pos is left stale -- nothing in a single-plane scene depends on x, y,
+// and every decision on z is taken on l.
 MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtra& mx, V3 pos,
-                           V3 dir, float sig, float u, float lphi) {
+                           V3 dir, float sig, float u, float lphi, bool need_pos) {
   Flight fl;
   fl.lphi = NAN;
+  fl.pos = pos;
   float s3 = 3.0f * m.sigma;
-  float h = pos.z - pr.z0;
   float c = dir.z;
-  if (h > s3) {
-    if (!(c < 0.0f)) {
-      fl.outcome = kEscaped;
+  bool known = lphi == lphi;
+  float h = pos.z - pr.z0;     // valid unless (known && !need_pos)
+  float l0 = lphi;
+  if (!known) {
+    if (h > s3) {
+      if (!(c < 0.0f)) {
+        fl.outcome = kEscaped;
+        return fl;
+      }
+      pos = fma3(dir, (s3 - h) / c, pos);
       fl.pos = pos;
-      return fl;
+      h = s3;
+      l0 = mx.lphi_hi;
+    } else {
+      if (h < -6.0f * m.sigma) {
+        fl.outcome = kAbsorbed;
+        return fl;
+      }
+      l0 = log_ndtr(h * m.inv_sigma);
     }
-    pos = fma3(dir, (s3 - h) / c, pos);
-    h = s3;
-    lphi = mx.lphi_hi;
-  }
-  if (h < -6.0f * m.sigma) {
-    fl.outcome = kAbsorbed;
-    fl.pos = pos;
-    return fl;
   }
   float tau = -flog(u);
   if (fabsf(c) < 1e-6f) {
-    float st = mills(h * m.inv_sigma) * m.inv_sigma * sig;
+    // grazing: f stays put; this rare branch needs the true height
+    float hg = (known && !need_pos) ? m.sigma * inv_log_ndtr(l0) : h;
+    float st = mills(hg * m.inv_sigma) * m.inv_sigma * sig;
     if (!(st > 0.0f)) {
       fl.outcome = kEscaped;
-      fl.pos = pos;
       return fl;
     }
     fl.outcome = kCollided;
+    pos.z = pr.z0 + hg;
     fl.pos = fma3(dir, tau / st, pos);
     return fl;
   }
-  float l0 = lphi == lphi ? lphi : log_ndtr(h * m.inv_sigma);
   float dl = tau * fabsf(c) / sig;          // change of log Phi along the flight
   float l1;
   if (c > 0.0f) {
     l1 = l0 + dl;
     if (!(l1 < mx.lphi_hi)) {
       fl.outcome = kEscaped;
-      fl.pos = pos;
       return fl;
     }
   } else {
     l1 = l0 - dl;
     if (!(l1 >= mx.lphi_lo_col)) {
       fl.outcome = kAbsorbed;
-      fl.pos = pos;
       return fl;
     }
   }
-  float h1 = m.sigma * inv_log_ndtr(l1);
-  // keep the root on the travelled side of h despite rounding
-  h1 = c > 0.0f ? fmaxf(h1, h) : fminf(h1, h);
   fl.outcome = kCollided;
-  fl.pos = fma3(dir, (h1 - h) / c, pos);
-  fl.pos.z = pr.z0 + h1;
   fl.lphi = l1;
+  if (need_pos) {
+    float h1 = m.sigma * inv_log_ndtr(l1);
+    // keep the root on the travelled side of h despite rounding
+    h1 = c > 0.0f ? fmaxf(h1, h) : fminf(h1, h);
+    fl.pos = fma3(dir, (h1 - h) / c, pos);
+    fl.pos.z = pr.z0 + h1;
+  }
   return fl;
 }
 
 // closed-form shadow transmittance of a single plane over |f| <= 3 sigma
 // between field values h (start) and h_end (light; +/-inf for the sun);
-// lphi = log Phi(h / sigma) when known (NaN otherwise)
+// lphi = log Phi(h / sigma) when known (NaN otherwise; h is then not read)
 MF_HD float planar_shadow_tr(const MediumK& m, const MediumExtra& mx, float h, float h_end,
                              float c, float sig, float lphi) {
   float s3 = 3.0f * m.sigma;
-  float a = fminf(fmaxf(h, -s3), s3);
-  float b = fminf(fmaxf(h_end, -s3), s3);
-  if (a == b) return 1.0f;
-  if (fabsf(c) < 1e-6f) return 0.0f;
-  // both ends through one copy of log_ndtr (I-cache)
-  float la = 0.0f, lb = 0.0f, e = a;
-  float known = lphi;
+  float ea = fminf(fmaxf(h, -s3), s3);
+  float eb = fminf(fmaxf(h_end, -s3), s3);
+  // clamping f to the band is clamping log Phi to [log Phi(-3), log Phi(3)]
+  float la = lphi == lphi ? fminf(fmaxf(lphi, mx.lphi_lo_rat), mx.lphi_hi)
+                          : (ea >= s3 ? mx.lphi_hi : (ea <= -s3 ? mx.lphi_lo_rat : NAN));
+  float lb = eb >= s3 ? mx.lphi_hi : (eb <= -s3 ? mx.lphi_lo_rat : NAN);
+  // the ends still unknown through one copy of log_ndtr (I-cache)
 #pragma unroll 1
   for (int i = 0; i < 2; ++i) {
-    float l = e >= s3 ? mx.lphi_hi
-                      : (e <= -s3 ? mx.lphi_lo_rat
-                                  : (known == known ? known : log_ndtr(e * m.inv_sigma)));
-    la = i == 0 ? l : la;
-    lb = l;
-    e = b;
-    known = NAN;
+    float cur = i == 0 ? la : lb;
+    if (!(cur == cur)) {
+      float l = log_ndtr((i == 0 ? ea : eb) * m.inv_sigma);
+      la = i == 0 ? l : la;
+      lb = i == 0 ? lb : l;
+    }
   }
+  if (la == lb) return 1.0f;
+  if (fabsf(c) < 1e-6f) return 0.0f;
   return expf(-sig / fabsf(c) * fabsf(lb - la));
 }
 
