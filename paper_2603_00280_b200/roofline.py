@@ -62,19 +62,30 @@ EVENTS = {
 }
 
 
-# single-plane scenes reuse sigma(dir) of the flight as sigma(wo) at the
-# scatter (identity frame) and precompute sigma(w_sun) once per render: that
-# work is not repeated per event
-PLANAR_DISCOUNT = {"scatters": PRIMS["proj_area"], "nee": PRIMS["proj_area"]}
+# Single-plane scenes without a point light (configs 2, 4; pool_kernel):
+#   - the flight is sampled in log-Phi space from the previous collision's
+#     carried log Phi: Philox block + 4 uniforms + sigma(dir) + log(u) + the
+#     log-Phi step (no log_ndtr, and no inv_log_ndtr since no position is
+#     read; an entry from above starts at the constant log Phi(3));
+#   - the scatter reuses sigma(dir) as sigma(wo) (identity frame);
+#   - NEE to the sun: phase_eval + the closed-form transmittance from the
+#     carried log Phi (clamp, one exp), sigma(w_sun) precomputed per render.
+PLANAR_EVENTS = {
+    "paths": EVENTS["paths"],
+    "segments": (44 + 4 + PRIMS["proj_area"][0] + 1 + 2 + 1, PRIMS["proj_area"][1] + 3),
+    "scatters": (EVENTS["scatters"][0] - PRIMS["proj_area"][0],
+                 EVENTS["scatters"][1] - PRIMS["proj_area"][1]),
+    "nee": (9 + PRIMS["phase_eval"][0] + 5 + 3 + 9, PRIMS["phase_eval"][1] + 2),
+    "slope_iters": EVENTS["slope_iters"],
+    "track_steps": EVENTS["track_steps"],
+}
 
 
 def algorithmic_ops(stats, planar=False):
-    """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters."""
+    """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters;
+    planar=True: the sun-lit single-plane event costs (PLANAR_EVENTS)."""
     f = s = 0.0
-    for ev, (cf, cs) in EVENTS.items():
-        if planar and ev in PLANAR_DISCOUNT:
-            cf -= PLANAR_DISCOUNT[ev][0]
-            cs -= PLANAR_DISCOUNT[ev][1]
+    for ev, (cf, cs) in (PLANAR_EVENTS if planar else EVENTS).items():
         n = float(stats.get(ev, 0))
         f += n * cf
         s += n * cs
