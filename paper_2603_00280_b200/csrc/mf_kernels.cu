@@ -698,8 +698,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
     float sig_o = 0.0f, sig_b = 0.0f;
     bool sample = false;
     Frame fr = frame_about(v3(0.0f, 0.0f, 1.0f));
+    bool live = false;
     if (stage == kStageRaygen) {
-      // raygen, full width: path indices with one atomicAdd
+      // raygen, full width: path indices with one atomicAdd; the new paths
+      // go straight on to their first flight below
       unsigned need = __ballot_sync(full, slot >= 0);
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(ps.counter, (unsigned)__popc(need));
@@ -708,11 +710,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       uint32_t my = base + (uint32_t)lane;
       if (slot >= 0 && my < ps.n_paths && start_path<false>(sc, ps, st, my)) {
         cn.v[kStPaths]++;
-        tag = kTagFlight;
+        live = true;
       }
     } else if (slot >= 0) {
       pool_load(P, slot, ps, st, sig_o, sig_b);
-      if (stage == kStageFlight) {
+      live = true;
+    }
+    if (live) {
+      if (stage != kStageBeck) {
         if (!flight_stage<0>(sc, st, cn)) {
           finish_path(ps, st, cn);
         } else {
