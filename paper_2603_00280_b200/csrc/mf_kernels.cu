@@ -792,26 +792,48 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
 }
 
 // per-pixel fixed-order sum of a pass (render.py:150,165-166)
+// Block = 8 warps x 32 consecutive local pixels.  Warp w sums the samples
+// of chunk w (S/8 consecutive samples, fixed order; each load of the warp is
+// one coalesced 128-byte row of the sample-major slots), then the eight
+// partial sums combine through shared memory in a fixed tree.  Eight times
+// the memory-level parallelism of one thread per pixel; the order depends on
+// S only, so the image stays deterministic.
+constexpr int kAccWarps = 8;
 __global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__ SceneDev sc,
                                                           const __grid_constant__ PassDev ps,
                                                           uint32_t n_local, float inv_spp,
                                                           float* accum) {
-  uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lp >= n_local) return;
+  __shared__ float part[3][kAccWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t lp = blockIdx.x * 32u + (uint32_t)lane;
+  uint32_t chunk = (ps.S + kAccWarps - 1) / kAccWarps;
+  uint32_t s_lo = min(ps.S, (uint32_t)w * chunk), s_hi = min(ps.S, s_lo + chunk);
+  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+  if (lp < n_local) {
+    const float* r = ps.rad + lp;
+    for (uint32_t s = s_lo; s < s_hi; ++s) {
+      size_t o = (size_t)s * n_local;
+      s0 += __ldg(r + o);
+      s1 += __ldg(r + ps.n_paths + o);
+      s2 += __ldg(r + 2u * ps.n_paths + o);
+    }
+  }
+  part[0][w][lane] = s0;
+  part[1][w][lane] = s1;
+  part[2][w][lane] = s2;
+  __syncthreads();
+  if (w != 0 || lp >= n_local) return;
   int pixel = local_to_pixel(sc, ps, lp);
   if (pixel < 0) return;
-  // fixed sample order; slot s * n_local + lp makes each sample's loads
-  // coalesced across the warp's pixels
-  const float* r = ps.rad + lp;
-  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
-  for (uint32_t s = 0; s < ps.S; ++s) {
-    size_t o = (size_t)s * n_local;
-    s0 += __ldg(r + o);
-    s1 += __ldg(r + ps.n_paths + o);
-    s2 += __ldg(r + 2u * ps.n_paths + o);
+  float t[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float q0 = part[c][0][lane] + part[c][1][lane], q1 = part[c][2][lane] + part[c][3][lane];
+    float q2 = part[c][4][lane] + part[c][5][lane], q3 = part[c][6][lane] + part[c][7][lane];
+    t[c] = (q0 + q1) + (q2 + q3);
   }
   float* a = accum + (size_t)pixel * 3;
-  float v0 = a[0] + s0 * inv_spp, v1 = a[1] + s1 * inv_spp, v2 = a[2] + s2 * inv_spp;
+  float v0 = a[0] + t[0] * inv_spp, v1 = a[1] + t[1] * inv_spp, v2 = a[2] + t[2] * inv_spp;
   a[0] = v0;
   a[1] = v1;
   a[2] = v2;
@@ -1350,8 +1372,8 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
       scratch_free(&scr, st);
       return rc;
     }
-    uint32_t nb = (uint32_t)((n_local + 255) / 256);
-    accumulate_kernel<<<nb, 256, 0, st>>>(sc, ps, (uint32_t)n_local, inv_spp, d_accum);
+    accumulate_kernel<<<(uint32_t)((n_local + 31) / 32), 256, 0, st>>>(sc, ps, (uint32_t)n_local,
+                                                                      inv_spp, d_accum);
     g_launches++;
     MF_CUDA(cudaGetLastError());
   }
