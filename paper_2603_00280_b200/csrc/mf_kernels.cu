@@ -545,17 +545,18 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 // ended (9 of 32).  Here every warp owns kPool path slots in shared memory
 // (SoA, one tag per slot) and each iteration runs ONE stage on 32 slots that
 // wait for it:
-//   R  raygen into 32 empty slots (while path indices last);
-//   A  flight and, on a collision, NEE and the mixture branch: the cheap
-//      hemisphere branch samples in place (phase tail, depth cap, RR), the
-//      Beckmann branch parks the path for B;
-//   B  Beckmann visible-normal sample + phase tail + depth cap / RR.
-// B and R run only as full warps (until the work runs out); with 96 slots
-// and fewer than 32 in each of B and R, A always has more than 32.
-// Each path runs exactly the arithmetic of path_kernel<0> with the same
-// random stream (pixel, sample, segment, call), so the image is bit-identical
-// to it (tests/test_gpu_render.py); only the order in which paths advance
-// changes.
+//   R  raygen into empty slots, then the first flight;
+//   B  Beckmann visible normal of parked paths;
+//   T  phase tail (pdf, weight, new direction) + depth cap / RR of paths
+//      whose visible normal is drawn, then their next flight;
+// where "flight" = free flight + NEE + the mixture branch: the Beckmann
+// branch parks the path for B, the cheap hemisphere branch draws its normal
+// in place and parks the path for T.  Every slot is empty or waits for B or
+// T, so with 96 slots one of the three always has a full warp of 32 until
+// the path indices run out.  Each path executes exactly the megakernel's
+// arithmetic on the same Philox stream, so the image is bit-identical to
+// path_kernel<0> (tests/test_gpu_render.py); only the order in which paths
+// advance changes.
 
 #ifndef MF_POOL
 #define MF_POOL 96
@@ -563,43 +564,70 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 constexpr int kPool = MF_POOL;
 static_assert(kPool % 32 == 0 && kPool <= 128, "pool size: whole warps of slots");
 constexpr int kPoolWords = kPool / 32;
-constexpr int kPoolF = 18;   // pos3 dir3 T3 L3 sig_o sig_b u_br u_s2 u_rr lphi
-constexpr int kPoolU = 4;    // pid pixel sample bounce
 constexpr int kWarpsPerBlock = kBlock / 32;
 
-enum PoolStage : int { kStageFlight = 0, kStageBeck = 1, kStageRaygen = 2 };
-constexpr uint8_t kTagEmpty = 0, kTagFlight = 1, kTagBeck = 2;
+enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageTail = 2 };
+constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagTail = 2;
 
+// float fields of a slot: dir3 T3 L3 sig_o sig_b u_rr lphi, then a union of
+// (u_br, u_s2) while waiting for B and (wm3, vm) while waiting for T, then
+// pos.z (read by the flight after a grazing one, whose log Phi is unknown)
+// and pos.x, pos.y when a point light reads positions
+enum PoolF : int { kFDir = 0, kFT = 3, kFL = 6, kFSigO = 9, kFSigB = 10, kFUrr = 11,
+                   kFLphi = 12, kFU = 13, kFVm = 16, kFPz = 17, kFPxy = 18 };
+template <bool kPoint>
 struct PoolSlots {
-  float f[kPoolF][kPool];
-  uint32_t u[kPoolU][kPool];
+  float f[kPoint ? 20 : 18][kPool];
+  uint32_t u[4][kPool];   // pid pixel sample bounce
   uint8_t tag[kPool];
-  uint8_t list[32];   // this iteration's slot of each lane
+  uint8_t list[32];       // this iteration's slot of each lane
 };
 
-__device__ __forceinline__ void pool_store(PoolSlots& P, int s, const PathState& st, float sig_o,
-                                           float sig_b) {
-  P.f[0][s] = st.pos.x; P.f[1][s] = st.pos.y; P.f[2][s] = st.pos.z;
-  P.f[3][s] = st.dir.x; P.f[4][s] = st.dir.y; P.f[5][s] = st.dir.z;
-  P.f[6][s] = st.T.x;   P.f[7][s] = st.T.y;   P.f[8][s] = st.T.z;
-  P.f[9][s] = st.L.x;   P.f[10][s] = st.L.y;  P.f[11][s] = st.L.z;
-  P.f[12][s] = sig_o;   P.f[13][s] = sig_b;
-  P.f[14][s] = st.u_br; P.f[15][s] = st.u_s2; P.f[16][s] = st.u_rr;
-  P.f[17][s] = st.lphi;
+template <bool kPoint>
+__device__ __forceinline__ void pool_store(PoolSlots<kPoint>& P, int s, const PathState& st,
+                                           float sig_o, float sig_b, uint8_t tag, V3 wm,
+                                           float vm) {
+  P.f[kFDir][s] = st.dir.x; P.f[kFDir + 1][s] = st.dir.y; P.f[kFDir + 2][s] = st.dir.z;
+  P.f[kFT][s] = st.T.x;     P.f[kFT + 1][s] = st.T.y;     P.f[kFT + 2][s] = st.T.z;
+  P.f[kFL][s] = st.L.x;     P.f[kFL + 1][s] = st.L.y;     P.f[kFL + 2][s] = st.L.z;
+  P.f[kFSigO][s] = sig_o;   P.f[kFSigB][s] = sig_b;
+  P.f[kFUrr][s] = st.u_rr;  P.f[kFLphi][s] = st.lphi;
+  if (tag == kTagBeck) {
+    P.f[kFU][s] = st.u_br;  P.f[kFU + 1][s] = st.u_s2;
+  } else {
+    P.f[kFU][s] = wm.x;     P.f[kFU + 1][s] = wm.y;     P.f[kFU + 2][s] = wm.z;
+    P.f[kFVm][s] = vm;
+  }
+  P.f[kFPz][s] = st.pos.z;
+  if constexpr (kPoint) {
+    P.f[kFPxy][s] = st.pos.x; P.f[kFPxy + 1][s] = st.pos.y;
+  }
   P.u[0][s] = st.pid;   P.u[1][s] = st.rng.pixel; P.u[2][s] = st.rng.sample;
   P.u[3][s] = (uint32_t)st.bounce;
 }
 
-__device__ __forceinline__ void pool_load(const PoolSlots& P, int s, const PassDev& ps,
-                                          PathState& st, float& sig_o, float& sig_b) {
-  st.pos = v3(P.f[0][s], P.f[1][s], P.f[2][s]);
-  st.dir = v3(P.f[3][s], P.f[4][s], P.f[5][s]);
-  st.T = v3(P.f[6][s], P.f[7][s], P.f[8][s]);
-  st.L = v3(P.f[9][s], P.f[10][s], P.f[11][s]);
-  sig_o = P.f[12][s];
-  sig_b = P.f[13][s];
-  st.u_br = P.f[14][s]; st.u_s2 = P.f[15][s]; st.u_rr = P.f[16][s];
-  st.lphi = P.f[17][s];
+template <bool kPoint>
+__device__ __forceinline__ void pool_load(const PoolSlots<kPoint>& P, int s, const PassDev& ps,
+                                          bool beck, PathState& st, float& sig_o, float& sig_b,
+                                          V3& wm, float& vm) {
+  st.dir = v3(P.f[kFDir][s], P.f[kFDir + 1][s], P.f[kFDir + 2][s]);
+  st.T = v3(P.f[kFT][s], P.f[kFT + 1][s], P.f[kFT + 2][s]);
+  st.L = v3(P.f[kFL][s], P.f[kFL + 1][s], P.f[kFL + 2][s]);
+  sig_o = P.f[kFSigO][s];
+  sig_b = P.f[kFSigB][s];
+  st.u_rr = P.f[kFUrr][s];
+  st.lphi = P.f[kFLphi][s];
+  if (beck) {
+    st.u_br = P.f[kFU][s];
+    st.u_s2 = P.f[kFU + 1][s];
+  } else {
+    wm = v3(P.f[kFU][s], P.f[kFU + 1][s], P.f[kFU + 2][s]);
+    vm = P.f[kFVm][s];
+  }
+  // x, y are never read without a point light (a single plane is
+  // translation invariant)
+  if constexpr (kPoint) st.pos = v3(P.f[kFPxy][s], P.f[kFPxy + 1][s], P.f[kFPz][s]);
+  else st.pos = v3(0.0f, 0.0f, P.f[kFPz][s]);
   st.pid = P.u[0][s];
   st.rng.k0 = ps.k0;
   st.rng.k1 = ps.k1;
@@ -646,12 +674,13 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
 template <bool kPoint>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
                                                                   const __grid_constant__ PassDev ps) {
-  __shared__ PoolSlots pools[kWarpsPerBlock];
+  __shared__ PoolSlots<kPoint> pools[kWarpsPerBlock];
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  PoolSlots& P = pools[threadIdx.x >> 5];
+  PoolSlots<kPoint>& P = pools[threadIdx.x >> 5];
   const MediumK& m = sc.media[0];
+  const Frame fr = frame_about(v3(0.0f, 0.0f, 1.0f));
   Counters cn;
 #pragma unroll
   for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
@@ -661,22 +690,23 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
   bool exhausted = false;    // warp-uniform
   while (true) {
     // per-stage slot masks from the tags (lane l reads slots l, l+32, ...)
-    unsigned qa[kPoolWords], qb[kPoolWords], qe[kPoolWords];
-    int na = 0, nb = 0, ne = 0;
+    unsigned qb[kPoolWords], qt[kPoolWords], qe[kPoolWords];
+    int nb = 0, nt = 0, ne = 0;
 #pragma unroll
     for (int w = 0; w < kPoolWords; ++w) {
       uint8_t t = P.tag[w * 32 + lane];
-      qa[w] = __ballot_sync(full, t == kTagFlight);
       qb[w] = __ballot_sync(full, t == kTagBeck);
+      qt[w] = __ballot_sync(full, t == kTagTail);
       qe[w] = exhausted ? 0u : __ballot_sync(full, t == kTagEmpty);
-      na += __popc(qa[w]);
       nb += __popc(qb[w]);
+      nt += __popc(qt[w]);
       ne += __popc(qe[w]);
     }
     int stage;
     if (nb >= 32) stage = kStageBeck;
+    else if (nt >= 32) stage = kStageTail;
     else if (ne >= 32) stage = kStageRaygen;
-    else if (na > 0) stage = kStageFlight;
+    else if (nt > 0 && nt >= nb) stage = kStageTail;
     else if (nb > 0) stage = kStageBeck;
     else if (ne > 0) stage = kStageRaygen;
     else break;
@@ -684,7 +714,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
     int n = 0;
 #pragma unroll
     for (int w = 0; w < kPoolWords; ++w) {
-      unsigned c = stage == kStageFlight ? qa[w] : (stage == kStageBeck ? qb[w] : qe[w]);
+      unsigned c = stage == kStageBeck ? qb[w] : (stage == kStageTail ? qt[w] : qe[w]);
       int r = n + __popc(c & lt);
       if (((c >> lane) & 1u) && r < 32) P.list[r] = (uint8_t)(w * 32 + lane);
       n += __popc(c);
@@ -695,13 +725,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
 
     uint8_t tag = kTagEmpty;
     PathState st;
-    float sig_o = 0.0f, sig_b = 0.0f;
-    bool sample = false;
-    Frame fr = frame_about(v3(0.0f, 0.0f, 1.0f));
-    bool live = false;
+    float sig_o = 0.0f, sig_b = 0.0f, vm = 0.0f;
+    V3 wm = v3(0.0f, 0.0f, 0.0f);
+    bool fly = false;
     if (stage == kStageRaygen) {
-      // raygen, full width: path indices with one atomicAdd; the new paths
-      // go straight on to their first flight below
+      // raygen, full width: path indices with one atomicAdd
       unsigned need = __ballot_sync(full, slot >= 0);
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(ps.counter, (unsigned)__popc(need));
@@ -710,76 +738,72 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       uint32_t my = base + (uint32_t)lane;
       if (slot >= 0 && my < ps.n_paths && start_path<false>(sc, ps, st, my)) {
         cn.v[kStPaths]++;
-        live = true;
+        fly = true;
       }
     } else if (slot >= 0) {
-      pool_load(P, slot, ps, st, sig_o, sig_b);
-      live = true;
-    }
-    if (live) {
-      if (stage != kStageBeck) {
-        if (!flight_stage<0>(sc, st, cn)) {
-          finish_path(ps, st, cn);
-        } else {
-          // scatter_stages<0> up to the mixture branch
-          V3 pos = st.cpos;
-          V3 wo = to_local(fr, st.dir);
-          sig_o = st.csig;
-          cn.v[kStScatters]++;
-          if (!(sig_o >= 1e-12f)) {
-            cn.v[kStDegenerate]++;
-            finish_path(ps, st, cn);
+      pool_load<kPoint>(P, slot, ps, stage == kStageBeck, st, sig_o, sig_b, wm, vm);
+      V3 v = neg3(to_local(fr, st.dir));
+      if (stage == kStageBeck) {
+        // Beckmann branch of the mixture (phase_sample, two-uniform convention)
+        float uu = remap_branch_uniform(st.u_br, m.mix);
+        int iters = 0;
+        wm = beckmann_visible_normal(m, v, uu, st.u_s2, &iters);
+        vm = dot3(v, wm);
+        cn.v[kStSlopeIters] += (uint32_t)iters;
+        tag = kTagTail;
+      } else {
+        // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
+        PhaseSample smp = phase_sample_tail(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
+        st.dir = to_world(fr, smp.wi);
+        st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
+        st.bounce++;
+        bool done = false;
+        if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+          done = true;
+        } else if (st.bounce > 8) {                    // render.py:96-105
+          float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+          if (st.u_rr >= q) {
+            done = true;
           } else {
-            planar_nee<kPoint>(sc, st, cn, fr, wo, sig_o, pos);
-            st.pos = pos;
-            sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
-            // the cheap hemisphere branch samples right here; the Beckmann
-            // branch waits for a full warp of Beckmann samples
-            if (sig_b > 1e-12f && st.u_br < m.mix) tag = kTagBeck;
-            else sample = true;
+            st.T = mul3(st.T, 1.0f / q);
           }
         }
-      } else {
-        sample = true;
+        if (done) finish_path(ps, st, cn);
+        else fly = true;
       }
     }
     __syncwarp();
-    if (sample) {
-      // stage 3 of scatter_stages<0>: phase sample, depth cap, RR
-      V3 wo = to_local(fr, st.dir);
-      V3 v = neg3(wo);
-      float uu = remap_branch_uniform(st.u_br, m.mix);
-      V3 wm;
-      float vm;
-      int iters = 0;
-      if (stage == kStageBeck) {
-        wm = beckmann_visible_normal(m, v, uu, st.u_s2, &iters);
-        vm = dot3(v, wm);
+    if (fly) {
+      // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
+      if (!flight_stage<0>(sc, st, cn)) {
+        finish_path(ps, st, cn);
       } else {
-        wm = hemisphere_about(v, uu, st.u_s2);
-        vm = uu;
-      }
-      PhaseSample smp = phase_sample_tail(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
-      cn.v[kStSlopeIters] += (uint32_t)iters;
-      st.dir = to_world(fr, smp.wi);
-      st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
-      st.bounce++;
-      bool done = false;
-      if (st.bounce >= ps.max_bounces) {             // render.py:92-94
-        done = true;
-      } else if (st.bounce > 8) {                    // render.py:96-105
-        float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
-        if (st.u_rr >= q) {
-          done = true;
+        V3 pos = st.cpos;
+        V3 wo = to_local(fr, st.dir);
+        sig_o = st.csig;
+        cn.v[kStScatters]++;
+        if (!(sig_o >= 1e-12f)) {
+          cn.v[kStDegenerate]++;
+          finish_path(ps, st, cn);
         } else {
-          st.T = mul3(st.T, 1.0f / q);
+          planar_nee<kPoint>(sc, st, cn, fr, wo, sig_o, pos);
+          st.pos = pos;
+          sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
+          if (sig_b > 1e-12f && st.u_br < m.mix) {
+            tag = kTagBeck;
+          } else {
+            // hemisphere branch: the normal now (cheap), the tail in stage T
+            V3 v = neg3(wo);
+            float uu = remap_branch_uniform(st.u_br, m.mix);
+            wm = hemisphere_about(v, uu, st.u_s2);
+            vm = uu;   // z of wm in v's frame, exactly (ndf.py:375-380)
+            tag = kTagTail;
+          }
         }
       }
-      if (done) finish_path(ps, st, cn);
-      else tag = kTagFlight;
     }
     if (slot >= 0) {
-      if (tag != kTagEmpty) pool_store(P, slot, st, sig_o, sig_b);
+      if (tag != kTagEmpty) pool_store<kPoint>(P, slot, st, sig_o, sig_b, tag, wm, vm);
       P.tag[slot] = tag;
     }
     __syncwarp();
