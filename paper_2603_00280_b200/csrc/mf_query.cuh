@@ -98,7 +98,7 @@ MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo,
   q.phase = phase_eval(m, wol, wil, sig_safe);
   q.pdf = phase_pdf(m, wol, wil, sig_b);
   float uu = remap_branch_uniform(u1, m.mix);
-  PhaseSample s = phase_sample(m, wol, sig_safe, sig_b, u1, uu, u2, mask);
+  PhaseSample s = phase_sample<true>(m, wol, sig_safe, sig_b, u1, uu, u2, mask);
   q.ws = to_world(fr, s.wi);
   q.pdf_s = s.pdf;
   q.w = s.weight;
