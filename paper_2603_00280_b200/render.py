@@ -81,7 +81,13 @@ def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, 
     # accumulate kernels count non-finite / negative radiance and mf_render
     # raises NumericFailureError (a MacrofacetError) for any
     img, _ = render_device(scene, spp, seed, max_bounces=max_bounces, tile=tile, stats=True)
-    return RadianceImage(pixels=img.to(torch.float64).cpu().numpy(),
+    # float64 on the device, one copy into page-locked memory (torch's
+    # caching host allocator recycles it); the array keeps its buffer alive
+    d64 = img.to(torch.float64)
+    host = torch.empty(d64.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(d64, non_blocking=True)
+    torch.cuda.current_stream(d64.device).synchronize()
+    return RadianceImage(pixels=host.numpy(),
                          meta={"seed": int(seed), "spp": int(spp), "scene_hash": scene_hash})
 
 

@@ -1,4 +1,4 @@
-"""Host-side breakdown of one render() call on config 2 (GPU box)."""
+"""Host-side cost of render() variants on config 2 (GPU box)."""
 import sys
 import time
 
@@ -7,35 +7,43 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2603_00280_b200 as mf  # noqa: E402
-from paper_2603_00280_b200 import configs  # noqa: E402
+from paper_2603_00280_b200 import configs, _lib  # noqa: E402
+from paper_2603_00280_b200.image import RadianceImage  # noqa: E402
+from paper_2603_00280_b200.render import render_device  # noqa: E402
 
 scene = configs.config2_scene()
-for _ in range(3):
-    mf.render(scene, 64, 1, max_bounces=16)
-T = {}
 
 
-def tick(k, t0):
-    T[k] = T.get(k, 0.0) + (time.perf_counter() - t0) * 1e3
-    return time.perf_counter()
+def cur():
+    return mf.render(scene, 64, 1, max_bounces=16)
 
 
-N = 20
-for _ in range(N):
+def pinned():
+    img, _ = render_device(scene, 64, 1, max_bounces=16, stats=True)
+    d64 = img.to(torch.float64)
+    h = torch.empty(d64.shape, dtype=torch.float64, pin_memory=True)
+    h.copy_(d64, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return RadianceImage(pixels=h.numpy(), meta={})
+
+
+def dev_only():
+    img, _ = render_device(scene, 64, 1, max_bounces=16, stats=True)
+    return img
+
+
+def dev_nostats():
+    img, _ = render_device(scene, 64, 1, max_bounces=16, stats=False)
+    torch.cuda.synchronize()
+    return img
+
+
+for fn in (cur, pinned, dev_only, dev_nostats, cur, pinned, dev_only, dev_nostats):
+    for _ in range(3):
+        fn()
     torch.cuda.synchronize()
     t = time.perf_counter()
-    img, st = mf.render_device(scene, 64, 1, max_bounces=16, stats=True)
-    t = tick("render_device(stats)", t)
-    flags = torch.stack(((~torch.isfinite(img)).any(), (img < 0.0).any()))
-    t = tick("flags (async)", t)
-    pixels = img.to(torch.float64).cpu().numpy()
-    t = tick("double+d2h", t)
-    f = flags.cpu().numpy()
-    t = tick("flags d2h", t)
-    out = mf.RadianceImage(pixels=pixels, meta={})
-    t = tick("RadianceImage", t)
+    for _ in range(30):
+        fn()
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    mf.render(scene, 64, 1, max_bounces=16)
-    t = tick("render() total", t)
-print({k: round(v / N, 3) for k, v in T.items()})
+    print(fn.__name__, round((time.perf_counter() - t) / 30 * 1e3, 4), "ms")
