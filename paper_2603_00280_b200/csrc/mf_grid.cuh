@@ -160,7 +160,8 @@ MF_HD bool grid_box(const GridDev& g, V3 o, V3 d, float* t0, float* t1) {
 // Random draws: blocks (segment, call0 + k) of the path's Philox stream.
 template <typename RngBlock>
 MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_block,
-                         uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max) {
+                         uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
+                         float rr_min = 0.0f) {
   GridWalk w;
   w.outcome = 0;
   w.pos = pos;
@@ -220,6 +221,19 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
         if (st > mu * 1.00001f) w.violations++;
         if (ratio) {
           w.weight *= fmaxf(1.0f - st / mu, 0.0f);
+          if (w.weight < rr_min && w.weight > 0.0f) {
+            // Russian roulette on the weight (see walk() in mf_transport.cuh)
+            if (avail == 0) {
+              bits = rng_block(call++);
+              avail = 4;
+            }
+            float ur = u01(bits.x);
+            bits.x = bits.y;
+            bits.y = bits.z;
+            bits.z = bits.w;
+            --avail;
+            w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
+          }
           if (!(w.weight > 0.0f)) {
             w.pos = p;
             return w;

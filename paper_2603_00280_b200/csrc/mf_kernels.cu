@@ -228,6 +228,13 @@ __device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t pixel, f
   }
 }
 
+// Russian-roulette threshold of the renderer's shadow-ray weights (walk());
+// the transmittance_estimate API (ratio_kernel) keeps plain ratio tracking
+#ifndef MF_SHADOW_RR
+#define MF_SHADOW_RR 0.05f
+#endif
+constexpr float kShadowRR = MF_SHADOW_RR;
+
 // shadow transmittance from pos towards unit direction wl over distance t_max
 template <int kMode>
 __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& st, V3 pos, V3 wl,
@@ -242,12 +249,13 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
     uint32_t seg = (uint32_t)st.bounce;
     GridWalk w = grid_walk(sc.grid, sc.media[0],
                            [&](uint32_t call) { return rng_block(r, seg, call); }, kCallShadow,
-                           pos, wl, true, t_max);
+                           pos, wl, true, t_max, kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)w.steps;
     cn.v[kStViolations] += (uint32_t)w.violations;
     return w.weight;
   } else {
-    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max);
+    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max,
+                        kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
     return w.weight;

@@ -282,8 +282,13 @@ MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mu
 // ratio == false: delta tracking (collision mode); ratio == true: ratio
 // tracking of the transmittance up to distance t_max (shadow rays).
 // Random draws: Philox blocks (segment, call0 + k), 4 uniforms each.
+// rr_min > 0 (ratio mode): Russian roulette on the ratio-tracking weight --
+// below rr_min it survives with probability weight / rr_min at weight rr_min
+// (unbiased: the expectation of every sample is unchanged), so a shadow ray
+// through an optically thick shell stops once it can no longer contribute
+// instead of tracking the whole shell.
 MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, uint32_t call0,
-                      V3 pos, V3 dir, bool ratio, float t_max) {
+                      V3 pos, V3 dir, bool ratio, float t_max, float rr_min = 0.0f) {
   WalkResult w;
   w.outcome = kEscaped;
   w.prim = -1;
@@ -405,6 +410,16 @@ MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, 
     if (st > maj * 1.00001f) w.violations++;
     if (ratio) {
       w.weight *= fmaxf(1.0f - st / maj, 0.0f);
+      if (w.weight < rr_min && w.weight > 0.0f) {
+        if (avail == 0) {
+          bits = rng_block(rng, segment, call++);
+          avail = 4;
+        }
+        float ur = u01(bits.x);
+        bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
+        --avail;
+        w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
+      }
       if (!(w.weight > 0.0f)) {
         w.outcome = kEscaped;
         w.pos = pos;

@@ -103,9 +103,10 @@ extern "C" {
 // Host run of the device walker (csrc/mf_transport.cuh walk) for n rays:
 // org/dir SoA [3][n]; path i keyed (pixel = i, sample = 0, segment 0).
 // out: state[n] (0 escaped, 1 absorbed, 2 collided), pos SoA [3][n], weight[n]
+// rr_min: Russian-roulette threshold of ratio weights (0: plain ratio tracking)
 int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t n, uint64_t seed,
              int ratio, int32_t* state, float* pos, float* weight, float majorant_scale,
-             int64_t* violations) {
+             int64_t* violations, float rr_min) {
   SceneDev sc;
   std::string err;
   if (build_scene(*scene, &sc, &err) != MF_OK) return 1;
@@ -119,7 +120,7 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
     if (sc.has_grid) {
       GridWalk w = grid_walk(sc.grid, sc.media[0],
                              [&](uint32_t call) { return rng_block(r, 0u, call); },
-                             ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY);
+                             ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY, rr_min);
       state[i] = w.outcome;
       pos[i] = w.pos.x;
       pos[n + i] = w.pos.y;
@@ -128,7 +129,7 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
       *violations += w.violations;
       continue;
     }
-    WalkResult w = walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY);
+    WalkResult w = walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY, rr_min);
     state[i] = w.outcome;
     pos[i] = w.pos.x;
     pos[n + i] = w.pos.y;

@@ -48,7 +48,7 @@ def run_walk(lib, cs, o, d, n, ratio=False, seed=3):
                         D.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(n), ctypes.c_uint64(seed),
                         int(ratio), st.ctypes.data_as(ctypes.c_void_p),
                         pos.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p),
-                        ctypes.c_float(1.0), ctypes.byref(v)) == 0
+                        ctypes.c_float(1.0), ctypes.byref(v), ctypes.c_float(0.0)) == 0
     return st, pos, w, v.value
 
 

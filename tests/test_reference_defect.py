@@ -86,7 +86,7 @@ def test_device_walker_matches_quadrature(host_math):
                                   ctypes.c_uint64(3), 0, st.ctypes.data_as(ctypes.c_void_p),
                                   pos.ctypes.data_as(ctypes.c_void_p),
                                   w.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(1.0),
-                                  ctypes.byref(viol)) == 0
+                                  ctypes.byref(viol), ctypes.c_float(0.0)) == 0
         ex = exact_escape(ORIGIN, d)
         se = np.sqrt(max(ex * (1 - ex), 1e-5) / n)
         assert abs(np.mean(st == 0) - ex) <= 4 * se, (d, np.mean(st == 0), ex)
