@@ -247,7 +247,9 @@ int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d
  * cells an upper bound of the extinction over the cell and over all
  * directions (exact min/max of the trilinear SDF and sigma over the cell's
  * vertices; max over sigma samples and directions of rho * sigma_proj).
- * Writes d_majorant_out (n_maj^3 floats). */
+ * Cells without medium store -D instead, D >= 1 the Chebyshev distance in
+ * cells to the nearest cell with medium (capped at 16): the walker's
+ * empty-space jumps.  Writes d_majorant_out (n_maj^3 floats). */
 int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* stream);
 
 /* ---------------------------------------------------------------------

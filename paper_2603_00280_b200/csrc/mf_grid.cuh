@@ -267,6 +267,27 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
       w.pos = fma3(dir, t1, pos);
       return w;   // escaped the grid (or reached the light)
     }
+    if (mu <= -2.0f) {
+      // empty space: jump (D - 1) cells in every axis, then restart the DDA
+      // (stepping the cheap DDA and the costly tentative collisions in
+      // separate re-converged loops was measured slower: 4.4 vs 3.2 ms)
+      float tj = t + (-mu - 1.0f) * fminf(fminf(dtx, dty), dtz);
+      if (tj >= t1) {
+        w.pos = fma3(dir, t1, pos);
+        return w;
+      }
+      if (tj > t_exit) {
+        t = tj;
+        V3 q = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
+        cx = clampi((int)q.x, 0, n - 1);
+        cy = clampi((int)q.y, 0, n - 1);
+        cz = clampi((int)q.z, 0, n - 1);
+        tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
+        ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
+        tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
+        continue;
+      }
+    }
     t = t_exit;
     if (tx <= ty && tx <= tz) {
       cx += sx;
@@ -284,6 +305,38 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   }
   w.pos = fma3(dir, t, pos);
   return w;
+}
+
+// ---------------------------------------------------------------------------
+// empty-space distances (second pass of mf_grid_majorant)
+//
+// A cell whose majorant is 0 holds no medium.  Such cells store -D instead,
+// D = the Chebyshev distance (in cells) to the nearest cell with medium,
+// capped at kSkipMax + 1: from any point of the cell the ray can advance
+// (D - 1) cells in every axis without meeting medium, so grid_walk jumps
+// over empty space instead of stepping through it cell by cell (no random
+// numbers are drawn in empty cells, so the process is unchanged).
+constexpr int kSkipMax = 15;
+
+MF_HD float grid_cell_skip(const float* maj, int n, int cx, int cy, int cz) {
+  if (maj[((size_t)cx * n + cy) * n + cz] > 0.0f) return maj[((size_t)cx * n + cy) * n + cz];
+  for (int k = 1; k <= kSkipMax; ++k) {
+    // the shell of the (2k+1)^3 cube around the cell
+    for (int i = cx - k; i <= cx + k; ++i) {
+      if (i < 0 || i >= n) continue;
+      bool face_i = i == cx - k || i == cx + k;
+      for (int j = cy - k; j <= cy + k; ++j) {
+        if (j < 0 || j >= n) continue;
+        bool face_j = face_i || j == cy - k || j == cy + k;
+        int step = face_j ? 1 : 2 * k;
+        for (int l = cz - k; l <= cz + k; l += step) {
+          if (l < 0 || l >= n) continue;
+          if (maj[((size_t)i * n + j) * n + l] > 0.0f) return -(float)k;
+        }
+      }
+    }
+  }
+  return -(float)(kSkipMax + 1);
 }
 
 // ---------------------------------------------------------------------------

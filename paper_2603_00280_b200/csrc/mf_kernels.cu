@@ -926,6 +926,14 @@ __global__ void __launch_bounds__(128) grid_majorant_kernel(const __grid_constan
   out[c] = grid_cell_majorant(g, cx, cy, cz);
 }
 
+// second pass: empty cells store -(distance to medium) (grid_cell_skip);
+// in place is safe -- only the sign of a neighbour is read
+__global__ void __launch_bounds__(128) grid_skip_kernel(float* maj, int n) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n * n * n) return;
+  maj[c] = grid_cell_skip(maj, n, c / (n * n), (c / n) % n, c % n);
+}
+
 // ---------------------------------------------------------------------------
 // roofline microbenchmarks: 8 independent FFMA chains / 4 MUFU.EX2 chains
 
@@ -1176,6 +1184,10 @@ int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* str
   int cells = grid->n_maj * grid->n_maj * grid->n_maj;
   grid_majorant_kernel<<<(cells + 127) / 128, 128, 0, (cudaStream_t)stream>>>(sc.grid,
                                                                               d_majorant_out);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  grid_skip_kernel<<<(cells + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_majorant_out,
+                                                                          grid->n_maj);
   g_launches++;
   MF_CUDA(cudaGetLastError());
   return MF_OK;

@@ -166,6 +166,7 @@ int mfh_grid_majorant(const mf_grid_field* grid, float* out) {
   if (build_scene(tmp, &sc, &err) != MF_OK) return 1;
   int n = grid->n_maj;
   for (int c = 0; c < n * n * n; ++c) out[c] = grid_cell_majorant(sc.grid, c / (n * n), (c / n) % n, c % n);
+  for (int c = 0; c < n * n * n; ++c) out[c] = grid_cell_skip(out, n, c / (n * n), (c / n) % n, c % n);
   return 0;
 }
 

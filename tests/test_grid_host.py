@@ -102,3 +102,17 @@ def test_config5_majorant_bounds_extinction(host_math):
         assert viol == 0
         _, _, w, viol = run_walk(host_math, cs, o, d, n // 8, ratio=True, seed=21 + k)
         assert viol == 0 and np.all((w >= 0) & (w <= 1))
+
+
+def test_majorant_empty_space_distances(host_math):
+    """Cells without medium hold -D, D the Chebyshev distance (cells) to the
+    nearest cell with medium, capped at 16 (grid_walk's empty-space jumps)."""
+    sdf, sigma = config5_fields(n_sdf=64, n_sigma=32)
+    n = 16
+    _, maj = grid_scene(sdf.values, sigma, 0.03, 0.08, n, host_math)
+    m = maj.reshape(n, n, n)
+    full = np.argwhere(m > 0)
+    assert len(full) and np.any(m < 0)
+    for c in np.argwhere(m <= 0):
+        d = int(np.min(np.max(np.abs(full - c), axis=1)))
+        assert m[tuple(c)] == -min(d, 16), (c, m[tuple(c)], d)
