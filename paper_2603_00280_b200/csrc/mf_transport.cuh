@@ -287,8 +287,19 @@ MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mu
 // (unbiased: the expectation of every sample is unchanged), so a shadow ray
 // through an optically thick shell stops once it can no longer contribute
 // instead of tracking the whole shell.
-MF_HD WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment, uint32_t call0,
-                      V3 pos, V3 dir, bool ratio, float t_max, float rr_min = 0.0f) {
+#ifndef MF_WALK_OUTLINE
+#define MF_WALK_OUTLINE 1
+#endif
+#if MF_WALK_OUTLINE && defined(__CUDACC__)
+#define MF_WALK_FN __host__ __device__ __noinline__
+#else
+#define MF_WALK_FN MF_HD
+#endif
+// Out of line on the device: the flight and the shadow walks share one copy
+// of the tracking loop in the instruction stream.
+MF_WALK_FN WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment,
+                           uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
+                           float rr_min = 0.0f) {
   WalkResult w;
   w.outcome = kEscaped;
   w.prim = -1;
