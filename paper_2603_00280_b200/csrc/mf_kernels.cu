@@ -245,11 +245,8 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
     float sig = sig_known >= 0.0f ? sig_known : proj_area(m, wl);
     return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig, st.lphi);
   } else if constexpr (kMode == 2) {
-    const PathRng& r = st.rng;
-    uint32_t seg = (uint32_t)st.bounce;
-    GridWalk w = grid_walk(sc.grid, sc.media[0],
-                           [&](uint32_t call) { return rng_block(r, seg, call); }, kCallShadow,
-                           pos, wl, true, t_max, kShadowRR);
+    GridWalk w = grid_walk_path(sc.grid, sc.media[0], st.rng, (uint32_t)st.bounce, kCallShadow,
+                                pos, wl, true, t_max, kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)w.steps;
     cn.v[kStViolations] += (uint32_t)w.violations;
     return w.weight;
@@ -286,11 +283,8 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
   st.csig = -1.0f;
   int outcome;
   if constexpr (kMode == 2) {
-    const PathRng& r = st.rng;
-    uint32_t seg = (uint32_t)st.bounce;
-    GridWalk w = grid_walk(sc.grid, sc.media[0],
-                           [&](uint32_t call) { return rng_block(r, seg, call); }, 1u, st.pos,
-                           st.dir, false, INFINITY);
+    GridWalk w = grid_walk_path(sc.grid, sc.media[0], st.rng, (uint32_t)st.bounce, 1u, st.pos,
+                                st.dir, false, INFINITY, 0.0f);
     cn.v[kStTrackSteps] += (uint32_t)w.steps;
     cn.v[kStViolations] += (uint32_t)w.violations;
     st.cpos = w.pos;
