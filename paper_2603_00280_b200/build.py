@@ -23,6 +23,8 @@ NVCC_FLAGS = [
     # explicit intrinsics are used where accuracy allows; keep IEEE exp/log
     # (no --use_fast_math) but approximate division / sqrt and FTZ
     "-prec-div=false", "-prec-sqrt=false", "-ftz=true",
+    # a value-returning function that can fall off its end is an error
+    "-Xcudafe", "--diag_error=940", "-Xcompiler", "-Werror=return-type",
     "-Xptxas", "-v",
 ]
 

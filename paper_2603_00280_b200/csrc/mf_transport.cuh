@@ -315,175 +315,221 @@ MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mu
 #endif
 // Out of line on the device: the flight and the shadow walks share one copy
 // of the tracking loop in the instruction stream.
+// Resumable walker state: walk_begin + walk_step (one iteration of the
+// tracking loop) let a kernel interleave the steps of many walks; walk()
+// runs one walk to the end.
+struct WalkState {
+  V3 p;          // current position
+  V3 dir;
+  float travel, t_max, weight, rr_min, lo_mult;
+  uint32_t call;
+  U4 bits;
+  int avail;
+  int steps, violations;
+  int outcome, prim;
+  V3 pos;        // final position
+  bool ratio;
+};
+
+MF_HD void walk_begin(WalkState& w, V3 pos, V3 dir, bool ratio, float t_max, uint32_t call0,
+                      float rr_min) {
+  w.p = pos;
+  w.dir = dir;
+  w.travel = 0.0f;
+  w.t_max = t_max;
+  w.weight = 1.0f;
+  w.rr_min = rr_min;
+  w.lo_mult = ratio ? -3.0f : -6.0f;
+  w.call = call0;
+  w.bits = U4{0, 0, 0, 0};
+  w.avail = 0;
+  w.steps = 0;
+  w.violations = 0;
+  w.outcome = kEscaped;
+  w.prim = -1;
+  w.pos = pos;
+  w.ratio = ratio;
+}
+
+// One iteration of the delta / ratio tracking loop (transport.py:196-297);
+// returns true when the walk has ended (w.outcome, w.pos, w.prim, w.weight).
+MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, WalkState& w) {
+  // fields, band membership, gaps (transport.py:197-212)
+  bool any_band = false;
+  float gap_min = INFINITY;
+  bool all_done = true;
+  float maj = 0.0f;
+  float cap = INFINITY;
+  float fs[kMaxPrims];
+  for (int j = 0; j < sc.n_prims; ++j) {
+    const PrimDev& p = sc.prims[j];
+    const MediumK& m = sc.media[j];
+    float f = prim_field(p, w.p);
+    fs[j] = f;
+    float lo = w.lo_mult * m.sigma, hi = 3.0f * m.sigma;
+    if (!w.ratio && f < lo) {
+      w.outcome = kAbsorbed;
+      w.pos = w.p;
+      return true;
+    }
+    if (f >= lo && f <= hi) {
+      any_band = true;
+      cap = fminf(cap, MF_STEP_FRAC * m.sigma);
+    } else {
+      float g = level_distance(p, w.p, w.dir, f > hi ? hi : lo);
+      gap_min = fminf(gap_min, g);
+      if (g < INFINITY) all_done = false;
+      cap = fminf(cap, fmaxf(g, sc.min_skip));
+    }
+  }
+  // majorant over the step [0, cap] (transport.py:226-231 with exact
+  // geometry): min of f along the step (planes: linear; spheres: closest
+  // approach) and, for media whose sigma(w) decreases with cos(theta), the
+  // direction factor at the step start (cos(theta) grows along a chord)
+  for (int j = 0; j < sc.n_prims; ++j) {
+    const PrimDev& p = sc.prims[j];
+    const MediumK& m = sc.media[j];
+    float f = fs[j];
+    float lo = w.lo_mult * m.sigma, hi = 3.0f * m.sigma;
+    if (!(f >= lo && f <= hi)) continue;
+    float fmin, dirf;
+    if (p.shape == 0) {
+      fmin = f + cap * fminf(w.dir.z, 0.0f);
+      dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az, w.dir);
+    } else {
+      V3 oc = sub3(w.p, p.c);
+      float b = dot3(oc, w.dir);
+      float r2 = dot3(oc, oc);
+      float ts = fminf(fmaxf(-b, 0.0f), cap);
+      fmin = fsqrt(fmaxf(fmaf(ts, ts + 2.0f * b, r2), 0.0f)) - p.radius;
+      if (sc.mx[j].area_monotone) {
+        float c = b * frsqrt(fmaxf(r2, 1e-30f));
+        c = fminf(fmaxf(c, -1.0f), 1.0f);
+        dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az,
+                                  v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c)) * 1.0001f;
+      } else {
+        dirf = sc.mx[j].sig_max;
+      }
+    }
+    float fb = fmaxf(fmin - 1e-6f * (1.0f + fabsf(f)), lo);
+    maj += mills(fb * m.inv_sigma) * m.inv_sigma * dirf;
+  }
+  if (!any_band) {
+    if (all_done || w.travel + gap_min >= w.t_max) {
+      w.outcome = kEscaped;
+      w.pos = w.p;
+      return true;
+    }
+    // float32: step past the level set by a few ulps of |w.p| so the next
+    // iteration lands inside the band (transport.py:221 uses min_skip)
+    float ulp = 4.8e-7f * (1.0f + fmaxf(fabsf(w.p.x), fmaxf(fabsf(w.p.y), fabsf(w.p.z))));
+    float skip = fmaxf(gap_min, sc.min_skip) + ulp;
+    w.p = fma3(w.dir, skip, w.p);
+    w.travel += skip;
+    return false;
+  }
+  if (w.avail == 0) {
+    w.bits = rng_block(rng, segment, w.call++);
+    w.avail = 4;
+  }
+  float u1 = u01(w.bits.x);
+  w.bits.x = w.bits.y; w.bits.y = w.bits.z; w.bits.z = w.bits.w;
+  --w.avail;
+  float dt = maj > 0.0f ? -flog(u1) / maj : INFINITY;
+  w.steps++;
+  if (dt > cap) {
+    w.p = fma3(w.dir, cap, w.p);
+    w.travel += cap;
+    if (w.ratio && w.travel >= w.t_max) {
+      w.outcome = kEscaped;
+      w.pos = w.p;
+      return true;
+    }
+    return false;
+  }
+  w.p = fma3(w.dir, dt, w.p);
+  w.travel += dt;
+  if (w.ratio && w.travel >= w.t_max) {
+    w.outcome = kEscaped;
+    w.pos = w.p;
+    return true;
+  }
+  float parts[kMaxPrims];
+  float st = 0.0f;
+  for (int j = 0; j < sc.n_prims; ++j) {
+    parts[j] = prim_extinction(sc, j, w.p, w.dir, w.lo_mult);
+    st += parts[j];
+  }
+  if (st > maj * 1.00001f) w.violations++;
+  if (w.ratio) {
+    w.weight *= fmaxf(1.0f - st / maj, 0.0f);
+    if (w.weight < w.rr_min && w.weight > 0.0f) {
+      if (w.avail == 0) {
+        w.bits = rng_block(rng, segment, w.call++);
+        w.avail = 4;
+      }
+      float ur = u01(w.bits.x);
+      w.bits.x = w.bits.y; w.bits.y = w.bits.z; w.bits.z = w.bits.w;
+      --w.avail;
+      w.weight = ur * w.rr_min < w.weight ? w.rr_min : 0.0f;
+    }
+    if (!(w.weight > 0.0f)) {
+      w.outcome = kEscaped;
+      w.pos = w.p;
+      return true;
+    }
+  } else {
+    if (w.avail == 0) {
+      w.bits = rng_block(rng, segment, w.call++);
+      w.avail = 4;
+    }
+    float u2 = u01(w.bits.x);
+    w.bits.x = w.bits.y; w.bits.y = w.bits.z; w.bits.z = w.bits.w;
+    --w.avail;
+    float pick = u2 * maj;
+    if (pick < st) {
+      // u2 * majorant doubles as the primitive selector (transport.py:276-279)
+      float acc = 0.0f;
+      int k = sc.n_prims - 1;
+      for (int j = 0; j < sc.n_prims; ++j) {
+        acc += parts[j];
+        if (pick < acc) {
+          k = j;
+          break;
+        }
+      }
+      w.outcome = kCollided;
+      w.prim = k;
+      w.pos = w.p;
+      return true;
+    }
+  }
+  return false;   // null collision: the walk goes on
+}
+
 MF_WALK_FN WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment,
                            uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
                            float rr_min = 0.0f) {
+  WalkState s;
+  walk_begin(s, pos, dir, ratio, t_max, call0, rr_min);
   WalkResult w;
-  w.outcome = kEscaped;
-  w.prim = -1;
-  w.weight = 1.0f;
-  w.steps = 0;
-  w.violations = 0;
-  float lo_mult = ratio ? -3.0f : -6.0f;
-  float travel = 0.0f;
-  uint32_t call = call0;
-  U4 bits = U4{0, 0, 0, 0};
-  int avail = 0;
   for (int iter = 0; iter < 1000000; ++iter) {
-    // fields, band membership, gaps (transport.py:197-212)
-    bool any_band = false;
-    float gap_min = INFINITY;
-    bool all_done = true;
-    float maj = 0.0f;
-    float cap = INFINITY;
-    float fs[kMaxPrims];
-    for (int j = 0; j < sc.n_prims; ++j) {
-      const PrimDev& p = sc.prims[j];
-      const MediumK& m = sc.media[j];
-      float f = prim_field(p, pos);
-      fs[j] = f;
-      float lo = lo_mult * m.sigma, hi = 3.0f * m.sigma;
-      if (!ratio && f < lo) {
-        w.outcome = kAbsorbed;
-        w.pos = pos;
-        return w;
-      }
-      if (f >= lo && f <= hi) {
-        any_band = true;
-        cap = fminf(cap, MF_STEP_FRAC * m.sigma);
-      } else {
-        float g = level_distance(p, pos, dir, f > hi ? hi : lo);
-        gap_min = fminf(gap_min, g);
-        if (g < INFINITY) all_done = false;
-        cap = fminf(cap, fmaxf(g, sc.min_skip));
-      }
-    }
-    // majorant over the step [0, cap] (transport.py:226-231 with exact
-    // geometry): min of f along the step (planes: linear; spheres: closest
-    // approach) and, for media whose sigma(w) decreases with cos(theta), the
-    // direction factor at the step start (cos(theta) grows along a chord)
-    for (int j = 0; j < sc.n_prims; ++j) {
-      const PrimDev& p = sc.prims[j];
-      const MediumK& m = sc.media[j];
-      float f = fs[j];
-      float lo = lo_mult * m.sigma, hi = 3.0f * m.sigma;
-      if (!(f >= lo && f <= hi)) continue;
-      float fmin, dirf;
-      if (p.shape == 0) {
-        fmin = f + cap * fminf(dir.z, 0.0f);
-        dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az, dir);
-      } else {
-        V3 oc = sub3(pos, p.c);
-        float b = dot3(oc, dir);
-        float r2 = dot3(oc, oc);
-        float ts = fminf(fmaxf(-b, 0.0f), cap);
-        fmin = fsqrt(fmaxf(fmaf(ts, ts + 2.0f * b, r2), 0.0f)) - p.radius;
-        if (sc.mx[j].area_monotone) {
-          float c = b * frsqrt(fmaxf(r2, 1e-30f));
-          c = fminf(fmaxf(c, -1.0f), 1.0f);
-          dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az,
-                                    v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c)) * 1.0001f;
-        } else {
-          dirf = sc.mx[j].sig_max;
-        }
-      }
-      float fb = fmaxf(fmin - 1e-6f * (1.0f + fabsf(f)), lo);
-      maj += mills(fb * m.inv_sigma) * m.inv_sigma * dirf;
-    }
-    if (!any_band) {
-      if (all_done || travel + gap_min >= t_max) {
-        w.outcome = kEscaped;
-        w.pos = pos;
-        return w;
-      }
-      // float32: step past the level set by a few ulps of |pos| so the next
-      // iteration lands inside the band (transport.py:221 uses min_skip)
-      float ulp = 4.8e-7f * (1.0f + fmaxf(fabsf(pos.x), fmaxf(fabsf(pos.y), fabsf(pos.z))));
-      float skip = fmaxf(gap_min, sc.min_skip) + ulp;
-      pos = fma3(dir, skip, pos);
-      travel += skip;
-      continue;
-    }
-    if (avail == 0) {
-      bits = rng_block(rng, segment, call++);
-      avail = 4;
-    }
-    float u1 = u01(bits.x);
-    bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
-    --avail;
-    float dt = maj > 0.0f ? -flog(u1) / maj : INFINITY;
-    w.steps++;
-    if (dt > cap) {
-      pos = fma3(dir, cap, pos);
-      travel += cap;
-      if (ratio && travel >= t_max) {
-        w.outcome = kEscaped;
-        w.pos = pos;
-        return w;
-      }
-      continue;
-    }
-    pos = fma3(dir, dt, pos);
-    travel += dt;
-    if (ratio && travel >= t_max) {
-      w.outcome = kEscaped;
-      w.pos = pos;
+    if (walk_step(sc, rng, segment, s)) {
+      w.outcome = s.outcome;
+      w.prim = s.prim;
+      w.pos = s.pos;
+      w.weight = s.weight;
+      w.steps = s.steps;
+      w.violations = s.violations;
       return w;
-    }
-    float parts[kMaxPrims];
-    float st = 0.0f;
-    for (int j = 0; j < sc.n_prims; ++j) {
-      parts[j] = prim_extinction(sc, j, pos, dir, lo_mult);
-      st += parts[j];
-    }
-    if (st > maj * 1.00001f) w.violations++;
-    if (ratio) {
-      w.weight *= fmaxf(1.0f - st / maj, 0.0f);
-      if (w.weight < rr_min && w.weight > 0.0f) {
-        if (avail == 0) {
-          bits = rng_block(rng, segment, call++);
-          avail = 4;
-        }
-        float ur = u01(bits.x);
-        bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
-        --avail;
-        w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
-      }
-      if (!(w.weight > 0.0f)) {
-        w.outcome = kEscaped;
-        w.pos = pos;
-        return w;
-      }
-    } else {
-      if (avail == 0) {
-        bits = rng_block(rng, segment, call++);
-        avail = 4;
-      }
-      float u2 = u01(bits.x);
-      bits.x = bits.y; bits.y = bits.z; bits.z = bits.w;
-      --avail;
-      float pick = u2 * maj;
-      if (pick < st) {
-        // u2 * majorant doubles as the primitive selector (transport.py:276-279)
-        float acc = 0.0f;
-        int k = sc.n_prims - 1;
-        for (int j = 0; j < sc.n_prims; ++j) {
-          acc += parts[j];
-          if (pick < acc) {
-            k = j;
-            break;
-          }
-        }
-        w.outcome = kCollided;
-        w.prim = k;
-        w.pos = pos;
-        return w;
-      }
     }
   }
   w.outcome = kAbsorbed;  // iteration cap: treated as lost (counted by the caller)
-  w.pos = pos;
+  w.prim = -1;
+  w.pos = s.p;
+  w.weight = s.weight;
   w.steps = -1;
+  w.violations = s.violations;
   return w;
 }
 

@@ -1,3 +1,4 @@
+import glob
 import os
 import subprocess
 import sys
@@ -23,11 +24,12 @@ def host_math():
     out_dir = os.path.join(ROOT, "tests", "native", "_build")
     so = os.path.join(out_dir, "libmf_host.so")
     src = os.path.join(ROOT, "tests", "native", "mf_host_shim.cpp")
-    deps = [src] + [os.path.join(ROOT, "paper_2603_00280_b200", "csrc", f)
-                    for f in ("mf_math.cuh", "mf_poly.inc", "mf_query.cuh", "mf_prepare.h")]
+    deps = [src] + sorted(glob.glob(os.path.join(ROOT, "paper_2603_00280_b200", "csrc", "*"))) + [
+        os.path.join(ROOT, "include", "macrofacet_b200.h")]
     if not os.path.exists(so) or any(os.path.getmtime(d) > os.path.getmtime(so) for d in deps):
         os.makedirs(out_dir, exist_ok=True)
         subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
+                        "-Wall", "-Wno-unknown-pragmas", "-Werror=return-type",
                         "-o", so, src], check=True)
     return ctypes.CDLL(so)
 
