@@ -48,6 +48,18 @@ def _params(spp, seed, max_bounces, tile, shard, rank, nranks, accumulate=False)
     return p
 
 
+def _c_scene(scene: ShellScene, device):
+    """The flattened C scene, built once per (immutable) scene and device."""
+    cache = scene.__dict__.get("_c_scene_cache")
+    if cache is None:
+        cache = {}
+        object.__setattr__(scene, "_c_scene_cache", cache)
+    cs = cache.get(device)
+    if cs is None:
+        cs = cache[device] = to_c_scene(scene)
+    return cs
+
+
 def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
                   shard="tiles", out=None, stats=False, stream=None, c_scene=None):
     """Render into a (H, W, 3) float32 CUDA tensor holding radiance / spp for
@@ -61,7 +73,7 @@ def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0,
     if out.dtype != torch.float32 or not out.is_cuda or not out.is_contiguous() or \
             tuple(out.shape) != (cam.height, cam.width, 3):
         raise ParameterDomainError("out must be a contiguous (H, W, 3) float32 CUDA tensor")
-    cs = c_scene if c_scene is not None else to_c_scene(scene)
+    cs = c_scene if c_scene is not None else _c_scene(scene, out.device.index)
     st = _lib.MfStats() if stats else None
     s = stream if stream is not None else _lib.stream_handle(torch, out.device)
     _lib.check(lib.mf_render(ctypes.byref(cs), ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
