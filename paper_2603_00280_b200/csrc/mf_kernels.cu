@@ -638,20 +638,40 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint>& P, int s, con
   st.bounce = (int)P.u[3][s];
 }
 
+// shadow transmittance towards the sun from a single-plane collision whose
+// log Phi is unknown (after a grazing flight): the general closed form, out
+// of line (one copy in the instruction stream, rarely executed)
+__device__ __noinline__ float planar_sun_tr_cold(const SceneDev& sc, float h, float lphi) {
+  return planar_shadow_tr(sc.media[0], sc.mx[0], h, sc.sun_to.z > 0.0f ? INFINITY : -INFINITY,
+                          sc.sun_to.z, sc.sun_sig, lphi);
+}
+
 // next-event estimation at a collision of the single plane (the stage-2
 // block of scatter_stages<0>, same arithmetic); kPoint: the scene has a point
-// light (its code is compiled out otherwise)
+// light (its code is compiled out otherwise).  The plane frame is the
+// identity (frame_about(0,0,1) = (1,0,0),(0,1,0),(0,0,1)), so directions are
+// used as they are.  With the collision's log Phi known, the sun's closed-form
+// transmittance (planar_shadow_tr) reduces to clamping it to the band and one
+// exponential: the sun end is a band edge fixed per render.
 template <bool kPoint>
 __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Counters& cn,
-                                           const Frame& fr, V3 wo, float sig_o, V3 pos) {
+                                           V3 wo, float sig_o, V3 pos) {
   const MediumK& m = sc.media[0];
   if (sc.has_sun) {
-    V3 wl = to_local(fr, sc.sun_to);
-    V3 ph = phase_eval(m, wo, wl, sig_o);
+    V3 ph = phase_eval(m, wo, sc.sun_to, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr<0>(sc, st, pos, sc.sun_to, INFINITY,
-                              sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
+      float tr;
+      if (st.lphi == st.lphi) {
+        const MediumExtra& mx = sc.mx[0];
+        float c = sc.sun_to.z;
+        float la = fminf(fmaxf(st.lphi, mx.lphi_lo_rat), mx.lphi_hi);
+        float lb = c > 0.0f ? mx.lphi_hi : mx.lphi_lo_rat;
+        tr = la == lb ? 1.0f
+                      : (fabsf(c) < 1e-6f ? 0.0f : expf(-sc.sun_sig / fabsf(c) * fabsf(lb - la)));
+      } else {
+        tr = planar_sun_tr_cold(sc, pos.z - sc.prims[0].z0, st.lphi);
+      }
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
     }
@@ -661,8 +681,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
     float r2 = dot3(d, d);
     float ir = frsqrt(r2);
     V3 wlw = mul3(d, ir);
-    V3 wl = to_local(fr, wlw);
-    V3 ph = phase_eval(m, wo, wl, sig_o);
+    V3 ph = phase_eval(m, wo, wlw, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr<0>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
@@ -682,7 +701,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
   const unsigned lt = (1u << lane) - 1u;
   PoolSlots<kPoint>& P = pools[threadIdx.x >> 5];
   const MediumK& m = sc.media[0];
-  const Frame fr = frame_about(v3(0.0f, 0.0f, 1.0f));
   Counters cn;
 #pragma unroll
   for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
@@ -744,7 +762,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       }
     } else if (slot >= 0) {
       pool_load<kPoint>(P, slot, ps, stage == kStageBeck, st, sig_o, sig_b, wm, vm);
-      V3 v = neg3(to_local(fr, st.dir));
+      V3 v = neg3(st.dir);   // the plane frame is the identity
       if (stage == kStageBeck) {
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
         float uu = remap_branch_uniform(st.u_br, m.mix);
@@ -756,7 +774,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       } else {
         // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
         PhaseSample smp = phase_sample_tail(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
-        st.dir = to_world(fr, smp.wi);
+        st.dir = smp.wi;
         st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
         st.bounce++;
         bool done = false;
@@ -781,14 +799,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
         finish_path(ps, st, cn);
       } else {
         V3 pos = st.cpos;
-        V3 wo = to_local(fr, st.dir);
+        V3 wo = st.dir;
         sig_o = st.csig;
         cn.v[kStScatters]++;
         if (!(sig_o >= 1e-12f)) {
           cn.v[kStDegenerate]++;
           finish_path(ps, st, cn);
         } else {
-          planar_nee<kPoint>(sc, st, cn, fr, wo, sig_o, pos);
+          planar_nee<kPoint>(sc, st, cn, wo, sig_o, pos);
           st.pos = pos;
           sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
           if (sig_b > 1e-12f && st.u_br < m.mix) {
