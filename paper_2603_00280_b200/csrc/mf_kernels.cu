@@ -575,67 +575,99 @@ constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagTail = 2;
 // (u_br, u_s2) while waiting for B and (wm3, vm) while waiting for T, then
 // pos.z (read by the flight after a grazing one, whose log Phi is unknown)
 // and pos.x, pos.y when a point light reads positions
-enum PoolF : int { kFDir = 0, kFT = 3, kFL = 6, kFSigO = 9, kFSigB = 10, kFUrr = 11,
-                   kFLphi = 12, kFU = 13, kFVm = 16, kFPz = 17, kFPxy = 18 };
-template <bool kPoint>
+// (grey scenes, kMono: T and L are one channel each and the slot is 4 words
+// shorter)
+template <bool kMono>
+struct PoolF {
+  static constexpr int kC = kMono ? 1 : 3;
+  static constexpr int kDir = 0, kT = 3, kL = 3 + kC, kSigO = 3 + 2 * kC, kSigB = kSigO + 1,
+                       kUrr = kSigO + 2, kLphi = kSigO + 3, kU = kSigO + 4, kVm = kSigO + 7,
+                       kPz = kSigO + 8, kPxy = kSigO + 9;
+};
+template <bool kPoint, bool kMono>
 struct PoolSlots {
-  float f[kPoint ? 20 : 18][kPool];
+  float f[PoolF<kMono>::kPxy + (kPoint ? 2 : 0)][kPool];
   uint32_t u[4][kPool];   // pid pixel sample bounce
   uint8_t tag[kPool];
   uint8_t list[32];       // this iteration's slot of each lane
 };
 
-template <bool kPoint>
-__device__ __forceinline__ void pool_store(PoolSlots<kPoint>& P, int s, const PathState& st,
+template <bool kPoint, bool kMono>
+__device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, const PathState& st,
                                            float sig_o, float sig_b, uint8_t tag, V3 wm,
                                            float vm) {
-  P.f[kFDir][s] = st.dir.x; P.f[kFDir + 1][s] = st.dir.y; P.f[kFDir + 2][s] = st.dir.z;
-  P.f[kFT][s] = st.T.x;     P.f[kFT + 1][s] = st.T.y;     P.f[kFT + 2][s] = st.T.z;
-  P.f[kFL][s] = st.L.x;     P.f[kFL + 1][s] = st.L.y;     P.f[kFL + 2][s] = st.L.z;
-  P.f[kFSigO][s] = sig_o;   P.f[kFSigB][s] = sig_b;
-  P.f[kFUrr][s] = st.u_rr;  P.f[kFLphi][s] = st.lphi;
-  if (tag == kTagBeck) {
-    P.f[kFU][s] = st.u_br;  P.f[kFU + 1][s] = st.u_s2;
-  } else {
-    P.f[kFU][s] = wm.x;     P.f[kFU + 1][s] = wm.y;     P.f[kFU + 2][s] = wm.z;
-    P.f[kFVm][s] = vm;
+  using F = PoolF<kMono>;
+  P.f[F::kDir][s] = st.dir.x; P.f[F::kDir + 1][s] = st.dir.y; P.f[F::kDir + 2][s] = st.dir.z;
+  P.f[F::kT][s] = st.T.x;
+  P.f[F::kL][s] = st.L.x;
+  if constexpr (!kMono) {
+    P.f[F::kT + 1][s] = st.T.y; P.f[F::kT + 2][s] = st.T.z;
+    P.f[F::kL + 1][s] = st.L.y; P.f[F::kL + 2][s] = st.L.z;
   }
-  P.f[kFPz][s] = st.pos.z;
+  P.f[F::kSigO][s] = sig_o; P.f[F::kSigB][s] = sig_b;
+  P.f[F::kUrr][s] = st.u_rr; P.f[F::kLphi][s] = st.lphi;
+  if (tag == kTagBeck) {
+    P.f[F::kU][s] = st.u_br;  P.f[F::kU + 1][s] = st.u_s2;
+  } else {
+    P.f[F::kU][s] = wm.x;     P.f[F::kU + 1][s] = wm.y;     P.f[F::kU + 2][s] = wm.z;
+    P.f[F::kVm][s] = vm;
+  }
+  P.f[F::kPz][s] = st.pos.z;
   if constexpr (kPoint) {
-    P.f[kFPxy][s] = st.pos.x; P.f[kFPxy + 1][s] = st.pos.y;
+    P.f[F::kPxy][s] = st.pos.x; P.f[F::kPxy + 1][s] = st.pos.y;
   }
   P.u[0][s] = st.pid;   P.u[1][s] = st.rng.pixel; P.u[2][s] = st.rng.sample;
   P.u[3][s] = (uint32_t)st.bounce;
 }
 
-template <bool kPoint>
-__device__ __forceinline__ void pool_load(const PoolSlots<kPoint>& P, int s, const PassDev& ps,
-                                          bool beck, PathState& st, float& sig_o, float& sig_b,
-                                          V3& wm, float& vm) {
-  st.dir = v3(P.f[kFDir][s], P.f[kFDir + 1][s], P.f[kFDir + 2][s]);
-  st.T = v3(P.f[kFT][s], P.f[kFT + 1][s], P.f[kFT + 2][s]);
-  st.L = v3(P.f[kFL][s], P.f[kFL + 1][s], P.f[kFL + 2][s]);
-  sig_o = P.f[kFSigO][s];
-  sig_b = P.f[kFSigB][s];
-  st.u_rr = P.f[kFUrr][s];
-  st.lphi = P.f[kFLphi][s];
-  if (beck) {
-    st.u_br = P.f[kFU][s];
-    st.u_s2 = P.f[kFU + 1][s];
+// kMono: the three channels of T and L are set to the one stored value; only
+// channel x is stored back and written out, so the y / z arithmetic is dead
+// code the compiler removes
+template <bool kPoint, bool kMono>
+__device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int s,
+                                          const PassDev& ps, bool beck, PathState& st,
+                                          float& sig_o, float& sig_b, V3& wm, float& vm) {
+  using F = PoolF<kMono>;
+  st.dir = v3(P.f[F::kDir][s], P.f[F::kDir + 1][s], P.f[F::kDir + 2][s]);
+  if constexpr (kMono) {
+    float t = P.f[F::kT][s], l = P.f[F::kL][s];
+    st.T = v3(t, t, t);
+    st.L = v3(l, l, l);
   } else {
-    wm = v3(P.f[kFU][s], P.f[kFU + 1][s], P.f[kFU + 2][s]);
-    vm = P.f[kFVm][s];
+    st.T = v3(P.f[F::kT][s], P.f[F::kT + 1][s], P.f[F::kT + 2][s]);
+    st.L = v3(P.f[F::kL][s], P.f[F::kL + 1][s], P.f[F::kL + 2][s]);
+  }
+  sig_o = P.f[F::kSigO][s];
+  sig_b = P.f[F::kSigB][s];
+  st.u_rr = P.f[F::kUrr][s];
+  st.lphi = P.f[F::kLphi][s];
+  if (beck) {
+    st.u_br = P.f[F::kU][s];
+    st.u_s2 = P.f[F::kU + 1][s];
+  } else {
+    wm = v3(P.f[F::kU][s], P.f[F::kU + 1][s], P.f[F::kU + 2][s]);
+    vm = P.f[F::kVm][s];
   }
   // x, y are never read without a point light (a single plane is
   // translation invariant)
-  if constexpr (kPoint) st.pos = v3(P.f[kFPxy][s], P.f[kFPxy + 1][s], P.f[kFPz][s]);
-  else st.pos = v3(0.0f, 0.0f, P.f[kFPz][s]);
+  if constexpr (kPoint) st.pos = v3(P.f[F::kPxy][s], P.f[F::kPxy + 1][s], P.f[F::kPz][s]);
+  else st.pos = v3(0.0f, 0.0f, P.f[F::kPz][s]);
   st.pid = P.u[0][s];
   st.rng.k0 = ps.k0;
   st.rng.k1 = ps.k1;
   st.rng.pixel = P.u[1][s];
   st.rng.sample = P.u[2][s];
   st.bounce = (int)P.u[3][s];
+}
+
+// a finished path of a grey scene: channel x written to all three slots
+__device__ __forceinline__ void finish_path_mono(const PassDev& ps, const PathState& st,
+                                                 Counters& cn) {
+  float r = st.L.x;
+  if (!isfinite(r) || r < 0.0f) cn.v[kStNonfinite]++;
+  ps.rad[st.pid] = r;
+  ps.rad[ps.n_paths + st.pid] = r;
+  ps.rad[2u * ps.n_paths + st.pid] = r;
 }
 
 // shadow transmittance towards the sun from a single-plane collision whose
@@ -692,18 +724,22 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
   }
 }
 
-template <bool kPoint>
+template <bool kPoint, bool kMono>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
                                                                   const __grid_constant__ PassDev ps) {
-  __shared__ PoolSlots<kPoint> pools[kWarpsPerBlock];
+  __shared__ PoolSlots<kPoint, kMono> pools[kWarpsPerBlock];
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  PoolSlots<kPoint>& P = pools[threadIdx.x >> 5];
+  PoolSlots<kPoint, kMono>& P = pools[threadIdx.x >> 5];
   const MediumK& m = sc.media[0];
   Counters cn;
 #pragma unroll
   for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
+  auto finish = [&](const PathState& q) {
+    if constexpr (kMono) finish_path_mono(ps, q, cn);
+    else finish_path(ps, q, cn);
+  };
 #pragma unroll
   for (int w = 0; w < kPoolWords; ++w) P.tag[w * 32 + lane] = kTagEmpty;
   __syncwarp();
@@ -761,7 +797,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
         fly = true;
       }
     } else if (slot >= 0) {
-      pool_load<kPoint>(P, slot, ps, stage == kStageBeck, st, sig_o, sig_b, wm, vm);
+      pool_load<kPoint, kMono>(P, slot, ps, stage == kStageBeck, st, sig_o, sig_b, wm, vm);
       V3 v = neg3(st.dir);   // the plane frame is the identity
       if (stage == kStageBeck) {
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
@@ -781,14 +817,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
         if (st.bounce >= ps.max_bounces) {             // render.py:92-94
           done = true;
         } else if (st.bounce > 8) {                    // render.py:96-105
-          float q = fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+          float q = kMono ? fminf(st.T.x, 1.0f) : fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
           if (st.u_rr >= q) {
             done = true;
           } else {
             st.T = mul3(st.T, 1.0f / q);
           }
         }
-        if (done) finish_path(ps, st, cn);
+        if (done) finish(st);
         else fly = true;
       }
     }
@@ -796,7 +832,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
     if (fly) {
       // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
       if (!flight_stage<0>(sc, st, cn)) {
-        finish_path(ps, st, cn);
+        finish(st);
       } else {
         V3 pos = st.cpos;
         V3 wo = st.dir;
@@ -804,7 +840,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
         cn.v[kStScatters]++;
         if (!(sig_o >= 1e-12f)) {
           cn.v[kStDegenerate]++;
-          finish_path(ps, st, cn);
+          finish(st);
         } else {
           planar_nee<kPoint>(sc, st, cn, wo, sig_o, pos);
           st.pos = pos;
@@ -823,7 +859,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       }
     }
     if (slot >= 0) {
-      if (tag != kTagEmpty) pool_store<kPoint>(P, slot, st, sig_o, sig_b, tag, wm, vm);
+      if (tag != kTagEmpty) pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b, tag, wm, vm);
       P.tag[slot] = tag;
     }
     __syncwarp();
@@ -1012,7 +1048,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int blocks[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 int device_occupancy(Occupancy* occ) {
@@ -1040,10 +1076,14 @@ int device_occupancy(Occupancy* occ) {
                                                         kBlock, 0));
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[5], path_kernel<2, true>,
                                                         kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[6], pool_kernel<false>, kBlock,
-                                                        0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[7], pool_kernel<true>, kBlock,
-                                                        0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[6], pool_kernel<false, false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[7], pool_kernel<true, false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[8], pool_kernel<false, true>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[9], pool_kernel<true, true>,
+                                                        kBlock, 0));
   for (int& b : o.blocks) b = std::max(b, 1);
   if (dev < 64) {
     cache[dev] = o;
@@ -1143,10 +1183,15 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
     // pool's bit-exactness test compares the two)
     else if (megakernel_requested()) path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
     else {
-      int pk = sc.has_point ? 7 : 6;
+      int pk = (sc.has_point ? 7 : 6) + (sc.mono ? 2 : 0);
       grid = (int)std::max<int64_t>(1, std::min<int64_t>(occ.sms * occ.blocks[pk], need));
-      if (sc.has_point) pool_kernel<true><<<grid, kBlock, 0, st>>>(sc, ps);
-      else pool_kernel<false><<<grid, kBlock, 0, st>>>(sc, ps);
+      if (sc.mono) {
+        if (sc.has_point) pool_kernel<true, true><<<grid, kBlock, 0, st>>>(sc, ps);
+        else pool_kernel<false, true><<<grid, kBlock, 0, st>>>(sc, ps);
+      } else {
+        if (sc.has_point) pool_kernel<true, false><<<grid, kBlock, 0, st>>>(sc, ps);
+        else pool_kernel<false, false><<<grid, kBlock, 0, st>>>(sc, ps);
+      }
     }
 #else
     else path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);

@@ -207,6 +207,18 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
         return (*err = std::string("point light inside a shell is not supported"), MF_ERR_UNSUPPORTED);
     }
   }
+  // grey scene: Fresnel one or a grey albedo, and grey lights / environment;
+  // then all three colour channels of a path carry the same value
+  auto grey = [](V3 v) { return v.x == v.y && v.y == v.z; };
+  sc.mono = 1;
+  for (int j = 0; j < sc.n_prims; ++j) {
+    const MediumK& m = sc.media[j];
+    bool g = m.fresnel == kOne ||
+             (m.fresnel == kAlbedo && m.albedo[0] == m.albedo[1] && m.albedo[1] == m.albedo[2]);
+    if (!g) sc.mono = 0;
+  }
+  if (!grey(sc.env) || (sc.has_sun && !grey(sc.sun_L)) || (sc.has_point && !grey(sc.point_I)))
+    sc.mono = 0;
   *out = sc;
   return MF_OK;
 }

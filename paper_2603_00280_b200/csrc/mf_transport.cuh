@@ -58,6 +58,7 @@ struct MediumExtra {
 struct SceneDev {
   int n_prims;
   int single_plane;    // 1: analytic planar transport
+  int mono;            // 1: every radiance / weight factor is grey (pool_kernel<*, true>)
   PrimDev prims[kMaxPrims];
   MediumK media[kMaxPrims];
   MediumExtra mx[kMaxPrims];
