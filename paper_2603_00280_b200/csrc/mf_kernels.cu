@@ -271,7 +271,7 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
 // in st.cpos / st.ck / st.csig for the scatter stage); on escape / absorption
 // the environment term is added and false is returned (path finished).
 // kMode: 0 single plane (analytic), 1 general shells (tracking), 2 grid field
-template <int kMode>
+template <int kMode, int kSpec = kSpecRuntime>
 __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, Counters& cn) {
   cn.v[kStSegments]++;
   U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
@@ -291,7 +291,7 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
     outcome = w.outcome;
   } else if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
-    float sig = proj_area(m, st.dir);
+    float sig = proj_area<kSpec>(m, st.dir);
     st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
     // positions matter only to a point light
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi,
@@ -685,12 +685,12 @@ __device__ __noinline__ float planar_sun_tr_cold(const SceneDev& sc, float h, fl
 // used as they are.  With the collision's log Phi known, the sun's closed-form
 // transmittance (planar_shadow_tr) reduces to clamping it to the band and one
 // exponential: the sun end is a band edge fixed per render.
-template <bool kPoint>
+template <bool kPoint, int kSpec>
 __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Counters& cn,
                                            V3 wo, float sig_o, V3 pos) {
   const MediumK& m = sc.media[0];
   if (sc.has_sun) {
-    V3 ph = phase_eval(m, wo, sc.sun_to, sig_o);
+    V3 ph = phase_eval<kSpec>(m, wo, sc.sun_to, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr;
@@ -713,7 +713,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
     float r2 = dot3(d, d);
     float ir = frsqrt(r2);
     V3 wlw = mul3(d, ir);
-    V3 ph = phase_eval(m, wo, wlw, sig_o);
+    V3 ph = phase_eval<kSpec>(m, wo, wlw, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr<0>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
@@ -724,7 +724,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
   }
 }
 
-template <bool kPoint, bool kMono>
+template <bool kPoint, bool kMono, int kSpec>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
                                                                   const __grid_constant__ PassDev ps) {
   __shared__ PoolSlots<kPoint, kMono> pools[kWarpsPerBlock];
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
         tag = kTagTail;
       } else {
         // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
-        PhaseSample smp = phase_sample_tail(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
+        PhaseSample smp = phase_sample_tail<kSpec>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
         st.dir = smp.wi;
         st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
         st.bounce++;
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
     __syncwarp();
     if (fly) {
       // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
-      if (!flight_stage<0>(sc, st, cn)) {
+      if (!flight_stage<0, kSpec>(sc, st, cn)) {
         finish(st);
       } else {
         V3 pos = st.cpos;
@@ -842,9 +842,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          planar_nee<kPoint>(sc, st, cn, wo, sig_o, pos);
+          planar_nee<kPoint, kSpec>(sc, st, cn, wo, sig_o, pos);
           st.pos = pos;
-          sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
+          sig_b = (kSpec == kSpecRuntime && m.kind == kBeckmann) ? sig_o
+                                                                 : proj_area_erf(wo, m.ax, m.ay, 0.0f);
           if (sig_b > 1e-12f && st.u_br < m.mix) {
             tag = kTagBeck;
           } else {
@@ -1048,8 +1049,19 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int blocks[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
+
+template <bool kPoint, bool kMono, int kSpec>
+cudaError_t occ_pool(int* blocks) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, pool_kernel<kPoint, kMono, kSpec>,
+                                                       kBlock, 0);
+}
+
+template <bool kPoint, bool kMono, int kSpec>
+void launch_pool(int grid, const SceneDev& sc, const PassDev& ps, cudaStream_t st) {
+  pool_kernel<kPoint, kMono, kSpec><<<grid, kBlock, 0, st>>>(sc, ps);
+}
 
 int device_occupancy(Occupancy* occ) {
   static std::mutex mu;
@@ -1076,14 +1088,15 @@ int device_occupancy(Occupancy* occ) {
                                                         kBlock, 0));
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[5], path_kernel<2, true>,
                                                         kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[6], pool_kernel<false, false>,
-                                                        kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[7], pool_kernel<true, false>,
-                                                        kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[8], pool_kernel<false, true>,
-                                                        kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[9], pool_kernel<true, true>,
-                                                        kBlock, 0));
+  // pool kernels: blocks[6 + point + 2 mono + 4 spec]
+  MF_CUDA((occ_pool<false, false, 0>(&o.blocks[6])));
+  MF_CUDA((occ_pool<true, false, 0>(&o.blocks[7])));
+  MF_CUDA((occ_pool<false, true, 0>(&o.blocks[8])));
+  MF_CUDA((occ_pool<true, true, 0>(&o.blocks[9])));
+  MF_CUDA((occ_pool<false, false, 1>(&o.blocks[10])));
+  MF_CUDA((occ_pool<true, false, 1>(&o.blocks[11])));
+  MF_CUDA((occ_pool<false, true, 1>(&o.blocks[12])));
+  MF_CUDA((occ_pool<true, true, 1>(&o.blocks[13])));
   for (int& b : o.blocks) b = std::max(b, 1);
   if (dev < 64) {
     cache[dev] = o;
@@ -1183,15 +1196,15 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
     // pool's bit-exactness test compares the two)
     else if (megakernel_requested()) path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
     else {
-      int pk = (sc.has_point ? 7 : 6) + (sc.mono ? 2 : 0);
+      bool spec = sc.media[0].kind == kGeneralized && sc.media[0].fresnel == kAlbedo;
+      int pk = 6 + (sc.has_point ? 1 : 0) + (sc.mono ? 2 : 0) + (spec ? 4 : 0);
       grid = (int)std::max<int64_t>(1, std::min<int64_t>(occ.sms * occ.blocks[pk], need));
-      if (sc.mono) {
-        if (sc.has_point) pool_kernel<true, true><<<grid, kBlock, 0, st>>>(sc, ps);
-        else pool_kernel<false, true><<<grid, kBlock, 0, st>>>(sc, ps);
-      } else {
-        if (sc.has_point) pool_kernel<true, false><<<grid, kBlock, 0, st>>>(sc, ps);
-        else pool_kernel<false, false><<<grid, kBlock, 0, st>>>(sc, ps);
-      }
+      using L = void (*)(int, const SceneDev&, const PassDev&, cudaStream_t);
+      static const L pools[8] = {launch_pool<false, false, 0>, launch_pool<true, false, 0>,
+                                 launch_pool<false, true, 0>,  launch_pool<true, true, 0>,
+                                 launch_pool<false, false, 1>, launch_pool<true, false, 1>,
+                                 launch_pool<false, true, 1>,  launch_pool<true, true, 1>};
+      pools[pk - 6](grid, sc, ps, st);
     }
 #else
     else path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
