@@ -271,7 +271,9 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
 // in st.cpos / st.ck / st.csig for the scatter stage); on escape / absorption
 // the environment term is added and false is returned (path finished).
 // kMode: 0 single plane (analytic), 1 general shells (tracking), 2 grid field
-template <int kMode, int kSpec = kSpecRuntime>
+// kNeedPos (single plane): 1 / 0 when the caller knows at compile time
+// whether a point light reads positions, -1 to ask the scene
+template <int kMode, int kSpec = kSpecRuntime, int kNeedPos = -1>
 __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, Counters& cn) {
   cn.v[kStSegments]++;
   U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
@@ -295,7 +297,7 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
     st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
     // positions matter only to a point light
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi,
-                              sc.has_point != 0);
+                              kNeedPos < 0 ? sc.has_point != 0 : kNeedPos == 1);
     st.cpos = fl.pos;
     st.lphi = fl.lphi;
     outcome = fl.outcome;
@@ -403,7 +405,7 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
   unsigned smask = __ballot_sync(amask, !done);
   if (!done) {
     float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
-    float uu = remap_branch_uniform(u_br, m.mix);
+    float uu = remap_branch_uniform_render(u_br, m);
     PhaseSample smp = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2, smask);
     cn.v[kStSlopeIters] += (uint32_t)smp.iters;
     st.dir = to_world(fr, smp.wi);
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
       V3 v = neg3(st.dir);   // the plane frame is the identity
       if (stage == kStageBeck) {
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
-        float uu = remap_branch_uniform(st.u_br, m.mix);
+        float uu = remap_branch_uniform_render(st.u_br, m);
         int iters = 0;
         wm = beckmann_visible_normal(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
@@ -831,7 +833,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
     __syncwarp();
     if (fly) {
       // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
-      if (!flight_stage<0, kSpec>(sc, st, cn)) {
+      if (!flight_stage<0, kSpec, kPoint ? 1 : 0>(sc, st, cn)) {
         finish(st);
       } else {
         V3 pos = st.cpos;
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_c
           } else {
             // hemisphere branch: the normal now (cheap), the tail in stage T
             V3 v = neg3(wo);
-            float uu = remap_branch_uniform(st.u_br, m.mix);
+            float uu = remap_branch_uniform_render(st.u_br, m);
             wm = hemisphere_about(v, uu, st.u_s2);
             vm = uu;   // z of wm in v's frame, exactly (ndf.py:375-380)
             tag = kTagTail;

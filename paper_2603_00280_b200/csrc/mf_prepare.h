@@ -60,6 +60,8 @@ inline int prepare_medium(const mf_medium& in, MediumK* out, std::string* err) {
   m.sigma = (float)in.sigma;
   m.inv_sigma = (float)(1.0 / in.sigma);
   m.mix = (float)in.mix_ratio;
+  m.inv_mix = in.mix_ratio > 0.0 ? (float)(1.0 / in.mix_ratio) : 0.0f;
+  m.inv_1m_mix = in.mix_ratio < 1.0 ? (float)(1.0 / (1.0 - in.mix_ratio)) : 0.0f;
   m.inv_ax = (float)(1.0 / in.ax);
   m.inv_ay = (float)(1.0 / in.ay);
   const double pi = 3.14159265358979323846;

@@ -55,6 +55,12 @@ MF_HD float remap_branch_uniform(float u1, float mix) {
   return u1 < mix ? div_rn(u1, mix) : div_rn(u1 - mix, 1.0f - mix);
 }
 
+// the same remap on the render path, by the reciprocals prepared on the host
+// (identical to remap_branch_uniform when R is a power of two, e.g. R = 1/2)
+MF_HD float remap_branch_uniform_render(float u1, const MediumK& m) {
+  return u1 < m.mix ? u1 * m.inv_mix : (u1 - m.mix) * m.inv_1m_mix;
+}
+
 struct QueryResult {
   float sigma_t;
   V3 phase;

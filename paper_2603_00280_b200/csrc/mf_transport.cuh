@@ -150,6 +150,29 @@ struct Flight {
   float lphi;   // log Phi(f / sigma) at pos after a collision, NaN otherwise
 };
 
+// log Phi of a start height inside the band (rare on the render path: paths
+// enter from above and carry log Phi after each collision); out of line
+MF_COLD float log_ndtr_cold(float u) { return log_ndtr(u); }
+
+// grazing flight (|cos theta| < 1e-6): f stays put, so this branch needs the
+// true height (from l0 when the height was not tracked); out of line
+MF_COLD Flight planar_flight_grazing(const PrimDev& pr, const MediumK& m, V3 pos, V3 dir,
+                                    float sig, float tau, float l0, float h, bool from_l0) {
+  Flight fl;
+  fl.lphi = NAN;
+  fl.pos = pos;
+  float hg = from_l0 ? m.sigma * inv_log_ndtr(l0) : h;
+  float st = mills(hg * m.inv_sigma) * m.inv_sigma * sig;
+  if (!(st > 0.0f)) {
+    fl.outcome = kEscaped;
+    return fl;
+  }
+  fl.outcome = kCollided;
+  pos.z = pr.z0 + hg;
+  fl.pos = fma3(dir, tau / st, pos);
+  return fl;
+}
+
 // One collision-mode flight from pos along dir through the shell of a
 // single plane, given u in (0,1).  sig = sigma(dir) in the plane frame.
 // The flight is sampled in log-Phi space: lphi = log Phi(f / sigma) at pos
@@ -185,23 +208,12 @@ MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtr
         fl.outcome = kAbsorbed;
         return fl;
       }
-      l0 = log_ndtr(h * m.inv_sigma);
+      l0 = log_ndtr_cold(h * m.inv_sigma);
     }
   }
   float tau = -flog(u);
-  if (fabsf(c) < 1e-6f) {
-    // grazing: f stays put; this rare branch needs the true height
-    float hg = (known && !need_pos) ? m.sigma * inv_log_ndtr(l0) : h;
-    float st = mills(hg * m.inv_sigma) * m.inv_sigma * sig;
-    if (!(st > 0.0f)) {
-      fl.outcome = kEscaped;
-      return fl;
-    }
-    fl.outcome = kCollided;
-    pos.z = pr.z0 + hg;
-    fl.pos = fma3(dir, tau / st, pos);
-    return fl;
-  }
+  if (fabsf(c) < 1e-6f) return planar_flight_grazing(pr, m, pos, dir, sig, tau, l0, h,
+                                                    known && !need_pos);
   float dl = tau * fabsf(c) / sig;          // change of log Phi along the flight
   float l1;
   if (c > 0.0f) {
