@@ -55,6 +55,11 @@ constexpr int kBlock = 128;
 #define MF_MIN_BLOCKS 6
 #endif
 constexpr int kMinBlocks = MF_MIN_BLOCKS;
+// the same for the path pool (its smem pools allow up to 7 blocks per SM)
+#ifndef MF_POOL_MIN_BLOCKS
+#define MF_POOL_MIN_BLOCKS 6
+#endif
+constexpr int kPoolMinBlocks = MF_POOL_MIN_BLOCKS;
 
 enum StatIdx {
   kStPaths = 0,
@@ -727,7 +732,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
 }
 
 template <bool kPoint, bool kMono, int kSpec>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
+__global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __grid_constant__ SceneDev sc,
                                                                   const __grid_constant__ PassDev ps) {
   __shared__ PoolSlots<kPoint, kMono> pools[kWarpsPerBlock];
   const unsigned full = 0xffffffffu;
