@@ -264,6 +264,29 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
   }
 }
 
+// shadow transmittance towards the sun from a single-plane collision whose
+// log Phi is unknown (after a grazing flight): the general closed form, out
+// of line (one copy in the instruction stream, rarely executed)
+__device__ __noinline__ float planar_sun_tr_cold(const SceneDev& sc, float h, float lphi) {
+  return planar_shadow_tr(sc.media[0], sc.mx[0], h, sc.sun_to.z > 0.0f ? INFINITY : -INFINITY,
+                          sc.sun_to.z, sc.sun_sig, lphi);
+}
+
+// sun transmittance from a single-plane collision (both render kernels):
+// with the collision's log Phi known, the closed form (planar_shadow_tr)
+// reduces to clamping it to the band and one MUFU exp2 -- the sun end is a
+// band edge fixed per render (sun_lb, sun_k2 prepared on the host)
+__device__ __forceinline__ float planar_sun_tr(const SceneDev& sc, float lphi, V3 pos) {
+  if (!(lphi == lphi)) return planar_sun_tr_cold(sc, pos.z - sc.prims[0].z0, lphi);
+  const MediumExtra& mx = sc.mx[0];
+  float la = fminf(fmaxf(lphi, mx.lphi_lo_rat), mx.lphi_hi);
+  if (la == sc.sun_lb) return 1.0f;
+  if (sc.sun_graze) return 0.0f;
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sc.sun_k2 * fabsf(sc.sun_lb - la)));
+  return r;
+}
+
 template <int kMode>
 __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev& ps,
                                                PathState& st, Counters& cn, unsigned amask,
@@ -384,8 +407,10 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
     V3 ph = phase_eval(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
-                           sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
+      float tr = kMode == 0 ? planar_sun_tr(sc, st.lphi, pos)
+                            : shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
+                                               sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn,
+                                               sc.sun_sig);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
     }
@@ -677,14 +702,6 @@ __device__ __forceinline__ void finish_path_mono(const PassDev& ps, const PathSt
   ps.rad[2u * ps.n_paths + st.pid] = r;
 }
 
-// shadow transmittance towards the sun from a single-plane collision whose
-// log Phi is unknown (after a grazing flight): the general closed form, out
-// of line (one copy in the instruction stream, rarely executed)
-__device__ __noinline__ float planar_sun_tr_cold(const SceneDev& sc, float h, float lphi) {
-  return planar_shadow_tr(sc.media[0], sc.mx[0], h, sc.sun_to.z > 0.0f ? INFINITY : -INFINITY,
-                          sc.sun_to.z, sc.sun_sig, lphi);
-}
-
 // next-event estimation at a collision of the single plane (the stage-2
 // block of scatter_stages<0>, same arithmetic); kPoint: the scene has a point
 // light (its code is compiled out otherwise).  The plane frame is the
@@ -700,17 +717,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
     V3 ph = phase_eval<kSpec>(m, wo, sc.sun_to, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr;
-      if (st.lphi == st.lphi) {
-        const MediumExtra& mx = sc.mx[0];
-        float c = sc.sun_to.z;
-        float la = fminf(fmaxf(st.lphi, mx.lphi_lo_rat), mx.lphi_hi);
-        float lb = c > 0.0f ? mx.lphi_hi : mx.lphi_lo_rat;
-        tr = la == lb ? 1.0f
-                      : (fabsf(c) < 1e-6f ? 0.0f : expf(-sc.sun_sig / fabsf(c) * fabsf(lb - la)));
-      } else {
-        tr = planar_sun_tr_cold(sc, pos.z - sc.prims[0].z0, st.lphi);
-      }
+      float tr = planar_sun_tr(sc, st.lphi, pos);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
     }

@@ -190,6 +190,12 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     sc.sun_to = v3((float)(-d[0] / dn), (float)(-d[1] / dn), (float)(-d[2] / dn));
     sc.sun_L = v3((float)in.sun_radiance[0], (float)in.sun_radiance[1], (float)in.sun_radiance[2]);
     if (sc.n_prims > 0) sc.sun_sig = proj_area(sc.media[0], sc.sun_to);
+    if (sc.n_prims > 0) {
+      double c = std::fabs((double)sc.sun_to.z);
+      sc.sun_graze = c < 1e-6 ? 1 : 0;
+      sc.sun_k2 = sc.sun_graze ? 0.0f : (float)(-(double)sc.sun_sig / c * 1.4426950408889634);
+      sc.sun_lb = sc.sun_to.z > 0.0f ? sc.mx[0].lphi_hi : sc.mx[0].lphi_lo_rat;
+    }
   }
   sc.has_point = in.has_point;
   if (in.has_point) {

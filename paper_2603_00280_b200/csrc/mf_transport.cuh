@@ -71,6 +71,10 @@ struct SceneDev {
   V3 sun_to;           // unit direction towards the sun (= -DirectionalLight.direction)
   V3 sun_L;
   float sun_sig;       // sigma(sun_to) in the plane frame (single-plane scenes)
+  // single plane, closed-form sun transmittance from a collision's log Phi l:
+  // Tr = 2^{sun_k2 |sun_lb - clamp(l)|}, sun_k2 = -sigma(sun) / |cos| log2(e)
+  float sun_k2, sun_lb;
+  int sun_graze;       // |cos| < 1e-6: Tr = 0 unless the band is not crossed
   int has_point;
   V3 point_pos;
   V3 point_I;
