@@ -247,7 +247,7 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
                                            float sig_known = -1.0f) {
   if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
-    float sig = sig_known >= 0.0f ? sig_known : proj_area(m, wl);
+    float sig = sig_known >= 0.0f ? sig_known : proj_area<kSpecRuntime, true>(m, wl);
     return planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0, h_end, wl.z, sig, st.lphi);
   } else if constexpr (kMode == 2) {
     GridWalk w = grid_walk_path(sc.grid, sc.media[0], st.rng, (uint32_t)st.bounce, kCallShadow,
@@ -321,7 +321,7 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, 
     outcome = w.outcome;
   } else if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
-    float sig = proj_area<kSpec>(m, st.dir);
+    float sig = proj_area<kSpec, true>(m, st.dir);
     st.csig = sig;   // sigma(dir) is sigma(wo) in the (identity) plane frame
     // positions matter only to a point light
     Flight fl = planar_flight(sc.prims[0], m, sc.mx[0], st.pos, st.dir, sig, u_fl, st.lphi,
@@ -392,7 +392,7 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
                                                float sig_known, bool done, float u_br,
                                                float u_s2, float u_rr) {
   V3 wo = to_local(fr, st.dir);
-  float sig_o = sig_known >= 0.0f ? sig_known : proj_area(m, wo);
+  float sig_o = sig_known >= 0.0f ? sig_known : proj_area<kSpecRuntime, true>(m, wo);
   if (!done) {
     cn.v[kStScatters]++;
     if (!(sig_o >= 1e-12f)) {
@@ -404,7 +404,7 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
   //      BASELINE extension)
   if (!done && sc.has_sun) {
     V3 wl = to_local(fr, sc.sun_to);
-    V3 ph = phase_eval(m, wo, wl, sig_o);
+    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = kMode == 0 ? planar_sun_tr(sc, st.lphi, pos)
@@ -421,7 +421,7 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
     float ir = frsqrt(r2);
     V3 wlw = mul3(d, ir);
     V3 wl = to_local(fr, wlw);
-    V3 ph = phase_eval(m, wo, wl, sig_o);
+    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr<kMode>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
@@ -434,9 +434,9 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
   // ---- stage 3: phase sampling (render.py:84-90), two-uniform convention
   unsigned smask = __ballot_sync(amask, !done);
   if (!done) {
-    float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf(wo, m.ax, m.ay, 0.0f);
+    float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
     float uu = remap_branch_uniform_render(u_br, m);
-    PhaseSample smp = phase_sample(m, wo, sig_o, sig_b, u_br, uu, u_s2, smask);
+    PhaseSample smp = phase_sample<false, true>(m, wo, sig_o, sig_b, u_br, uu, u_s2, smask);
     cn.v[kStSlopeIters] += (uint32_t)smp.iters;
     st.dir = to_world(fr, smp.wi);
     st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
@@ -714,7 +714,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
                                            V3 wo, float sig_o, V3 pos) {
   const MediumK& m = sc.media[0];
   if (sc.has_sun) {
-    V3 ph = phase_eval<kSpec>(m, wo, sc.sun_to, sig_o);
+    V3 ph = phase_eval<kSpec, true>(m, wo, sc.sun_to, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = planar_sun_tr(sc, st.lphi, pos);
@@ -727,7 +727,7 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
     float r2 = dot3(d, d);
     float ir = frsqrt(r2);
     V3 wlw = mul3(d, ir);
-    V3 ph = phase_eval<kSpec>(m, wo, wlw, sig_o);
+    V3 ph = phase_eval<kSpec, true>(m, wo, wlw, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
       float tr = shadow_tr<0>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
@@ -817,13 +817,13 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
         float uu = remap_branch_uniform_render(st.u_br, m);
         int iters = 0;
-        wm = beckmann_visible_normal(m, v, uu, st.u_s2, &iters);
+        wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
         cn.v[kStSlopeIters] += (uint32_t)iters;
         tag = kTagTail;
       } else {
         // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
-        PhaseSample smp = phase_sample_tail<kSpec>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
+        PhaseSample smp = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
         st.dir = smp.wi;
         st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
         st.bounce++;
@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
           planar_nee<kPoint, kSpec>(sc, st, cn, wo, sig_o, pos);
           st.pos = pos;
           sig_b = (kSpec == kSpecRuntime && m.kind == kBeckmann) ? sig_o
-                                                                 : proj_area_erf(wo, m.ax, m.ay, 0.0f);
+                                                                 : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
           if (sig_b > 1e-12f && st.u_br < m.mix) {
             tag = kTagBeck;
           } else {
