@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ Quer
 
 struct PassDev {
   uint32_t k0, k1;
+  // Philox round keys (k0 + r W0, k1 + r W1), so the unrolled rounds of the
+  // render kernels' own draws read them as constant-bank operands
+  uint32_t rk[20];
   int max_bounces;
   uint32_t n_paths;      // paths in this pass
   uint32_t S;            // samples per local pixel in this pass
@@ -302,9 +305,10 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
 // kNeedPos (single plane): 1 / 0 when the caller knows at compile time
 // whether a point light reads positions, -1 to ask the scene
 template <int kMode, int kSpec = kSpecRuntime, int kNeedPos = -1>
-__device__ __forceinline__ bool flight_stage(const SceneDev& sc, PathState& st, Counters& cn) {
+__device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& ps, PathState& st,
+                                             Counters& cn) {
   cn.v[kStSegments]++;
-  U4 b = rng_block(st.rng, (uint32_t)st.bounce, 0u);
+  U4 b = philox_rk(U4{st.rng.pixel, st.rng.sample, (uint32_t)st.bounce, 0u}, ps.rk);
   float u_fl = u01(b.x);
   st.u_br = u01(b.y);
   st.u_s2 = u01(b.z);
@@ -489,7 +493,7 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   }
   st.rng.pixel = (uint32_t)pixel;
   st.rng.sample = ps.sample_begin + s;
-  U4 jb = rng_block(st.rng, kSegCamera, 0u);
+  U4 jb = philox_rk(U4{st.rng.pixel, st.rng.sample, kSegCamera, 0u}, ps.rk);
   camera_ray(sc, (uint32_t)pixel, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
   return true;
 }
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
     }
     bool coll = false;
     if (active) {
-      coll = flight_stage<kMode>(sc, st, cn);
+      coll = flight_stage<kMode>(sc, ps, st, cn);
       if (!coll) {
         finish_path(ps, st, cn);
         active = false;
@@ -845,7 +849,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
     __syncwarp();
     if (fly) {
       // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
-      if (!flight_stage<0, kSpec, kPoint ? 1 : 0>(sc, st, cn)) {
+      if (!flight_stage<0, kSpec, kPoint ? 1 : 0>(sc, ps, st, cn)) {
         finish(st);
       } else {
         V3 pos = st.cpos;
@@ -1442,6 +1446,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   std::memset(&ps, 0, sizeof(ps));
   ps.k0 = (uint32_t)(p.seed & 0xffffffffu);
   ps.k1 = (uint32_t)(p.seed >> 32);
+  philox_round_keys(ps.k0, ps.k1, ps.rk);
   ps.max_bounces = p.max_bounces;
   ps.shard = p.shard;
   ps.rank = p.rank;
@@ -1551,6 +1556,7 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
   std::memset(&ps, 0, sizeof(ps));
   ps.k0 = (uint32_t)(seed & 0xffffffffu);
   ps.k1 = (uint32_t)(seed >> 32);
+  philox_round_keys(ps.k0, ps.k1, ps.rk);
   ps.max_bounces = max_bounces;
   ps.n_paths = (uint32_t)n;
   ps.S = 1;
