@@ -259,7 +259,7 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
     cn.v[kStViolations] += (uint32_t)w.violations;
     return w.weight;
   } else {
-    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max,
+    WalkResult w = walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max,
                         kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
@@ -334,7 +334,8 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& 
     st.lphi = fl.lphi;
     outcome = fl.outcome;
   } else {
-    WalkResult w = walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false, INFINITY);
+    WalkResult w = walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false,
+                                    INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
     st.cpos = w.pos;
@@ -380,7 +381,7 @@ __device__ __forceinline__ bool scatter_stage(const SceneDev& sc, const PassDev&
     return scatter_stages<kMode>(sc, ps, st, cn, amask, mg, frame_about(nrm), pos, -1.0f, false,
                                  st.u_br, st.u_s2, st.u_rr);
   } else {
-    V3 nrm = kMode == 0 ? v3(0.0f, 0.0f, 1.0f) : prim_normal(sc.prims[st.ck], pos);
+    V3 nrm = kMode == 0 ? v3(0.0f, 0.0f, 1.0f) : prim_normal<kMode == 3>(sc.prims[st.ck], pos);
     return scatter_stages<kMode>(sc, ps, st, cn, amask, sc.media[st.ck], frame_about(nrm), pos,
                                  kMode == 0 ? st.csig : -1.0f, false, st.u_br, st.u_s2,
                                  st.u_rr);
@@ -1067,7 +1068,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int blocks[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1105,6 +1106,11 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[4], path_kernel<1, true>,
                                                         kBlock, 0));
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[5], path_kernel<2, true>,
+                                                        kBlock, 0));
+  // single-sphere megakernel (mode 3): blocks[14] / [15] (caller rays)
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[14], path_kernel<3, false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[15], path_kernel<3, true>,
                                                         kBlock, 0));
   // pool kernels: blocks[6 + point + 2 mono + 4 spec]
   MF_CUDA((occ_pool<false, false, 0>(&o.blocks[6])));
@@ -1203,8 +1209,13 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   Occupancy occ;
   int rc = device_occupancy(&occ);
   if (rc) return rc;
-  int mode = sc.has_grid ? 2 : (sc.single_plane ? 0 : 1);
-  int grid = occ.sms * occ.blocks[mode + (caller_rays ? 3 : 0)];
+  // modes: 0 single plane, 1 general shells, 2 grid field, 3 one sphere
+  // (MF_GENERIC_WALK=1: the general walker for it, for the equality test)
+  const char* gw = std::getenv("MF_GENERIC_WALK");
+  bool generic = gw && gw[0] == '1';
+  int mode = sc.has_grid ? 2 : (sc.single_plane ? 0 : (sc.n_prims == 1 && !generic ? 3 : 1));
+  int grid = occ.sms * (mode == 3 ? occ.blocks[caller_rays ? 15 : 14]
+                                  : occ.blocks[mode + (caller_rays ? 3 : 0)]);
   int64_t need = ((int64_t)ps.n_paths + kBlock - 1) / kBlock;
   grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
   if (mode == 0) {
@@ -1230,6 +1241,9 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   } else if (mode == 1) {
     if (caller_rays) path_kernel<1, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else path_kernel<1, false><<<grid, kBlock, 0, st>>>(sc, ps);
+  } else if (mode == 3) {
+    if (caller_rays) path_kernel<3, true><<<grid, kBlock, 0, st>>>(sc, ps);
+    else path_kernel<3, false><<<grid, kBlock, 0, st>>>(sc, ps);
   } else {
     if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);

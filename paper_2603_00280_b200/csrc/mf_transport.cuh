@@ -104,14 +104,17 @@ constexpr uint32_t kCallShadow = 0x80000000u;
 // ---------------------------------------------------------------------------
 // fields
 
+// kSphere: the primitive is known to be a sphere (single-sphere walker)
+template <bool kSphere = false>
 MF_HD float prim_field(const PrimDev& p, V3 x) {
-  if (p.shape == 0) return x.z - p.z0;
+  if (!kSphere && p.shape == 0) return x.z - p.z0;
   V3 d = sub3(x, p.c);
   return fsqrt(dot3(d, d)) - p.radius;
 }
 
+template <bool kSphere = false>
 MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
-  if (p.shape == 0) return v3(0.0f, 0.0f, 1.0f);
+  if (!kSphere && p.shape == 0) return v3(0.0f, 0.0f, 1.0f);
   V3 d = sub3(x, p.c);
   float r2 = dot3(d, d);
   return r2 > 0.0f ? mul3(d, frsqrt(r2)) : v3(0.0f, 0.0f, 1.0f);
@@ -123,8 +126,9 @@ MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
 // surface itself; inside: second root), not by a threshold on the first
 // root -- in float32 a ray sitting on the level set must not be sent to the
 // far side.
+template <bool kSphere = false>
 MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
-  if (p.shape == 0) {
+  if (!kSphere && p.shape == 0) {
     float t = (level - (pos.z - p.z0)) / dir.z;
     return (t >= 0.0f && t < INFINITY) ? t : INFINITY;
   }
@@ -304,12 +308,13 @@ struct WalkResult {
 };
 
 // Extinction of prim j at x along dir (local frame), 0 outside its region.
+template <bool kSphere = false>
 MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mult) {
   const PrimDev& p = sc.prims[j];
   const MediumK& m = sc.media[j];
-  float f = prim_field(p, x);
+  float f = prim_field<kSphere>(p, x);
   if (f < lo_mult * m.sigma || f > 3.0f * m.sigma) return 0.0f;
-  Frame fr = frame_about(prim_normal(p, x));
+  Frame fr = frame_about(prim_normal<kSphere>(p, x));
   float sg = proj_area_outlined(m.kind, m.ax, m.ay, m.az, to_local(fr, dir));
   return mills(f * m.inv_sigma) * m.inv_sigma * sg;
 }
@@ -370,7 +375,12 @@ MF_HD void walk_begin(WalkState& w, V3 pos, V3 dir, bool ratio, float t_max, uin
 
 // One iteration of the delta / ratio tracking loop (transport.py:196-297);
 // returns true when the walk has ended (w.outcome, w.pos, w.prim, w.weight).
+// kOne: the scene is one sphere (BASELINE config 3) -- the primitive loops
+// run once with their arrays in registers and the plane branches fold away;
+// the arithmetic is the general walker's, so the results are identical.
+template <bool kOne = false>
 MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, WalkState& w) {
+  const int n_prims = kOne ? 1 : sc.n_prims;
   // fields, band membership, gaps (transport.py:197-212)
   bool any_band = false;
   float gap_min = INFINITY;
@@ -378,10 +388,10 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
   float maj = 0.0f;
   float cap = INFINITY;
   float fs[kMaxPrims];
-  for (int j = 0; j < sc.n_prims; ++j) {
+  for (int j = 0; j < n_prims; ++j) {
     const PrimDev& p = sc.prims[j];
     const MediumK& m = sc.media[j];
-    float f = prim_field(p, w.p);
+    float f = prim_field<kOne>(p, w.p);
     fs[j] = f;
     float lo = w.lo_mult * m.sigma, hi = 3.0f * m.sigma;
     if (!w.ratio && f < lo) {
@@ -393,7 +403,7 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
       any_band = true;
       cap = fminf(cap, MF_STEP_FRAC * m.sigma);
     } else {
-      float g = level_distance(p, w.p, w.dir, f > hi ? hi : lo);
+      float g = level_distance<kOne>(p, w.p, w.dir, f > hi ? hi : lo);
       gap_min = fminf(gap_min, g);
       if (g < INFINITY) all_done = false;
       cap = fminf(cap, fmaxf(g, sc.min_skip));
@@ -403,14 +413,14 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
   // geometry): min of f along the step (planes: linear; spheres: closest
   // approach) and, for media whose sigma(w) decreases with cos(theta), the
   // direction factor at the step start (cos(theta) grows along a chord)
-  for (int j = 0; j < sc.n_prims; ++j) {
+  for (int j = 0; j < n_prims; ++j) {
     const PrimDev& p = sc.prims[j];
     const MediumK& m = sc.media[j];
     float f = fs[j];
     float lo = w.lo_mult * m.sigma, hi = 3.0f * m.sigma;
     if (!(f >= lo && f <= hi)) continue;
     float fmin, dirf;
-    if (p.shape == 0) {
+    if (!kOne && p.shape == 0) {
       fmin = f + cap * fminf(w.dir.z, 0.0f);
       dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az, w.dir);
     } else {
@@ -473,8 +483,8 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
   }
   float parts[kMaxPrims];
   float st = 0.0f;
-  for (int j = 0; j < sc.n_prims; ++j) {
-    parts[j] = prim_extinction(sc, j, w.p, w.dir, w.lo_mult);
+  for (int j = 0; j < n_prims; ++j) {
+    parts[j] = prim_extinction<kOne>(sc, j, w.p, w.dir, w.lo_mult);
     st += parts[j];
   }
   if (st > maj * 1.00001f) w.violations++;
@@ -507,8 +517,8 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
     if (pick < st) {
       // u2 * majorant doubles as the primitive selector (transport.py:276-279)
       float acc = 0.0f;
-      int k = sc.n_prims - 1;
-      for (int j = 0; j < sc.n_prims; ++j) {
+      int k = n_prims - 1;
+      for (int j = 0; j < n_prims; ++j) {
         acc += parts[j];
         if (pick < acc) {
           k = j;
@@ -524,14 +534,15 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
   return false;   // null collision: the walk goes on
 }
 
-MF_WALK_FN WalkResult walk(const SceneDev& sc, const PathRng& rng, uint32_t segment,
+template <bool kOne = false>
+MF_WALK_FN WalkResult walk(const SceneDev& sc, PathRng rng, uint32_t segment,
                            uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
                            float rr_min = 0.0f) {
   WalkState s;
   walk_begin(s, pos, dir, ratio, t_max, call0, rr_min);
   WalkResult w;
   for (int iter = 0; iter < 1000000; ++iter) {
-    if (walk_step(sc, rng, segment, s)) {
+    if (walk_step<kOne>(sc, rng, segment, s)) {
       w.outcome = s.outcome;
       w.prim = s.prim;
       w.pos = s.pos;
