@@ -275,6 +275,28 @@ __device__ __noinline__ float planar_sun_tr_cold(const SceneDev& sc, float h, fl
                           sc.sun_to.z, sc.sun_sig, lphi);
 }
 
+// point-light NEE at a single-plane collision: the radiance increment
+// T phase I Tr / r^2 (the plane frame is the identity).  Out of line: point
+// lights are not on the benchmark path, and one copy gives the pool and the
+// megakernel the same instructions (their images must match bit for bit).
+__device__ __noinline__ V3 planar_point_nee(const SceneDev& sc, const PathState& st, V3 wo,
+                                            float sig_o, V3 pos, int* nee) {
+  const MediumK& m = sc.media[0];
+  V3 d = sub3(sc.point_pos, pos);
+  float r2 = dot3(d, d);
+  float ir = frsqrt(r2);
+  V3 wl = mul3(d, ir);
+  V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+  if (!(ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f)) return v3(0.0f, 0.0f, 0.0f);
+  *nee = 1;
+  float sig = proj_area<kSpecRuntime, true>(m, wl);
+  float tr = planar_shadow_tr(m, sc.mx[0], pos.z - sc.prims[0].z0,
+                              sc.point_pos.z - sc.prims[0].z0, wl.z, sig, st.lphi);
+  float s = tr * frcp(r2);
+  return v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
+            st.T.z * ph.z * sc.point_I.z * s);
+}
+
 // sun transmittance from a single-plane collision (both render kernels):
 // with the collision's log Phi known, the closed form (planar_shadow_tr)
 // reduces to clamping it to the band and one MUFU exp2 -- the sun end is a
@@ -420,7 +442,11 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
                            st.T.z * ph.z * sc.sun_L.z * tr));
     }
   }
-  if (!done && sc.has_point) {
+  if (kMode == 0 && !done && sc.has_point) {
+    int nee = 0;
+    st.L = add3(st.L, planar_point_nee(sc, st, wo, sig_o, pos, &nee));
+    cn.v[kStNee] += (uint32_t)nee;
+  } else if (!done && sc.has_point) {
     V3 d = sub3(sc.point_pos, pos);
     float r2 = dot3(d, d);
     float ir = frsqrt(r2);
@@ -603,6 +629,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 constexpr int kPool = MF_POOL;
 static_assert(kPool % 32 == 0 && kPool <= 128, "pool size: whole warps of slots");
 constexpr int kPoolWords = kPool / 32;
+constexpr int kRing = 128;   // power of two >= kPool
 constexpr int kWarpsPerBlock = kBlock / 32;
 
 enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageTail = 2 };
@@ -625,8 +652,10 @@ template <bool kPoint, bool kMono>
 struct PoolSlots {
   float f[PoolF<kMono>::kPxy + (kPoint ? 2 : 0)][kPool];
   uint32_t u[4][kPool];   // pid pixel sample bounce
-  uint8_t tag[kPool];
-  uint8_t list[32];       // this iteration's slot of each lane
+  // one ring of slot indices per tag (empty / waiting for B / waiting for
+  // T): a stage pops up to 32 slots of its ring, and every processed slot is
+  // pushed onto the ring of its new tag
+  uint8_t ring[3][kRing];
 };
 
 template <bool kPoint, bool kMono>
@@ -728,18 +757,9 @@ __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Co
     }
   }
   if (kPoint && sc.has_point) {
-    V3 d = sub3(sc.point_pos, pos);
-    float r2 = dot3(d, d);
-    float ir = frsqrt(r2);
-    V3 wlw = mul3(d, ir);
-    V3 ph = phase_eval<kSpec, true>(m, wo, wlw, sig_o);
-    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
-      cn.v[kStNee]++;
-      float tr = shadow_tr<0>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
-      float s = tr * frcp(r2);
-      st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
-                           st.T.z * ph.z * sc.point_I.z * s));
-    }
+    int nee = 0;
+    st.L = add3(st.L, planar_point_nee(sc, st, wo, sig_o, pos, &nee));
+    cn.v[kStNee] += (uint32_t)nee;
   }
 }
 
@@ -760,23 +780,13 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
     else finish_path(ps, q, cn);
   };
 #pragma unroll
-  for (int w = 0; w < kPoolWords; ++w) P.tag[w * 32 + lane] = kTagEmpty;
+  for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
   __syncwarp();
+  // ring heads / tails (warp-uniform): every slot starts empty
+  unsigned he = 0, hb = 0, ht = 0, te = kPool, tb = 0, tt = 0;
   bool exhausted = false;    // warp-uniform
   while (true) {
-    // per-stage slot masks from the tags (lane l reads slots l, l+32, ...)
-    unsigned qb[kPoolWords], qt[kPoolWords], qe[kPoolWords];
-    int nb = 0, nt = 0, ne = 0;
-#pragma unroll
-    for (int w = 0; w < kPoolWords; ++w) {
-      uint8_t t = P.tag[w * 32 + lane];
-      qb[w] = __ballot_sync(full, t == kTagBeck);
-      qt[w] = __ballot_sync(full, t == kTagTail);
-      qe[w] = exhausted ? 0u : __ballot_sync(full, t == kTagEmpty);
-      nb += __popc(qb[w]);
-      nt += __popc(qt[w]);
-      ne += __popc(qe[w]);
-    }
+    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nt = (int)(tt - ht);
     int stage;
     if (nb >= 32) stage = kStageBeck;
     else if (nt >= 32) stage = kStageTail;
@@ -785,18 +795,14 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
     else if (nb > 0) stage = kStageBeck;
     else if (ne > 0) stage = kStageRaygen;
     else break;
-    // compaction: the i-th candidate slot goes to lane i (through smem)
-    int n = 0;
-#pragma unroll
-    for (int w = 0; w < kPoolWords; ++w) {
-      unsigned c = stage == kStageBeck ? qb[w] : (stage == kStageTail ? qt[w] : qe[w]);
-      int r = n + __popc(c & lt);
-      if (((c >> lane) & 1u) && r < 32) P.list[r] = (uint8_t)(w * 32 + lane);
-      n += __popc(c);
-    }
-    __syncwarp();
-    int slot = lane < n ? (int)P.list[lane] : -1;
-    __syncwarp();
+    // pop up to 32 slots of the stage's ring, the i-th to lane i
+    int cnt = stage == kStageBeck ? nb : (stage == kStageTail ? nt : ne);
+    unsigned head = stage == kStageBeck ? hb : (stage == kStageTail ? ht : he);
+    int n = cnt < 32 ? cnt : 32;
+    int slot = lane < n ? (int)P.ring[stage][(head + (unsigned)lane) & (kRing - 1)] : -1;
+    if (stage == kStageBeck) hb += (unsigned)n;
+    else if (stage == kStageTail) ht += (unsigned)n;
+    else he += (unsigned)n;
 
     uint8_t tag = kTagEmpty;
     PathState st;
@@ -878,9 +884,21 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         }
       }
     }
-    if (slot >= 0) {
-      if (tag != kTagEmpty) pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b, tag, wm, vm);
-      P.tag[slot] = tag;
+    if (slot >= 0 && tag != kTagEmpty)
+      pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b, tag, wm, vm);
+    // push every processed slot onto the ring of its new tag
+    {
+      unsigned me = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
+      unsigned mb = __ballot_sync(full, slot >= 0 && tag == kTagBeck);
+      unsigned mt = __ballot_sync(full, slot >= 0 && tag == kTagTail);
+      if (slot >= 0) {
+        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : mt);
+        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : tt);
+        P.ring[tag][(tail + (unsigned)__popc(mine & lt)) & (kRing - 1)] = (uint8_t)slot;
+      }
+      te += (unsigned)__popc(me);
+      tb += (unsigned)__popc(mb);
+      tt += (unsigned)__popc(mt);
     }
     __syncwarp();
   }

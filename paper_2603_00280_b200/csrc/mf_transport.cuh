@@ -162,6 +162,18 @@ struct Flight {
 // enter from above and carry log Phi after each collision); out of line
 MF_COLD float log_ndtr_cold(float u) { return log_ndtr(u); }
 
+// position of a collision at log Phi l1 (only read by a point light); out of
+// line -- one copy, so every kernel computes it with the same instructions
+MF_COLD V3 planar_collision_pos(const PrimDev& pr, const MediumK& m, V3 pos, V3 dir, float h,
+                                float c, float l1) {
+  float h1 = m.sigma * inv_log_ndtr(l1);
+  // keep the root on the travelled side of h despite rounding
+  h1 = c > 0.0f ? fmaxf(h1, h) : fminf(h1, h);
+  V3 p = fma3(dir, (h1 - h) / c, pos);
+  p.z = pr.z0 + h1;
+  return p;
+}
+
 // grazing flight (|cos theta| < 1e-6): f stays put, so this branch needs the
 // true height (from l0 when the height was not tracked); out of line
 MF_COLD Flight planar_flight_grazing(const PrimDev& pr, const MediumK& m, V3 pos, V3 dir,
@@ -239,13 +251,7 @@ MF_HD Flight planar_flight(const PrimDev& pr, const MediumK& m, const MediumExtr
   }
   fl.outcome = kCollided;
   fl.lphi = l1;
-  if (need_pos) {
-    float h1 = m.sigma * inv_log_ndtr(l1);
-    // keep the root on the travelled side of h despite rounding
-    h1 = c > 0.0f ? fmaxf(h1, h) : fminf(h1, h);
-    fl.pos = fma3(dir, (h1 - h) / c, pos);
-    fl.pos.z = pr.z0 + h1;
-  }
+  if (need_pos) fl.pos = planar_collision_pos(pr, m, pos, dir, h, c, l1);
   return fl;
 }
 
