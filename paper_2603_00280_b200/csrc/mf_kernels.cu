@@ -632,8 +632,8 @@ constexpr int kPoolWords = kPool / 32;
 constexpr int kRing = 128;   // power of two >= kPool
 constexpr int kWarpsPerBlock = kBlock / 32;
 
-enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageTail = 2 };
-constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagTail = 2;
+enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageTail = 2, kStageHemi = 3 };
+constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagTail = 2, kTagHemi = 3;
 
 // float fields of a slot: dir3 T3 L3 sig_o sig_b u_rr lphi, then a union of
 // (u_br, u_s2) while waiting for B and (wm3, vm) while waiting for T, then
@@ -655,7 +655,7 @@ struct PoolSlots {
   // one ring of slot indices per tag (empty / waiting for B / waiting for
   // T): a stage pops up to 32 slots of its ring, and every processed slot is
   // pushed onto the ring of its new tag
-  uint8_t ring[3][kRing];
+  uint8_t ring[4][kRing];
 };
 
 template <bool kPoint, bool kMono>
@@ -672,7 +672,7 @@ __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, c
   }
   P.f[F::kSigO][s] = sig_o; P.f[F::kSigB][s] = sig_b;
   P.f[F::kUrr][s] = st.u_rr; P.f[F::kLphi][s] = st.lphi;
-  if (tag == kTagBeck) {
+  if (tag == kTagBeck || tag == kTagHemi) {
     P.f[F::kU][s] = st.u_br;  P.f[F::kU + 1][s] = st.u_s2;
   } else {
     P.f[F::kU][s] = wm.x;     P.f[F::kU + 1][s] = wm.y;     P.f[F::kU + 2][s] = wm.z;
@@ -783,25 +783,30 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
   for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
   __syncwarp();
   // ring heads / tails (warp-uniform): every slot starts empty
-  unsigned he = 0, hb = 0, ht = 0, te = kPool, tb = 0, tt = 0;
+  unsigned he = 0, hb = 0, ht = 0, hh = 0, te = kPool, tb = 0, tt = 0, th = 0;
   bool exhausted = false;    // warp-uniform
   while (true) {
-    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nt = (int)(tt - ht);
+    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nt = (int)(tt - ht),
+        nh = (int)(th - hh);
+    // a full warp of one stage if any; else the largest partial one
     int stage;
     if (nb >= 32) stage = kStageBeck;
+    else if (nh >= 32) stage = kStageHemi;
     else if (nt >= 32) stage = kStageTail;
     else if (ne >= 32) stage = kStageRaygen;
-    else if (nt > 0 && nt >= nb) stage = kStageTail;
-    else if (nb > 0) stage = kStageBeck;
+    else if (nt > 0 && nt >= nb && nt >= nh) stage = kStageTail;
+    else if (nb > 0 && nb >= nh) stage = kStageBeck;
+    else if (nh > 0) stage = kStageHemi;
     else if (ne > 0) stage = kStageRaygen;
     else break;
     // pop up to 32 slots of the stage's ring, the i-th to lane i
-    int cnt = stage == kStageBeck ? nb : (stage == kStageTail ? nt : ne);
-    unsigned head = stage == kStageBeck ? hb : (stage == kStageTail ? ht : he);
+    int cnt = stage == kStageBeck ? nb : (stage == kStageTail ? nt : (stage == kStageHemi ? nh : ne));
+    unsigned head = stage == kStageBeck ? hb : (stage == kStageTail ? ht : (stage == kStageHemi ? hh : he));
     int n = cnt < 32 ? cnt : 32;
     int slot = lane < n ? (int)P.ring[stage][(head + (unsigned)lane) & (kRing - 1)] : -1;
     if (stage == kStageBeck) hb += (unsigned)n;
     else if (stage == kStageTail) ht += (unsigned)n;
+    else if (stage == kStageHemi) hh += (unsigned)n;
     else he += (unsigned)n;
 
     uint8_t tag = kTagEmpty;
@@ -822,8 +827,11 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         fly = true;
       }
     } else if (slot >= 0) {
-      pool_load<kPoint, kMono>(P, slot, ps, stage == kStageBeck, st, sig_o, sig_b, wm, vm);
+      pool_load<kPoint, kMono>(P, slot, ps, stage != kStageTail, st, sig_o, sig_b, wm, vm);
       V3 v = neg3(st.dir);   // the plane frame is the identity
+      // next-event estimation of the collision, at full warp width: the
+      // first visit after the flight (B or H) runs it
+      if (stage != kStageTail) planar_nee<kPoint, kSpec>(sc, st, cn, st.dir, sig_o, st.pos);
       if (stage == kStageBeck) {
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
         float uu = remap_branch_uniform_render(st.u_br, m);
@@ -833,6 +841,12 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         cn.v[kStSlopeIters] += (uint32_t)iters;
         tag = kTagTail;
       } else {
+        if (stage == kStageHemi) {
+          // hemisphere branch of the mixture (ndf.py:375-380)
+          float uu = remap_branch_uniform_render(st.u_br, m);
+          wm = hemisphere_about(v, uu, st.u_s2);
+          vm = uu;   // z of wm in v's frame, exactly
+        }
         // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
         PhaseSample smp = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
         st.dir = smp.wi;
@@ -855,32 +869,22 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
     }
     __syncwarp();
     if (fly) {
-      // flight + NEE + mixture branch (scatter_stages<0> up to the branch)
+      // flight and the mixture branch (scatter_stages<0> up to the branch;
+      // the NEE runs in the next visit)
       if (!flight_stage<0, kSpec, kPoint ? 1 : 0>(sc, ps, st, cn)) {
         finish(st);
       } else {
-        V3 pos = st.cpos;
         V3 wo = st.dir;
         sig_o = st.csig;
+        st.pos = st.cpos;
         cn.v[kStScatters]++;
         if (!(sig_o >= 1e-12f)) {
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          planar_nee<kPoint, kSpec>(sc, st, cn, wo, sig_o, pos);
-          st.pos = pos;
           sig_b = (kSpec == kSpecRuntime && m.kind == kBeckmann) ? sig_o
                                                                  : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
-          if (sig_b > 1e-12f && st.u_br < m.mix) {
-            tag = kTagBeck;
-          } else {
-            // hemisphere branch: the normal now (cheap), the tail in stage T
-            V3 v = neg3(wo);
-            float uu = remap_branch_uniform_render(st.u_br, m);
-            wm = hemisphere_about(v, uu, st.u_s2);
-            vm = uu;   // z of wm in v's frame, exactly (ndf.py:375-380)
-            tag = kTagTail;
-          }
+          tag = (sig_b > 1e-12f && st.u_br < m.mix) ? kTagBeck : kTagHemi;
         }
       }
     }
@@ -891,14 +895,16 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
       unsigned me = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
       unsigned mb = __ballot_sync(full, slot >= 0 && tag == kTagBeck);
       unsigned mt = __ballot_sync(full, slot >= 0 && tag == kTagTail);
+      unsigned mh = __ballot_sync(full, slot >= 0 && tag == kTagHemi);
       if (slot >= 0) {
-        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : mt);
-        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : tt);
+        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : (tag == kTagTail ? mt : mh));
+        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : (tag == kTagTail ? tt : th));
         P.ring[tag][(tail + (unsigned)__popc(mine & lt)) & (kRing - 1)] = (uint8_t)slot;
       }
       te += (unsigned)__popc(me);
       tb += (unsigned)__popc(mb);
       tt += (unsigned)__popc(mt);
+      th += (unsigned)__popc(mh);
     }
     __syncwarp();
   }
