@@ -125,46 +125,143 @@ struct QueryArgs {
   int64_t n;
 };
 
-__global__ void __launch_bounds__(256) query_kernel(const __grid_constant__ QueryArgs a) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // every lane of a warp runs the same number of trips (so the sampler's
-  // re-convergence mask is well defined); lanes past n are predicated off
-  int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t w0 = first; w0 < a.n; w0 += stride) {
-    int64_t i = w0 + (threadIdx.x & 31);
-    unsigned qmask = __ballot_sync(0xffffffffu, i < a.n);
-    if (i >= a.n) continue;
-    V3 p = v3(__ldg(a.in.px + i), __ldg(a.in.py + i), __ldg(a.in.pz + i));
-    V3 wo = v3(__ldg(a.in.wox + i), __ldg(a.in.woy + i), __ldg(a.in.woz + i));
-    V3 wi = v3(__ldg(a.in.wix + i), __ldg(a.in.wiy + i), __ldg(a.in.wiz + i));
-    FieldPoint fp = field_at(a.shape, a.z0, a.c, a.radius, p);
-    if (a.in.f) fp.f = __ldg(a.in.f + i);
+// Config-1 queries, binned by mixture branch, per warp.  Phase A (one query
+// per lane): inputs, local frame, sigma_t, phase value, pdf, and the whole
+// sample of queries taking the cheap hemisphere branch (or degenerate);
+// queries taking the Beckmann branch (half of them) are queued in the warp's
+// shared-memory ring.  Phase B, whenever 32 are queued (and once more at the
+// end): the visible-slope solver -- most of a query's work -- on a full warp
+// instead of on the ~half of each warp's lanes whose branch chose it.  No
+// block barriers: each warp owns its ring.  Every query runs query_local's
+// arithmetic (medium.py:91-207, ndf.py:383-427).
+constexpr int kQBlock = 256;
+constexpr int kQRing = 64;           // power of two >= 2 x 32
+struct QueryRing {
+  uint32_t idx_lo[kQRing], idx_hi[kQRing];   // query index
+  float wo[3][kQRing];                       // local wo
+  float fr[9][kQRing];                       // local frame (t, b, n)
+  float uu[kQRing], u2[kQRing], sig_o[kQRing], sig_b[kQRing];
+};
+
+__device__ __forceinline__ void query_write_sample(const mf_query_out& o, int64_t i, V3 ws,
+                                                   float pdf_s, V3 w) {
+  if (o.wsx) o.wsx[i] = ws.x;
+  if (o.wsy) o.wsy[i] = ws.y;
+  if (o.wsz) o.wsz[i] = ws.z;
+  if (o.pdf_s) o.pdf_s[i] = pdf_s;
+  if (o.w_r) o.w_r[i] = w.x;
+  if (o.w_g) o.w_g[i] = w.y;
+  if (o.w_b) o.w_b[i] = w.z;
+}
+
+// Beckmann branch and tail of ring entry k
+__device__ __forceinline__ void query_beckmann(const QueryArgs& a, const QueryRing& R, int k) {
+  const MediumK& m = a.m;
+  int64_t j = (int64_t)(((uint64_t)R.idx_hi[k] << 32) | R.idx_lo[k]);
+  V3 wol = v3(R.wo[0][k], R.wo[1][k], R.wo[2][k]);
+  Frame fr;
+  fr.t = v3(R.fr[0][k], R.fr[1][k], R.fr[2][k]);
+  fr.b = v3(R.fr[3][k], R.fr[4][k], R.fr[5][k]);
+  fr.n = v3(R.fr[6][k], R.fr[7][k], R.fr[8][k]);
+  V3 v = neg3(wol);
+  int iters = 0;
+  V3 wm = beckmann_visible_normal<true>(m, v, R.uu[k], R.u2[k], &iters);
+  PhaseSample smp = phase_sample_tail(m, v, wm, dot3(v, wm), R.sig_o[k], R.sig_b[k], true);
+  query_write_sample(a.out, j, to_world(fr, smp.wi), smp.pdf, smp.weight);
+}
+
+__global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ QueryArgs a) {
+  __shared__ QueryRing rings[kQBlock / 32];
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  QueryRing& R = rings[threadIdx.x >> 5];
+  const MediumK& m = a.m;
+  const mf_query_out& o = a.out;
+  unsigned head = 0, tail = 0;   // warp-uniform ring positions
+  int64_t warp_id = ((int64_t)blockIdx.x * kQBlock + threadIdx.x) >> 5;
+  int64_t n_warps = ((int64_t)gridDim.x * kQBlock) >> 5;
+  for (int64_t c0 = warp_id * 32; c0 < a.n; c0 += n_warps * 32) {
+    int64_t i = c0 + lane;
+    bool queue = false;
+    V3 wol = v3(0.0f, 0.0f, 0.0f);
     Frame fr;
-    if (a.in.frame) {
-      const float* F = a.in.frame;
-      fr.t = v3(__ldg(F + i), __ldg(F + a.n + i), __ldg(F + 2 * a.n + i));
-      fr.b = v3(__ldg(F + 3 * a.n + i), __ldg(F + 4 * a.n + i), __ldg(F + 5 * a.n + i));
-      fr.n = v3(__ldg(F + 6 * a.n + i), __ldg(F + 7 * a.n + i), __ldg(F + 8 * a.n + i));
-    } else {
-      fr = frame_about(fp.n);
+    float uu = 0.0f, u2 = 0.0f, sig_safe = 1.0f, sig_b = 0.0f;
+    if (i < a.n) {
+      V3 p = v3(__ldg(a.in.px + i), __ldg(a.in.py + i), __ldg(a.in.pz + i));
+      V3 wo = v3(__ldg(a.in.wox + i), __ldg(a.in.woy + i), __ldg(a.in.woz + i));
+      V3 wi = v3(__ldg(a.in.wix + i), __ldg(a.in.wiy + i), __ldg(a.in.wiz + i));
+      float u1 = __ldg(a.in.u1 + i);
+      u2 = __ldg(a.in.u2 + i);
+      FieldPoint fp = field_at(a.shape, a.z0, a.c, a.radius, p);
+      if (a.in.f) fp.f = __ldg(a.in.f + i);
+      if (a.in.frame) {
+        const float* F = a.in.frame;
+        fr.t = v3(__ldg(F + i), __ldg(F + a.n + i), __ldg(F + 2 * a.n + i));
+        fr.b = v3(__ldg(F + 3 * a.n + i), __ldg(F + 4 * a.n + i), __ldg(F + 5 * a.n + i));
+        fr.n = v3(__ldg(F + 6 * a.n + i), __ldg(F + 7 * a.n + i), __ldg(F + 8 * a.n + i));
+      } else {
+        fr = frame_about(fp.n);
+      }
+      // query_local up to the sampler (mf_query.cuh)
+      u1 = fminf(fmaxf(u1, 5.9604644775390625e-08f), 0.99999994f);
+      u2 = fminf(fmaxf(u2, 5.9604644775390625e-08f), 0.99999994f);
+      wol = to_local(fr, wo);
+      V3 wil = to_local(fr, wi);
+      float sig_o = proj_area(m, wol);
+      float sigma_t = mills(fp.f * m.inv_sigma) * m.inv_sigma * sig_o;
+      sig_b = proj_area_erf(wol, m.ax, m.ay, 0.0f);
+      bool degenerate = !(sig_o >= 1e-12f);
+      sig_safe = degenerate ? 1.0f : sig_o;
+      V3 phase = phase_eval(m, wol, wil, sig_safe);
+      float pdf = phase_pdf(m, wol, wil, sig_b);
+      uu = remap_branch_uniform(u1, m.mix);
+      bool guided = sig_b > 1e-12f;
+      if (degenerate) {
+        phase = v3(0.0f, 0.0f, 0.0f);
+        pdf = 0.0f;
+      }
+      if (o.sigma_t) o.sigma_t[i] = sigma_t;
+      if (o.phase_r) o.phase_r[i] = phase.x;
+      if (o.phase_g) o.phase_g[i] = phase.y;
+      if (o.phase_b) o.phase_b[i] = phase.z;
+      if (o.pdf) o.pdf[i] = pdf;
+      if (o.flags) o.flags[i] = degenerate ? 1 : 0;
+      if (degenerate) {
+        query_write_sample(o, i, wo, 0.0f, v3(0.0f, 0.0f, 0.0f));
+      } else if (guided && u1 < m.mix) {
+        queue = true;
+      } else {
+        // hemisphere branch of the mixture (ndf.py:375-380) and the tail
+        V3 v = neg3(wol);
+        V3 wm = hemisphere_about(v, uu, u2);
+        PhaseSample smp = phase_sample_tail(m, v, wm, uu, sig_safe, sig_b, guided);
+        query_write_sample(o, i, to_world(fr, smp.wi), smp.pdf, smp.weight);
+      }
     }
-    QueryResult q = query_local(a.m, fp.f, fr, wo, wi, __ldg(a.in.u1 + i), __ldg(a.in.u2 + i),
-                                qmask);
-    const mf_query_out& o = a.out;
-    if (o.sigma_t) o.sigma_t[i] = q.sigma_t;
-    if (o.phase_r) o.phase_r[i] = q.phase.x;
-    if (o.phase_g) o.phase_g[i] = q.phase.y;
-    if (o.phase_b) o.phase_b[i] = q.phase.z;
-    if (o.pdf) o.pdf[i] = q.pdf;
-    if (o.wsx) o.wsx[i] = q.ws.x;
-    if (o.wsy) o.wsy[i] = q.ws.y;
-    if (o.wsz) o.wsz[i] = q.ws.z;
-    if (o.pdf_s) o.pdf_s[i] = q.pdf_s;
-    if (o.w_r) o.w_r[i] = q.w.x;
-    if (o.w_g) o.w_g[i] = q.w.y;
-    if (o.w_b) o.w_b[i] = q.w.z;
-    if (o.flags) o.flags[i] = q.flags;
+    // enqueue the Beckmann-branch queries of this chunk
+    unsigned qm = __ballot_sync(full, queue);
+    if (queue) {
+      int k = (int)((tail + (unsigned)__popc(qm & lt)) & (kQRing - 1));
+      R.idx_lo[k] = (uint32_t)i;
+      R.idx_hi[k] = (uint32_t)((uint64_t)i >> 32);
+      R.wo[0][k] = wol.x; R.wo[1][k] = wol.y; R.wo[2][k] = wol.z;
+      R.fr[0][k] = fr.t.x; R.fr[1][k] = fr.t.y; R.fr[2][k] = fr.t.z;
+      R.fr[3][k] = fr.b.x; R.fr[4][k] = fr.b.y; R.fr[5][k] = fr.b.z;
+      R.fr[6][k] = fr.n.x; R.fr[7][k] = fr.n.y; R.fr[8][k] = fr.n.z;
+      R.uu[k] = uu; R.u2[k] = u2; R.sig_o[k] = sig_safe; R.sig_b[k] = sig_b;
+    }
+    tail += (unsigned)__popc(qm);
+    __syncwarp();
+    if (tail - head >= 32) {
+      query_beckmann(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
+      head += 32;
+      __syncwarp();
+    }
   }
+  // drain
+  int left = (int)(tail - head);
+  if (lane < left) query_beckmann(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1398,9 +1495,13 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
   int dev = 0, sms = 148;
   MF_CUDA(cudaGetDevice(&dev));
   MF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int64_t blocks = (n + 255) / 256;
-  int grid = (int)std::min<int64_t>(blocks, (int64_t)sms * 8);
-  query_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  // two resident waves: every warp loops over many 32-query chunks, so its
+  // Beckmann ring fills to full warps
+  int per_sm = 1;
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_kernel, kQBlock, 0));
+  int64_t blocks = (n + kQBlock - 1) / kQBlock;
+  int grid = (int)std::min<int64_t>(blocks, (int64_t)sms * std::max(per_sm, 1) * 2);
+  query_kernel<<<grid, kQBlock, 0, (cudaStream_t)stream>>>(a);
   g_launches++;
   MF_CUDA(cudaGetLastError());
   return MF_OK;
