@@ -81,6 +81,27 @@ PLANAR_EVENTS = {
 }
 
 
+# One config-1 coefficient query (query_kernel): the scatter event's phase
+# sample (sigma_b, branch remap, 50/50 Beckmann / hemisphere proposal,
+# mixture pdf, vNDF weight, frame and rotations) + phase_eval of wi + the
+# density of sigma_t (mills and 3 multiplies) + the pdf of wi (half vector,
+# mixture pdf) + the two rotations of wo, wi into the local frame.
+QUERY = (EVENTS["scatters"][0] + PRIMS["phase_eval"][0] + PRIMS["mills"][0] + 3
+         + 9 + PRIMS["mixture_pdf"][0] + 3 + 2 * PRIMS["rotate"][0],
+         EVENTS["scatters"][1] + PRIMS["phase_eval"][1] + PRIMS["mills"][1]
+         + 1 + PRIMS["mixture_pdf"][1])
+
+
+def query_roofline(n_queries, kernel_ms, peak_fp32_ginst, peak_sfu_ginst):
+    """Roofline fraction of the query kernel from the per-query count QUERY."""
+    t = kernel_ms * 1e-3
+    af = n_queries * QUERY[0] / t / 1e9
+    asf = n_queries * QUERY[1] / t / 1e9
+    ff, fs = af / peak_fp32_ginst, asf / peak_sfu_ginst
+    return {"bound": "fp32" if ff >= fs else "sfu", "frac": max(ff, fs), "fp32_frac": ff,
+            "sfu_frac": fs, "fp32_per_query": QUERY[0], "sfu_per_query": QUERY[1]}
+
+
 def algorithmic_ops(stats, planar=False):
     """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters;
     planar=True: the sun-lit single-plane event costs (PLANAR_EVENTS)."""

@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2603_00280_b200 as mf  # noqa: E402
-from paper_2603_00280_b200 import configs  # noqa: E402
+from paper_2603_00280_b200 import _lib, configs, roofline  # noqa: E402
 
 
 def timed(fn, reps=3, warm=1):
@@ -43,6 +43,12 @@ def render_case(name, scene, spp, seed, depth, reps=3):
 
 torch.cuda.set_device(0)
 res = []
+# FP32 / MUFU issue peaks measured on this device (as bench.py)
+_lib_h = _lib.load()
+_f, _s = _lib.ctypes.c_double(), _lib.ctypes.c_double()
+_lib.check(_lib_h.mf_measure_peaks(_lib.ctypes.byref(_f), _lib.ctypes.byref(_s),
+                                   _lib.stream_handle(torch, torch.device("cuda", 0))))
+PEAK = (_f.value, _s.value)
 ONLY = sys.argv[1:]
 
 
@@ -62,7 +68,8 @@ for reps in ((1, 16) if want("config1") else ()):
     n = (1 << 20) * reps
     res.append({"case": f"config1 queries N=2^{20 + (4 if reps == 16 else 0)}", "ms": ms,
                 "Mqueries_s": n / ms / 1e3, "bytes_per_query": 96,
-                "GB_s": n * 96 / ms / 1e6})
+                "GB_s": n * 96 / ms / 1e6,
+                "roofline": roofline.query_roofline(n, ms, PEAK[0], PEAK[1])})
 if want("config2"):
     res.append(render_case("config2 256^2 x 64 spp d16", configs.config2_scene(), 64, 1, 16, 10))
 if want("config3"):
