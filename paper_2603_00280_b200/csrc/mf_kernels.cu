@@ -278,6 +278,7 @@ struct PassDev {
   uint32_t sample_begin; // global sample index of the pass's first sample
   uint32_t n_local;      // local pixels of this rank (render mode)
   int shard, rank, nranks, tile, tiles_x;
+  int mono;              // the pass buffer holds channel 0 only (grey pool kernel)
   float* rad;            // SoA [3][n_paths]
   unsigned int* counter;
   unsigned long long* stats;
@@ -823,14 +824,12 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int
   st.bounce = (int)P.u[3][s];
 }
 
-// a finished path of a grey scene: channel x written to all three slots
+// a finished path of a grey scene: channel x only (ps.mono)
 __device__ __forceinline__ void finish_path_mono(const PassDev& ps, const PathState& st,
                                                  Counters& cn) {
   float r = st.L.x;
   if (!isfinite(r) || r < 0.0f) cn.v[kStNonfinite]++;
-  ps.rad[st.pid] = r;
-  ps.rad[ps.n_paths + st.pid] = r;
-  ps.rad[2u * ps.n_paths + st.pid] = r;
+  ps.rad[st.pid] = r;   // one channel; accumulate_kernel (ps.mono) reads only it
 }
 
 // next-event estimation at a collision of the single plane (the stage-2
@@ -1032,11 +1031,18 @@ __global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__
   float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
   if (lp < n_local) {
     const float* r = ps.rad + lp;
-    for (uint32_t s = s_lo; s < s_hi; ++s) {
-      size_t o = (size_t)s * n_local;
-      s0 += __ldg(r + o);
-      s1 += __ldg(r + ps.n_paths + o);
-      s2 += __ldg(r + 2u * ps.n_paths + o);
+    if (ps.mono) {
+      // grey pool kernel: channel 0 only, the same sum for all three
+      for (uint32_t s = s_lo; s < s_hi; ++s) s0 += __ldg(r + (size_t)s * n_local);
+      s1 = s0;
+      s2 = s0;
+    } else {
+      for (uint32_t s = s_lo; s < s_hi; ++s) {
+        size_t o = (size_t)s * n_local;
+        s0 += __ldg(r + o);
+        s1 += __ldg(r + ps.n_paths + o);
+        s2 += __ldg(r + 2u * ps.n_paths + o);
+      }
     }
   }
   part[0][w][lane] = s0;
@@ -1619,6 +1625,10 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   ps.rad = scr.rad;
   ps.counter = scr.counter;
   ps.stats = scr.stats;
+#ifndef MF_NO_POOL
+  // the grey pool kernel writes one channel per path (finish_path_mono)
+  ps.mono = (sc.single_plane && !sc.has_grid && sc.mono && !megakernel_requested()) ? 1 : 0;
+#endif
   float inv_spp = (float)(1.0 / p.spp);
   // path-kernel timing: one event pair per pass, read after the final sync
   // (no host round trip between the path and accumulate kernels)
