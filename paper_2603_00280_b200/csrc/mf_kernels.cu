@@ -978,7 +978,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          sig_b = (kSpec == kSpecRuntime && m.kind == kBeckmann) ? sig_o
+          sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann)) ? sig_o
                                                                  : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
           tag = (sig_b > 1e-12f && st.u_br < m.mix) ? kTagBeck : kTagHemi;
         }
@@ -1195,7 +1195,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int blocks[20] = {};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1239,7 +1239,7 @@ int device_occupancy(Occupancy* occ) {
                                                         kBlock, 0));
   MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[15], path_kernel<3, true>,
                                                         kBlock, 0));
-  // pool kernels: blocks[6 + point + 2 mono + 4 spec]
+  // pool kernels: blocks[6 + point + 2 mono + 4 spec]; spec 2 at [16..19]
   MF_CUDA((occ_pool<false, false, 0>(&o.blocks[6])));
   MF_CUDA((occ_pool<true, false, 0>(&o.blocks[7])));
   MF_CUDA((occ_pool<false, true, 0>(&o.blocks[8])));
@@ -1248,6 +1248,10 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_pool<true, false, 1>(&o.blocks[11])));
   MF_CUDA((occ_pool<false, true, 1>(&o.blocks[12])));
   MF_CUDA((occ_pool<true, true, 1>(&o.blocks[13])));
+  MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
+  MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
+  MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));
+  MF_CUDA((occ_pool<true, true, 2>(&o.blocks[19])));
   for (int& b : o.blocks) b = std::max(b, 1);
   if (dev < 64) {
     cache[dev] = o;
@@ -1352,15 +1356,19 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
     // pool's bit-exactness test compares the two)
     else if (megakernel_requested()) path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
     else {
-      bool spec = sc.media[0].kind == kGeneralized && sc.media[0].fresnel == kAlbedo;
-      int pk = 6 + (sc.has_point ? 1 : 0) + (sc.mono ? 2 : 0) + (spec ? 4 : 0);
+      int spec = sc.media[0].fresnel != kAlbedo ? 0
+                 : (sc.media[0].kind == kGeneralized ? 1 : (sc.media[0].kind == kBeckmann ? 2 : 0));
+      int v = (sc.has_point ? 1 : 0) + (sc.mono ? 2 : 0);
+      int pk = spec == 2 ? 16 + v : 6 + v + (spec ? 4 : 0);
       grid = (int)std::max<int64_t>(1, std::min<int64_t>(occ.sms * occ.blocks[pk], need));
       using L = void (*)(int, const SceneDev&, const PassDev&, cudaStream_t);
-      static const L pools[8] = {launch_pool<false, false, 0>, launch_pool<true, false, 0>,
-                                 launch_pool<false, true, 0>,  launch_pool<true, true, 0>,
-                                 launch_pool<false, false, 1>, launch_pool<true, false, 1>,
-                                 launch_pool<false, true, 1>,  launch_pool<true, true, 1>};
-      pools[pk - 6](grid, sc, ps, st);
+      static const L pools[12] = {launch_pool<false, false, 0>, launch_pool<true, false, 0>,
+                                  launch_pool<false, true, 0>,  launch_pool<true, true, 0>,
+                                  launch_pool<false, false, 1>, launch_pool<true, false, 1>,
+                                  launch_pool<false, true, 1>,  launch_pool<true, true, 1>,
+                                  launch_pool<false, false, 2>, launch_pool<true, false, 2>,
+                                  launch_pool<false, true, 2>,  launch_pool<true, true, 2>};
+      pools[spec * 4 + v](grid, sc, ps, st);
     }
 #else
     else path_kernel<0, false><<<grid, kBlock, 0, st>>>(sc, ps);
