@@ -839,13 +839,14 @@ __device__ __forceinline__ void finish_path_mono(const PassDev& ps, const PathSt
 // used as they are.  With the collision's log Phi known, the sun's closed-form
 // transmittance (planar_shadow_tr) reduces to clamping it to the band and one
 // exponential: the sun end is a band edge fixed per render.
-template <bool kPoint, int kSpec>
+template <bool kPoint, int kSpec, bool kMono = false>
 __device__ __forceinline__ void planar_nee(const SceneDev& sc, PathState& st, Counters& cn,
                                            V3 wo, float sig_o, V3 pos) {
   const MediumK& m = sc.media[0];
   if (sc.has_sun) {
     V3 ph = phase_eval<kSpec, true>(m, wo, sc.sun_to, sig_o);
-    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+    // grey: the three channels are equal, x decides
+    if (kMono ? ph.x > 0.0f : (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f)) {
       cn.v[kStNee]++;
       float tr = planar_sun_tr(sc, st.lphi, pos);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
@@ -927,7 +928,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
       V3 v = neg3(st.dir);   // the plane frame is the identity
       // next-event estimation of the collision, at full warp width: the
       // first visit after the flight (B or H) runs it
-      if (stage != kStageTail) planar_nee<kPoint, kSpec>(sc, st, cn, st.dir, sig_o, st.pos);
+      if (stage != kStageTail) planar_nee<kPoint, kSpec, kMono>(sc, st, cn, st.dir, sig_o, st.pos);
       if (stage == kStageBeck) {
         // Beckmann branch of the mixture (phase_sample, two-uniform convention)
         float uu = remap_branch_uniform_render(st.u_br, m);
