@@ -299,9 +299,10 @@ MF_GRID_WALK_FN GridWalk grid_walk_path(const GridDev& g, const MediumK& base, P
 // general walker (delta / ratio tracking), any number of plane / sphere shells
 
 // sigma(w) for the walker, out of line: three call sites in the tracking
-// loop share one copy in the instruction stream (config 3: 11.07 -> 10.56 ms)
+// loop share one copy in the instruction stream (config 3: 11.07 -> 10.56 ms).
+// Walks are render / transmittance-estimate work: MUFU exp2 (kFast).
 MF_COLD float proj_area_outlined(int kind, float ax, float ay, float az, V3 w) {
-  return kind == kGGX ? proj_area_ggx(w, ax, ay) : proj_area_erf(w, ax, ay, az);
+  return kind == kGGX ? proj_area_ggx(w, ax, ay) : proj_area_erf<true>(w, ax, ay, az);
 }
 
 struct WalkResult {
