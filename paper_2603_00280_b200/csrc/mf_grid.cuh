@@ -122,9 +122,9 @@ MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir,
   Frame fr = frame_about(n);
   V3 wl = to_local(fr, dir);
   float ax = g.k_xy * sg, az = g.k_z * sg;
-  float area = proj_area_erf(wl, ax, ax, az);
+  float area = proj_area_erf<true>(wl, ax, ax, az);   // render walks: MUFU exp2
   (void)base;
-  return mills(fs.v * frcp(sg)) * frcp(sg) * area;
+  return mills<true>(fs.v * frcp(sg)) * frcp(sg) * area;
 }
 
 struct GridWalk {

@@ -323,7 +323,7 @@ MF_HD float prim_extinction(const SceneDev& sc, int j, V3 x, V3 dir, float lo_mu
   if (f < lo_mult * m.sigma || f > 3.0f * m.sigma) return 0.0f;
   Frame fr = frame_about(prim_normal<kSphere>(p, x));
   float sg = proj_area_outlined(m.kind, m.ax, m.ay, m.az, to_local(fr, dir));
-  return mills(f * m.inv_sigma) * m.inv_sigma * sg;
+  return mills<true>(f * m.inv_sigma) * m.inv_sigma * sg;
 }
 
 // ratio == false: delta tracking (collision mode); ratio == true: ratio
@@ -446,7 +446,7 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
       }
     }
     float fb = fmaxf(fmin - 1e-6f * (1.0f + fabsf(f)), lo);
-    maj += mills(fb * m.inv_sigma) * m.inv_sigma * dirf;
+    maj += mills<true>(fb * m.inv_sigma) * m.inv_sigma * dirf;
   }
   if (!any_band) {
     if (all_done || w.travel + gap_min >= w.t_max) {
