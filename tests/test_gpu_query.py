@@ -137,6 +137,56 @@ def test_sphere_field_and_frames(cuda):
     res = parity.check_rel(r["phase_r"], om.phase_eval_local(WOl, WIl, m)[:, 0],
                            tol=10 * parity.phase_tolerance(WOl, WIl, m))
     assert res["n_bad"] == 0, res
+    # sampled directions: per-query frames travel with the queued samples
+    # (query_kernel's Beckmann ring), world -> local with the oracle frame
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1).astype(np.float64)
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)
+    res = parity.check_samples(to_local(fr, ws), r["pdf_s"], w, WOl, m, u[:, 0], u[:, 1])
+    assert res["n_dir_bad"] == 0 and res["n_pdf_bad"] == 0 and res["n_w_bad"] == 0, res
+
+
+def test_caller_frames(cuda):
+    """Caller-given f and local frames (the reference's `local_frame`
+    argument, medium.py:91-207) with arbitrary orientations: sigma_t, phase
+    and samples in the caller's frame match the oracle."""
+    rs = np.random.default_rng(17)
+    n = 1 << 14
+    nrm = rs.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
+    from oracle.numerics import frame_about, to_local
+    tt, bb, nn = frame_about(nrm)
+    F = np.concatenate([tt.T, bb.T, nn.T]).astype(np.float32)     # rows t.xyz, b.xyz, n.xyz
+    # the frame exactly as the device sees it (float32)
+    fr32 = (F[0:3].T.astype(np.float64), F[3:6].T.astype(np.float64),
+            F[6:9].T.astype(np.float64))
+    f = (rs.uniform(-0.2, 0.1, n)).astype(np.float32)
+    p = np.zeros((n, 3), np.float32)
+    wo = rs.normal(size=(n, 3))
+    wo = (wo / np.linalg.norm(wo, axis=-1, keepdims=True)).astype(np.float32)
+    wi = rs.normal(size=(n, 3))
+    wi = (wi / np.linalg.norm(wi, axis=-1, keepdims=True)).astype(np.float32)
+    u = rs.uniform(size=(n, 2)).astype(np.float32)
+    med = configs.config1_medium()
+    d = cuda.device("cuda", 0)
+    t = lambda a: cuda.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(d)  # noqa: E731
+    out = mf.query_batch(med, t(p.T), t(wo.T), t(wi.T), t(u[:, 0]), t(u[:, 1]), f=t(f),
+                         frame=t(F))
+    r = {k: v.cpu().numpy() for k, v in out.items()}
+    m = parity.f32_medium(med)
+    WOl = to_local(fr32, wo.astype(np.float64))
+    WIl = to_local(fr32, wi.astype(np.float64))
+    res = parity.check_sigma_t(r["sigma_t"], f.astype(np.float64), m.sigma,
+                               om.extinction_local(WOl, f.astype(np.float64), m),
+                               extra=parity.area_conditioning(WOl, m))
+    assert res["n_bad"] == 0, res
+    res = parity.check_rel(r["phase_r"], om.phase_eval_local(WOl, WIl, m)[:, 0],
+                           tol=10 * parity.phase_tolerance(WOl, WIl, m))
+    assert res["n_bad"] == 0, res
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1).astype(np.float64)
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)
+    res = parity.check_samples(to_local(fr32, ws), r["pdf_s"], w, WOl, m, u[:, 0], u[:, 1])
+    assert res["frac_dir_within_1e-5"] >= 0.9999, res
+    assert res["n_dir_bad"] == 0 and res["n_pdf_bad"] == 0 and res["n_w_bad"] == 0, res
 
 
 def test_public_medium_api(cuda):
