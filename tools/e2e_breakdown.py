@@ -34,3 +34,10 @@ for _ in range(N):
 t_copy = (time.perf_counter() - t0) / N
 print({k: round(v * 1e3, 4) for k, v in dict(render=t_full, device_async=t_dev_async,
        device_stats_sync=t_dev_stats, device_sync=t_dev_sync, to64_d2h=t_copy).items()})
+import numpy as np
+h32 = torch.empty((256, 256, 3), dtype=torch.float32, pin_memory=True)
+t0 = time.perf_counter()
+for _ in range(N):
+    h32.copy_(out, non_blocking=True); torch.cuda.synchronize(); x = h32.numpy().astype(np.float64)
+t_b = (time.perf_counter() - t0) / N
+print({"d2h32_astype64": round(t_b * 1e3, 4)})
