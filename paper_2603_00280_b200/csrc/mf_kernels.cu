@@ -706,20 +706,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 // runs with the ~half of the lanes whose mixture branch chose it (10 of 32
 // active on config 2, ncu), and raygen with the few lanes whose path just
 // ended (9 of 32).  Here every warp owns kPool path slots in shared memory
-// (SoA, one tag per slot) and each iteration runs ONE stage on 32 slots that
-// wait for it:
+// (SoA) and one ring of slot indices per visit kind; each iteration pops up
+// to 32 slots of one ring and runs that visit on them:
 //   R  raygen into empty slots, then the first flight;
-//   B  Beckmann visible normal of parked paths;
-//   T  phase tail (pdf, weight, new direction) + depth cap / RR of paths
-//      whose visible normal is drawn, then their next flight;
-// where "flight" = free flight + NEE + the mixture branch: the Beckmann
-// branch parks the path for B, the cheap hemisphere branch draws its normal
-// in place and parks the path for T.  Every slot is empty or waits for B or
-// T, so with 96 slots one of the three always has a full warp of 32 until
-// the path indices run out.  Each path executes exactly the megakernel's
-// arithmetic on the same Philox stream, so the image is bit-identical to
-// path_kernel<0> (tests/test_gpu_render.py); only the order in which paths
-// advance changes.
+//   B  (a collision whose mixture branch is Beckmann) NEE, the Beckmann
+//      visible normal, the phase tail (pdf, weight, new direction), depth
+//      cap / RR, then the next flight;
+//   H  the same with the hemisphere branch's normal;
+// where "flight" = free flight and the mixture branch choice, which parks
+// the collided path on the B or H ring.  Every slot is empty or waits for B
+// or H, so with 96 slots one of the three always has a full warp of 32 until
+// the path indices run out, and every costly stage (NEE, either sampler, the
+// tail) runs at full warp width.  Each path executes exactly the
+// megakernel's arithmetic on the same Philox stream, so the image is
+// bit-identical to path_kernel<0> (tests/test_gpu_render.py); only the order
+// in which paths advance changes.
 
 #ifndef MF_POOL
 #define MF_POOL 96
@@ -730,36 +731,33 @@ constexpr int kPoolWords = kPool / 32;
 constexpr int kRing = 128;   // power of two >= kPool
 constexpr int kWarpsPerBlock = kBlock / 32;
 
-enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageTail = 2, kStageHemi = 3 };
-constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagTail = 2, kTagHemi = 3;
+enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageHemi = 2 };
+constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagHemi = 2;
 
-// float fields of a slot: dir3 T3 L3 sig_o sig_b u_rr lphi, then a union of
-// (u_br, u_s2) while waiting for B and (wm3, vm) while waiting for T, then
+// float fields of a slot: dir3 T3 L3 sig_o sig_b u_rr lphi u_br u_s2, then
 // pos.z (read by the flight after a grazing one, whose log Phi is unknown)
-// and pos.x, pos.y when a point light reads positions
-// (grey scenes, kMono: T and L are one channel each and the slot is 4 words
-// shorter)
+// and pos.x, pos.y when a point light reads positions (grey scenes, kMono:
+// T and L are one channel each and the slot is 4 words shorter)
 template <bool kMono>
 struct PoolF {
   static constexpr int kC = kMono ? 1 : 3;
   static constexpr int kDir = 0, kT = 3, kL = 3 + kC, kSigO = 3 + 2 * kC, kSigB = kSigO + 1,
-                       kUrr = kSigO + 2, kLphi = kSigO + 3, kU = kSigO + 4, kVm = kSigO + 7,
-                       kPz = kSigO + 8, kPxy = kSigO + 9;
+                       kUrr = kSigO + 2, kLphi = kSigO + 3, kU = kSigO + 4, kPz = kSigO + 6,
+                       kPxy = kSigO + 7;
 };
 template <bool kPoint, bool kMono>
 struct PoolSlots {
   float f[PoolF<kMono>::kPxy + (kPoint ? 2 : 0)][kPool];
   uint32_t u[4][kPool];   // pid pixel sample bounce
-  // one ring of slot indices per tag (empty / waiting for B / waiting for
-  // T): a stage pops up to 32 slots of its ring, and every processed slot is
+  // one ring of slot indices per tag (empty / waiting for B / for H): a
+  // visit pops up to 32 slots of its ring, and every processed slot is
   // pushed onto the ring of its new tag
-  uint8_t ring[4][kRing];
+  uint8_t ring[3][kRing];
 };
 
 template <bool kPoint, bool kMono>
 __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, const PathState& st,
-                                           float sig_o, float sig_b, uint8_t tag, V3 wm,
-                                           float vm) {
+                                           float sig_o, float sig_b) {
   using F = PoolF<kMono>;
   P.f[F::kDir][s] = st.dir.x; P.f[F::kDir + 1][s] = st.dir.y; P.f[F::kDir + 2][s] = st.dir.z;
   P.f[F::kT][s] = st.T.x;
@@ -770,12 +768,7 @@ __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, c
   }
   P.f[F::kSigO][s] = sig_o; P.f[F::kSigB][s] = sig_b;
   P.f[F::kUrr][s] = st.u_rr; P.f[F::kLphi][s] = st.lphi;
-  if (tag == kTagBeck || tag == kTagHemi) {
-    P.f[F::kU][s] = st.u_br;  P.f[F::kU + 1][s] = st.u_s2;
-  } else {
-    P.f[F::kU][s] = wm.x;     P.f[F::kU + 1][s] = wm.y;     P.f[F::kU + 2][s] = wm.z;
-    P.f[F::kVm][s] = vm;
-  }
+  P.f[F::kU][s] = st.u_br;  P.f[F::kU + 1][s] = st.u_s2;
   P.f[F::kPz][s] = st.pos.z;
   if constexpr (kPoint) {
     P.f[F::kPxy][s] = st.pos.x; P.f[F::kPxy + 1][s] = st.pos.y;
@@ -789,8 +782,8 @@ __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, c
 // code the compiler removes
 template <bool kPoint, bool kMono>
 __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int s,
-                                          const PassDev& ps, bool beck, PathState& st,
-                                          float& sig_o, float& sig_b, V3& wm, float& vm) {
+                                          const PassDev& ps, PathState& st, float& sig_o,
+                                          float& sig_b) {
   using F = PoolF<kMono>;
   st.dir = v3(P.f[F::kDir][s], P.f[F::kDir + 1][s], P.f[F::kDir + 2][s]);
   if constexpr (kMono) {
@@ -805,13 +798,8 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int
   sig_b = P.f[F::kSigB][s];
   st.u_rr = P.f[F::kUrr][s];
   st.lphi = P.f[F::kLphi][s];
-  if (beck) {
-    st.u_br = P.f[F::kU][s];
-    st.u_s2 = P.f[F::kU + 1][s];
-  } else {
-    wm = v3(P.f[F::kU][s], P.f[F::kU + 1][s], P.f[F::kU + 2][s]);
-    vm = P.f[F::kVm][s];
-  }
+  st.u_br = P.f[F::kU][s];
+  st.u_s2 = P.f[F::kU + 1][s];
   // x, y are never read without a point light (a single plane is
   // translation invariant)
   if constexpr (kPoint) st.pos = v3(P.f[F::kPxy][s], P.f[F::kPxy + 1][s], P.f[F::kPz][s]);
@@ -880,36 +868,31 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
   for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
   __syncwarp();
   // ring heads / tails (warp-uniform): every slot starts empty
-  unsigned he = 0, hb = 0, ht = 0, hh = 0, te = kPool, tb = 0, tt = 0, th = 0;
+  unsigned he = 0, hb = 0, hh = 0, te = kPool, tb = 0, th = 0;
   bool exhausted = false;    // warp-uniform
   while (true) {
-    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nt = (int)(tt - ht),
-        nh = (int)(th - hh);
-    // a full warp of one stage if any; else the largest partial one
+    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nh = (int)(th - hh);
+    // a full warp of one visit kind if any; else the largest partial one
     int stage;
     if (nb >= 32) stage = kStageBeck;
     else if (nh >= 32) stage = kStageHemi;
-    else if (nt >= 32) stage = kStageTail;
     else if (ne >= 32) stage = kStageRaygen;
-    else if (nt > 0 && nt >= nb && nt >= nh) stage = kStageTail;
     else if (nb > 0 && nb >= nh) stage = kStageBeck;
     else if (nh > 0) stage = kStageHemi;
     else if (ne > 0) stage = kStageRaygen;
     else break;
-    // pop up to 32 slots of the stage's ring, the i-th to lane i
-    int cnt = stage == kStageBeck ? nb : (stage == kStageTail ? nt : (stage == kStageHemi ? nh : ne));
-    unsigned head = stage == kStageBeck ? hb : (stage == kStageTail ? ht : (stage == kStageHemi ? hh : he));
+    // pop up to 32 slots of the visit's ring, the i-th to lane i
+    int cnt = stage == kStageBeck ? nb : (stage == kStageHemi ? nh : ne);
+    unsigned head = stage == kStageBeck ? hb : (stage == kStageHemi ? hh : he);
     int n = cnt < 32 ? cnt : 32;
     int slot = lane < n ? (int)P.ring[stage][(head + (unsigned)lane) & (kRing - 1)] : -1;
     if (stage == kStageBeck) hb += (unsigned)n;
-    else if (stage == kStageTail) ht += (unsigned)n;
     else if (stage == kStageHemi) hh += (unsigned)n;
     else he += (unsigned)n;
 
     uint8_t tag = kTagEmpty;
     PathState st;
-    float sig_o = 0.0f, sig_b = 0.0f, vm = 0.0f;
-    V3 wm = v3(0.0f, 0.0f, 0.0f);
+    float sig_o = 0.0f, sig_b = 0.0f;
     bool fly = false;
     if (stage == kStageRaygen) {
       // raygen, full width: path indices with one atomicAdd
@@ -924,45 +907,42 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         fly = true;
       }
     } else if (slot >= 0) {
-      pool_load<kPoint, kMono>(P, slot, ps, stage != kStageTail, st, sig_o, sig_b, wm, vm);
+      pool_load<kPoint, kMono>(P, slot, ps, st, sig_o, sig_b);
       V3 v = neg3(st.dir);   // the plane frame is the identity
-      // next-event estimation of the collision, at full warp width: the
-      // first visit after the flight (B or H) runs it
-      if (stage != kStageTail) planar_nee<kPoint, kSpec, kMono>(sc, st, cn, st.dir, sig_o, st.pos);
+      // next-event estimation of the collision (scatter_stages<0> stage 2)
+      planar_nee<kPoint, kSpec, kMono>(sc, st, cn, st.dir, sig_o, st.pos);
+      // the visible normal of the visit's mixture branch (phase_sample,
+      // two-uniform convention; ndf.py:358-380)
+      float uu = remap_branch_uniform_render(st.u_br, m);
+      V3 wm;
+      float vm;
       if (stage == kStageBeck) {
-        // Beckmann branch of the mixture (phase_sample, two-uniform convention)
-        float uu = remap_branch_uniform_render(st.u_br, m);
         int iters = 0;
         wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
         cn.v[kStSlopeIters] += (uint32_t)iters;
-        tag = kTagTail;
       } else {
-        if (stage == kStageHemi) {
-          // hemisphere branch of the mixture (ndf.py:375-380)
-          float uu = remap_branch_uniform_render(st.u_br, m);
-          wm = hemisphere_about(v, uu, st.u_s2);
-          vm = uu;   // z of wm in v's frame, exactly
-        }
-        // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
-        PhaseSample smp = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
-        st.dir = smp.wi;
-        st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
-        st.bounce++;
-        bool done = false;
-        if (st.bounce >= ps.max_bounces) {             // render.py:92-94
-          done = true;
-        } else if (st.bounce > 8) {                    // render.py:96-105
-          float q = kMono ? fminf(st.T.x, 1.0f) : fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
-          if (st.u_rr >= q) {
-            done = true;
-          } else {
-            st.T = mul3(st.T, 1.0f / q);
-          }
-        }
-        if (done) finish(st);
-        else fly = true;
+        wm = hemisphere_about(v, uu, st.u_s2);
+        vm = uu;   // z of wm in v's frame, exactly
       }
+      // stage 3 of scatter_stages<0>: phase tail, depth cap, RR
+      PhaseSample smp = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b, sig_b > 1e-12f);
+      st.dir = smp.wi;
+      st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
+      st.bounce++;
+      bool done = false;
+      if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+        done = true;
+      } else if (st.bounce > 8) {                    // render.py:96-105
+        float q = kMono ? fminf(st.T.x, 1.0f) : fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+        if (st.u_rr >= q) {
+          done = true;
+        } else {
+          st.T = mul3(st.T, 1.0f / q);
+        }
+      }
+      if (done) finish(st);
+      else fly = true;
     }
     __syncwarp();
     if (fly) {
@@ -979,28 +959,25 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann)) ? sig_o
-                                                                 : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
+          sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann))
+                      ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
           tag = (sig_b > 1e-12f && st.u_br < m.mix) ? kTagBeck : kTagHemi;
         }
       }
     }
-    if (slot >= 0 && tag != kTagEmpty)
-      pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b, tag, wm, vm);
+    if (slot >= 0 && tag != kTagEmpty) pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b);
     // push every processed slot onto the ring of its new tag
     {
       unsigned me = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
       unsigned mb = __ballot_sync(full, slot >= 0 && tag == kTagBeck);
-      unsigned mt = __ballot_sync(full, slot >= 0 && tag == kTagTail);
       unsigned mh = __ballot_sync(full, slot >= 0 && tag == kTagHemi);
       if (slot >= 0) {
-        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : (tag == kTagTail ? mt : mh));
-        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : (tag == kTagTail ? tt : th));
+        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : mh);
+        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : th);
         P.ring[tag][(tail + (unsigned)__popc(mine & lt)) & (kRing - 1)] = (uint8_t)slot;
       }
       te += (unsigned)__popc(me);
       tb += (unsigned)__popc(mb);
-      tt += (unsigned)__popc(mt);
       th += (unsigned)__popc(mh);
     }
     __syncwarp();
