@@ -914,9 +914,14 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
       // the visible normal of the visit's mixture branch (phase_sample,
       // two-uniform convention; ndf.py:358-380)
       float uu = remap_branch_uniform_render(st.u_br, m);
+      // Beckmann guide area of wo (the mixture pdf's sigma_b), here at full
+      // width; a B slot without a guide (sigma_b <= 1e-12) takes the
+      // hemisphere branch, as phase_sample does
+      sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann))
+                  ? sig_o : proj_area_erf<true>(st.dir, m.ax, m.ay, 0.0f);
       V3 wm;
       float vm;
-      if (stage == kStageBeck) {
+      if (stage == kStageBeck && sig_b > 1e-12f) {
         int iters = 0;
         wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
@@ -951,7 +956,6 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
       if (!flight_stage<0, kSpec, kPoint ? 1 : 0>(sc, ps, st, cn)) {
         finish(st);
       } else {
-        V3 wo = st.dir;
         sig_o = st.csig;
         st.pos = st.cpos;
         cn.v[kStScatters]++;
@@ -959,9 +963,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann))
-                      ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
-          tag = (sig_b > 1e-12f && st.u_br < m.mix) ? kTagBeck : kTagHemi;
+          tag = st.u_br < m.mix ? kTagBeck : kTagHemi;
         }
       }
     }
