@@ -734,16 +734,15 @@ constexpr int kWarpsPerBlock = kBlock / 32;
 enum PoolStage : int { kStageRaygen = 0, kStageBeck = 1, kStageHemi = 2 };
 constexpr uint8_t kTagEmpty = 0, kTagBeck = 1, kTagHemi = 2;
 
-// float fields of a slot: dir3 T3 L3 sig_o sig_b u_rr lphi u_br u_s2, then
+// float fields of a slot: dir3 T3 L3 sig_o u_rr lphi u_br u_s2, then
 // pos.z (read by the flight after a grazing one, whose log Phi is unknown)
 // and pos.x, pos.y when a point light reads positions (grey scenes, kMono:
 // T and L are one channel each and the slot is 4 words shorter)
 template <bool kMono>
 struct PoolF {
   static constexpr int kC = kMono ? 1 : 3;
-  static constexpr int kDir = 0, kT = 3, kL = 3 + kC, kSigO = 3 + 2 * kC, kSigB = kSigO + 1,
-                       kUrr = kSigO + 2, kLphi = kSigO + 3, kU = kSigO + 4, kPz = kSigO + 6,
-                       kPxy = kSigO + 7;
+  static constexpr int kDir = 0, kT = 3, kL = 3 + kC, kSigO = 3 + 2 * kC, kUrr = kSigO + 1,
+                       kLphi = kSigO + 2, kU = kSigO + 3, kPz = kSigO + 5, kPxy = kSigO + 6;
 };
 template <bool kPoint, bool kMono>
 struct PoolSlots {
@@ -757,7 +756,7 @@ struct PoolSlots {
 
 template <bool kPoint, bool kMono>
 __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, const PathState& st,
-                                           float sig_o, float sig_b) {
+                                           float sig_o) {
   using F = PoolF<kMono>;
   P.f[F::kDir][s] = st.dir.x; P.f[F::kDir + 1][s] = st.dir.y; P.f[F::kDir + 2][s] = st.dir.z;
   P.f[F::kT][s] = st.T.x;
@@ -766,7 +765,7 @@ __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, c
     P.f[F::kT + 1][s] = st.T.y; P.f[F::kT + 2][s] = st.T.z;
     P.f[F::kL + 1][s] = st.L.y; P.f[F::kL + 2][s] = st.L.z;
   }
-  P.f[F::kSigO][s] = sig_o; P.f[F::kSigB][s] = sig_b;
+  P.f[F::kSigO][s] = sig_o;
   P.f[F::kUrr][s] = st.u_rr; P.f[F::kLphi][s] = st.lphi;
   P.f[F::kU][s] = st.u_br;  P.f[F::kU + 1][s] = st.u_s2;
   P.f[F::kPz][s] = st.pos.z;
@@ -782,8 +781,7 @@ __device__ __forceinline__ void pool_store(PoolSlots<kPoint, kMono>& P, int s, c
 // code the compiler removes
 template <bool kPoint, bool kMono>
 __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int s,
-                                          const PassDev& ps, PathState& st, float& sig_o,
-                                          float& sig_b) {
+                                          const PassDev& ps, PathState& st, float& sig_o) {
   using F = PoolF<kMono>;
   st.dir = v3(P.f[F::kDir][s], P.f[F::kDir + 1][s], P.f[F::kDir + 2][s]);
   if constexpr (kMono) {
@@ -795,7 +793,6 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int
     st.L = v3(P.f[F::kL][s], P.f[F::kL + 1][s], P.f[F::kL + 2][s]);
   }
   sig_o = P.f[F::kSigO][s];
-  sig_b = P.f[F::kSigB][s];
   st.u_rr = P.f[F::kUrr][s];
   st.lphi = P.f[F::kLphi][s];
   st.u_br = P.f[F::kU][s];
@@ -907,7 +904,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         fly = true;
       }
     } else if (slot >= 0) {
-      pool_load<kPoint, kMono>(P, slot, ps, st, sig_o, sig_b);
+      pool_load<kPoint, kMono>(P, slot, ps, st, sig_o);
       V3 v = neg3(st.dir);   // the plane frame is the identity
       // next-event estimation of the collision (scatter_stages<0> stage 2)
       planar_nee<kPoint, kSpec, kMono>(sc, st, cn, st.dir, sig_o, st.pos);
@@ -967,7 +964,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
         }
       }
     }
-    if (slot >= 0 && tag != kTagEmpty) pool_store<kPoint, kMono>(P, slot, st, sig_o, sig_b);
+    if (slot >= 0 && tag != kTagEmpty) pool_store<kPoint, kMono>(P, slot, st, sig_o);
     // push every processed slot onto the ring of its new tag
     {
       unsigned me = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
