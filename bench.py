@@ -1,18 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the macrofacet hot path on B200 (contract in the task brief).
 
-Workload (BASELINE.json configs[1], "config 2"): planar GP surface render,
-256x256 pixels x 64 spp, depth 16, albedo 0.8, orthographic 45 deg camera,
-sun at 30 deg, black environment, seed 1 -- one step = one full render
-(4,194,304 paths) through the persistent path megakernel + per-pixel
-accumulation (+ one NCCL reduce of the fp32 image when N > 1).
+Headline workload (default, BASELINE.json's metric is quoted on it):
+config 4, the variance x correlation sweep -- nine planar GP-surface panels
+sigma in {0.01, 0.05, 0.2} x l_z in {0.02, 0.1, inf} (l_xy = 0.05, albedo
+0.8, orthographic 45 deg camera, sun at 30 deg), each 1024x1024 pixels x
+1024 spp, max depth 64, seed 3.  One step = all nine panels
+(9 x 2^30 = 9,663,676,416 paths): per panel one persistent path-pool launch
+with the per-pixel sums fused in, one finalize launch; at N > 1 one NCCL
+reduce of the nine fp32 panel buffers to rank 0.
 
-Multi-GPU: weak scaling by sample-range sharding -- every rank renders the
-whole image for its own 64-sample range (samples [64r, 64r+64) of a
-64N-spp render) and the fp32 buffers are summed by one NCCL reduce to
-rank 0.  `value` = all ranks' paths / max-over-ranks device time.
+Multi-GPU: strong scaling by image tiles -- 32x32 tiles interleaved
+t -> rank t mod N, so total work is fixed as N grows and the reduce is exact
+(non-owned pixels are +0.0): the image is bit-identical for every N.
+`value` = all paths of the step / max-over-ranks device time.
+
+Other workloads (`--workload`, one JSON line each, for the per-config
+roofline records in profiles/):
+  config1  coefficient queries, N = 2^20 (and a 2^24 kernel-only figure)
+  config2  planar render 256^2 x 64 spp, depth 16, seed 1
+  config3  sphere + point light 512^2 x 256 spp, depth 32, seed 2
+  config5  heterogeneous grid field 2048^2 x 4096 spp, depth 64, seed 4
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload config4|config1|config2|config3|config5]
 """
 
 from __future__ import annotations
@@ -30,9 +41,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "config2: planar GP surface render 256x256 x 64 spp, depth 16 (BASELINE configs[1])"
 METRIC = "Mpaths/s (pixel*spp/s)"
-PATHS_PER_RANK = 256 * 256 * 64
+QMETRIC = "Mqueries/s"
 
 
 def dist_env():
@@ -43,13 +53,41 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# workloads (BASELINE.json configs)
+
+def render_workload(name):
+    """(description, [scenes], spp, depth, seed, scene labels)."""
+    from paper_2603_00280_b200 import configs
+
+    if name == "config4":
+        scenes, labels = [], []
+        for sig in configs.CONFIG4_SIGMAS:
+            for lz in configs.CONFIG4_LZ:
+                scenes.append(configs.config4_scene(sig, lz))
+                labels.append(f"sigma={sig},l_z={lz}")
+        return ("config4: 3x3 panels sigma {0.01,0.05,0.2} x l_z {0.02,0.1,inf}, l_xy 0.05, "
+                "1024x1024 x 1024 spp each, depth 64, seed 3 (BASELINE configs[3])",
+                scenes, 1024, 64, 3, labels)
+    if name == "config2":
+        return ("config2: planar GP surface render 256x256 x 64 spp, depth 16, seed 1 "
+                "(BASELINE configs[1])", [configs.config2_scene()], 64, 16, 1, ["config2"])
+    if name == "config3":
+        return ("config3: sphere GP surface + point light 512x512 x 256 spp, depth 32, seed 2 "
+                "(BASELINE configs[2])", [configs.config3_scene()], 256, 32, 2, ["config3"])
+    if name == "config5":
+        return ("config5: heterogeneous GP field (256^3 SDF of 16 spheres + torus, 128^3 "
+                "value-noise sigma, l_xy 0.03, l_z 0.08) 2048x2048 x 4096 spp, depth 64, seed 4 "
+                "(BASELINE configs[4])", [configs.config5_scene()], 4096, 64, 4, ["config5"])
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML during the timed region)
 
 class ClockSampler:
     """SM clock and throttle reasons sampled every 5 ms through NVML while
-    the timed region runs (nvidia-smi fallback)."""
+    the timed region runs."""
 
-    # NVML clocks-event-reason bits
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
             "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
 
@@ -100,102 +138,168 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference path, process pool)
+# CPU side: the oracle port of the reference path (process pool)
 
-def cpu_baseline(seconds=15.0, workers=None):
+def cpu_mix(workload, budget_s, steps=1, warmup=0):
+    """Time the oracle port on `steps` bounded samples of the workload's
+    scene mix (equal paths per scene, like the GPU step).  Returns
+    (Mpaths/s, workers, sample description, seconds per step)."""
     from oracle import harness
-    from paper_2603_00280_b200 import configs
 
-    scene = configs.config2_scene()
-    workers = workers or harness.host_cores()
-    pool = harness.make_pool(scene, workers)
+    desc, scenes, spp, depth, seed, labels = render_workload(workload)
+    workers = harness.host_cores()
+    jobs, _ = harness.calibrated_mix(scenes, seed, depth, budget_s, workers)
+    pool = harness.make_pool(scenes, workers)
     try:
-        tile = 32 if workers <= 64 else 16
-        spp, n_tiles, rate1 = harness.calibrated_sample(scene, 16, 1, seconds, workers, tile, pool)
-        paths, dt = harness.timed_render(scene, spp, 1, 16, n_tiles, workers, tile, pool)
+        for _ in range(warmup):
+            harness.run_jobs(jobs, pool)
+        tot_p, tot_t = 0, 0.0
+        for _ in range(steps):
+            p, dt = harness.run_jobs(jobs, pool)
+            tot_p += p
+            tot_t += dt
     finally:
         pool.close()
         pool.join()
-    return {"value": paths / dt / 1e6, "unit": METRIC, "cores": workers, "kind": "port",
-            "sample": f"{n_tiles} tiles of {tile}x{tile} px x {spp} spp of config 2 "
-                      f"({paths} paths, {dt:.1f} s), oracle/tracer.py (float64 numpy restatement "
-                      "of the reference walk/trace_paths, identical RNG consumption) on "
-                      f"{workers} processes"}
+    label = f"{len(scenes)} {workload} scene(s) at depth {depth}"
+    return tot_p / tot_t / 1e6, workers, harness.describe(jobs, label, workers), tot_t / steps
 
+
+def cpu_queries(budget_s):
+    """The oracle port of the config-1 query batch (extinction, phase_eval,
+    pdf, phase sample in float64) over a process pool, on a bounded prefix
+    of the 2^20 inputs."""
+    import multiprocessing as mp
+
+    from oracle import harness
+
+    global _QIN
+    from paper_2603_00280_b200 import configs
+
+    _QIN = configs.config1_inputs()   # generated once, inherited by the forked workers
+    workers = harness.host_cores()
+    n = 1 << 14
+    t0 = time.perf_counter()
+    _query_chunk((0, n))
+    one = time.perf_counter() - t0
+    chunks = max(workers, int(budget_s * workers / max(one, 1e-6)))
+    chunks = min(chunks, (1 << 20) // n)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        t0 = time.perf_counter()
+        pool.map(_query_chunk, [(i * n, (i + 1) * n) for i in range(chunks)], chunksize=1)
+        dt = time.perf_counter() - t0
+    q = chunks * n
+    return q / dt / 1e6, workers, (f"{q} of the 2^20 config-1 queries in {chunks} chunks of {n}, "
+                                   "oracle/microfacet.py (float64 restatement of extinction, "
+                                   f"phase_eval, pdf, _phase_sample_u) on {workers} processes")
+
+
+_QIN = None
+
+
+def _query_chunk(rng):
+    from oracle import microfacet as om
+    from paper_2603_00280_b200 import configs
+
+    a, b = rng
+    p, wo, wi, u = _QIN
+    p, wo, wi, u = p[a:b], wo[a:b], wi[a:b], u[a:b]
+    med = _oracle_medium(configs.config1_medium())
+    wo64, wi64 = wo.astype(np.float64), wi.astype(np.float64)
+    om.extinction_local(wo64, p[:, 2].astype(np.float64), med)
+    om.phase_eval_local(wo64, wi64, med)
+    om.phase_pdf_local(wo64, wi64, med)
+    om.phase_sample_local(wo64, med, om.split_two_uniforms(u[:, 0], u[:, 1], med.mix_ratio))
+    return b - a
+
+
+def _oracle_medium(med):
+    import __graft_entry__ as g
+
+    return g._oracle_medium(med)
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port on the host cores
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import harness
-    from paper_2603_00280_b200 import configs
-
-    scene = configs.config2_scene()
-    workers = harness.host_cores()
-    tile = 32 if workers <= 64 else 16
-    pool = harness.make_pool(scene, workers)
-    try:
-        spp, n_tiles, _ = harness.calibrated_sample(scene, 16, 1, args.ref_seconds, workers, tile,
-                                                    pool)
-        for _ in range(args.warmup):
-            harness.timed_render(scene, spp, 1, 16, n_tiles, workers, tile, pool)
-        tot_paths = 0
-        tot_t = 0.0
-        for _ in range(args.steps):
-            p, dt = harness.timed_render(scene, spp, 1, 16, n_tiles, workers, tile, pool)
-            tot_paths += p
-            tot_t += dt
-    finally:
-        pool.close()
-        pool.join()
-    v = tot_paths / tot_t / 1e6
-    sample = (f"per step {n_tiles} tiles of {tile}x{tile} px x {spp} spp of config 2, "
-              "oracle/tracer.py (float64 numpy restatement of the reference render path) on "
-              f"{workers} processes")
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": METRIC, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample": sample},
-            "cpu_baseline": {"value": v, "unit": METRIC, "cores": workers, "kind": "port",
+    if args.workload == "config5":
+        print(json.dumps({"impl": "reference", "unavailable": "config 5 (grid SDF, per-voxel "
+                          "sigma) has no reference implementation (SURVEY.md 8(c))"}))
+        return 0
+    if args.workload == "config1":
+        v, workers, sample = cpu_queries(args.ref_seconds)
+        unit, wl = QMETRIC, "config1: 2^20 coefficient queries (BASELINE configs[0])"
+        ms = None
+    else:
+        v, workers, sample, sec = cpu_mix(args.workload, args.ref_seconds, args.steps,
+                                          args.warmup)
+        unit, wl = METRIC, render_workload(args.workload)[0]
+        ms = sec * 1e3
+    line = {"impl": "reference", "metric": unit, "value": v, "unit": unit, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": wl, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": unit, "cores": workers, "kind": "port",
                              "sample": sample},
-            "e2e": {"value": v, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# our arm: renders
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+def measure_peaks(torch, dev):
+    from paper_2603_00280_b200 import _lib
 
+    lib = _lib.load()
+    f, s = _lib.ctypes.c_double(), _lib.ctypes.c_double()
+    _lib.check(lib.mf_measure_peaks(_lib.ctypes.byref(f), _lib.ctypes.byref(s),
+                                    _lib.stream_handle(torch, dev)))
+    return f.value, s.value
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture of this workload (profiles/), or None."""
+    prof = os.path.join(ROOT, "profiles", f"ncu_{workload}.json")
+    if not os.path.exists(prof):
+        return None
+    try:
+        with open(prof) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_render(args, torch, dist, n, rank, local, dev):
     import paper_2603_00280_b200 as mf
-    from paper_2603_00280_b200 import _lib, configs, roofline
+    from paper_2603_00280_b200 import _lib, roofline
     from paper_2603_00280_b200.scene import to_c_scene
 
-    ws, rank, local = dist_env()
-    if ws != args.gpus and ws > 1:
-        print(f"warning: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
-    n = ws
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if n > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    desc, scenes, spp, depth, seed, labels = render_workload(args.workload)
     lib = _lib.load()
-    scene = configs.config2_scene()
-    cs = to_c_scene(scene)
-    spp_total = 64 * n
-    shard = "samples"
-    out = torch.empty((256, 256, 3), dtype=torch.float32, device=dev)
+    cam = scenes[0].camera
+    P = len(scenes)
+    cs = [to_c_scene(s) for s in scenes]
+    out = torch.empty((P, cam.height, cam.width, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    paths_per_step = P * cam.width * cam.height * spp
 
-    def step():
-        mf.render_device(scene, spp_total, 1, max_bounces=16, rank=rank, nranks=n, shard=shard,
-                         out=out, c_scene=cs)
+    def step(stats_acc=None):
+        for i in range(P):
+            _, st = mf.render_device(scenes[i], spp, seed, max_bounces=depth, tile=32, rank=rank,
+                                     nranks=n, shard="tiles", out=out[i], stats=True, c_scene=cs[i])
+            if stats_acc is not None:
+                stats_acc[i].append(st)
         if n > 1:
-            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
+            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)   # the one collective of the step
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -204,13 +308,14 @@ def run_ours(args):
         dist.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    acc = [[] for _ in range(P)]
     l0 = lib.mf_launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.fill_(float(i))          # evict L2 between steps (256 MiB > 126 MB L2)
             starts[i].record()
-            step()
+            step(acc)
             ends[i].record()
         torch.cuda.synchronize()
         if n > 1:
@@ -221,26 +326,23 @@ def run_ours(args):
     if n > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = n * PATHS_PER_RANK * args.steps / (ms_max * 1e-3) / 1e6
+    value = paths_per_step * args.steps / (ms_max * 1e-3) / 1e6
 
-    # e2e through the public API: render() (host image, float64, validated)
-    # at N=1; render_sharded() + host copy at N>1
-    torch.cuda.synchronize()
-    if n > 1:
-        dist.barrier()
-    e2e_steps = max(1, min(args.steps, 10))
+    # e2e through the public API: render() per scene (host float64 image,
+    # validated) at N = 1; render_sharded() + host copy on rank 0 at N > 1
+    e2e_steps = max(1, min(args.steps, 5))
 
     def e2e_step():
-        if n == 1:
-            mf.render(scene, 64, 1, max_bounces=16)
-        else:
-            img, _ = mf.render_sharded(scene, spp_total, 1, max_bounces=16, shard=shard)
-            if rank == 0:
-                img.cpu()
-            torch.cuda.synchronize()
+        for s in scenes:
+            if n == 1:
+                mf.render(s, spp, seed, max_bounces=depth)
+            else:
+                img, _ = mf.render_sharded(s, spp, seed, max_bounces=depth, shard="tiles")
+                if rank == 0:
+                    img.cpu()
+                torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        e2e_step()
+    e2e_step()
     torch.cuda.synchronize()
     if n > 1:
         dist.barrier()
@@ -250,57 +352,220 @@ def run_ours(args):
     e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if n > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = n * PATHS_PER_RANK * e2e_steps / float(e2e_t.item()) / 1e6
+    e2e_value = paths_per_step * e2e_steps / float(e2e_t.item()) / 1e6
 
-    result = None
-    if rank == 0:
-        # roofline of the dominant kernel (path megakernel), live CUDA events
-        fpk = _lib.ctypes.c_double()
-        spk = _lib.ctypes.c_double()
-        _lib.check(lib.mf_measure_peaks(_lib.ctypes.byref(fpk), _lib.ctypes.byref(spk),
-                                        _lib.stream_handle(torch, dev)))
-        _, st = mf.render_device(scene, spp_total, 1, max_bounces=16, rank=0, nranks=n,
-                                 shard=shard, out=out, stats=True, c_scene=cs)
-        rl = roofline.roofline(st, st["path_kernel_ms"], fpk.value, spk.value, planar=True)
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_path_kernel.json")
-        if os.path.exists(prof):
-            try:
-                with open(prof) as fh:
-                    traffic = json.load(fh).get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
-        roof = {"bound": rl["bound"], "achieved": rl["achieved"], "peak": rl["peak"],
-                "unit": rl["unit"], "frac": rl["frac"], "traffic": traffic,
-                "peak_source": "measured on this device by mf_measure_peaks (FFMA / MUFU.EX2 "
-                               "issue microbenchmarks)",
-                "fp32_frac": rl["fp32_frac"], "sfu_frac": rl["sfu_frac"],
-                "fp32_per_path": rl["fp32_per_path"], "sfu_per_path": rl["sfu_per_path"],
-                "kernel_ms": st["path_kernel_ms"], "kernel": "pool_kernel (single-plane path pool)"}
-        cpu = None
-        if n == 1 and not args.no_cpu:
-            cpu = cpu_baseline(args.cpu_seconds)
-        result = {
-            "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_paths_per_step": n * PATHS_PER_RANK,
-                       "spp_per_rank": 64, "shard": "samples (weak scaling)",
-                       "l2": "flushed between steps (256 MiB device write)",
-                       "parallelism": f"{n} GPU(s), one NCCL reduce per step" if n > 1 else "1 GPU"},
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": METRIC,
-                    "h2d_bytes_per_step": _lib.ctypes.sizeof(_lib.MfScene)
-                    + _lib.ctypes.sizeof(_lib.MfRenderParams),
-                    "d2h_bytes_per_step": 256 * 256 * 3 * 8,   # float64 image
-                    "api": "paper_2603_00280_b200.render()" if n == 1 else "render_sharded()"},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-            "stats_per_path": {k: v / max(st["paths"], 1) for k, v in st.items()
-                               if k not in ("paths", "path_kernel_ms")},
-        }
+    if rank != 0:
+        return None
+    # roofline of the dominant kernel from the TIMED steps: algorithmic ops
+    # from the device event counters of those launches over their CUDA-event
+    # time (measured inside mf_render on the launching stream)
+    pf, ps_ = measure_peaks(torch, dev)
+    F = S = 0.0
+    kms = 0.0
+    tot = {}
+    for i in range(P):
+        planar = scenes[i].primitives[0].sdf.__class__.__name__ == "Plane" and \
+            len(scenes[i].primitives) == 1
+        for st in acc[i]:
+            f, s = roofline.algorithmic_ops(st, planar=planar,
+                                            kind=getattr(scenes[i].primitives[0].medium, "kind",
+                                                         None))
+            F += f
+            S += s
+            kms += st["path_kernel_ms"]
+            for k, v in st.items():
+                tot[k] = tot.get(k, 0) + v
+    rl = roofline.from_ops(F, S, kms, pf, ps_, tot.get("paths", 1))
+    kernel = {"config4": "pool_kernel (single-plane path pool, grey)",
+              "config2": "pool_kernel (single-plane path pool, grey)",
+              "config3": "path_kernel<3> (single-sphere megakernel)",
+              "config5": "path_kernel<2> (grid-field megakernel)"}[args.workload]
+    roof = {"bound": rl["bound"], "achieved": rl["achieved"], "peak": rl["peak"],
+            "unit": rl["unit"], "frac": rl["frac"], "traffic": ncu_traffic(args.workload),
+            "peak_source": "measured on this device by mf_measure_peaks (FFMA / MUFU.EX2 issue "
+                           "microbenchmarks, all SMs)",
+            "fp32_frac": rl["fp32_frac"], "sfu_frac": rl["sfu_frac"],
+            "fp32_per_path": rl["fp32_per_path"], "sfu_per_path": rl["sfu_per_path"],
+            "kernel_ms_per_step": kms / args.steps,
+            "kernel_ms_per_scene": [sum(st["path_kernel_ms"] for st in a) / args.steps
+                                    for a in acc],
+            "kernel_share_of_step": kms / max(ms, 1e-9),
+            "kernel": kernel,
+            "work": "algorithmic FP32 / MUFU lane ops from the frozen per-event counts "
+                    "(paper_2603_00280_b200/roofline.py) x the device event counters of the "
+                    "timed launches"}
+    cpu = None
+    if n == 1 and not args.no_cpu and args.workload != "config5":
+        v, workers, sample, _ = cpu_mix(args.workload, args.cpu_seconds)
+        cpu = {"value": v, "unit": METRIC, "cores": workers, "kind": "port", "sample": sample}
+    elif args.workload == "config5":
+        cpu = {"value": None, "unit": METRIC, "cores": 0, "kind": "port",
+               "sample": "none: config 5 (grid SDF, per-voxel sigma) has no reference "
+                         "implementation to port (SURVEY.md 8(c))"}
+    h2d = P * (_lib.ctypes.sizeof(_lib.MfScene) + _lib.ctypes.sizeof(_lib.MfRenderParams))
+    return {
+        "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": desc, "paths_per_step": paths_per_step, "panels": labels,
+                   "shard": "32x32 image tiles interleaved over ranks (strong scaling)",
+                   "l2": "flushed between steps (256 MiB device write)",
+                   "parallelism": (f"{n} GPUs, one NCCL reduce of the {P} fp32 panel buffers per "
+                                   "step") if n > 1 else "1 GPU"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": P * cam.width * cam.height * 3 * 8,   # float64 images
+                "api": "paper_2603_00280_b200.render() per scene" if n == 1
+                else "render_sharded() per scene + rank-0 host copy"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "stats_per_path": {k: v / max(tot.get("paths", 1), 1) for k, v in tot.items()
+                           if k not in ("paths", "path_kernel_ms")},
+    }
+
+
+# ---------------------------------------------------------------------------
+# our arm: config-1 coefficient queries
+
+def run_queries(args, torch, n, rank, local, dev):
+    import paper_2603_00280_b200 as mf
+    from paper_2603_00280_b200 import _lib, configs, roofline
+
+    lib = _lib.load()
+    med = configs.config1_medium()
+    p, wo, wi, u = configs.config1_inputs()
+    N = p.shape[0]
+    # this rank's slice (no collective: queries are independent)
+    a, b = N * rank // n, N * (rank + 1) // n
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+            (("p", p[a:b].T), ("wo", wo[a:b].T), ("wi", wi[a:b].T), ("u1", u[a:b, 0]),
+             ("u2", u[a:b, 1]))}
+    d = {k: v.to(dev) for k, v in host.items()}
+    outs = {k: torch.empty(b - a, dtype=torch.int32 if k == "flags" else torch.float32,
+                           device=dev) for k in mf.medium._QUERY_OUTS}
+    host_out = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in outs.items()}
+
+    def call(dd, oo):
+        mf.query_batch(med, dd["p"], dd["wo"], dd["wi"], dd["u1"], dd["u2"], out=oo)
+
+    reps = 50
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 1)):
+        call(d, outs)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = lib.mf_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            starts[i].record()
+            for _ in range(reps):     # back to back: the queue stays ahead of the host
+                call(d, outs)
+            ends[i].record()
+        torch.cuda.synchronize()
+    launches = lib.mf_launch_count() - l0
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / (args.steps * reps)
+    value = (b - a) * n / (ms * 1e-3) / 1e6
+    # 2^24 (16 copies of the inputs): the kernel at a size that fills the GPU
+    big = {k: v.repeat(1, 16).contiguous() if v.dim() == 2 else v.repeat(16) for k, v in d.items()}
+    bouts = {k: v.repeat(16) for k, v in outs.items()}
+    call(big, bouts)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(10):
+        call(big, bouts)
+    s1.record()
+    torch.cuda.synchronize()
+    ms24 = s0.elapsed_time(s1) / 10
+    # e2e: pinned host inputs -> device -> kernel -> host outputs, every step
+    e2e_steps = max(3, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dd = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        oo = {k: torch.empty_like(v) for k, v in outs.items()}
+        call(dd, oo)
+        for k, v in oo.items():
+            host_out[k].copy_(v, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if rank != 0:
+        return None
+    pf, ps_ = measure_peaks(torch, dev)
+    rl = roofline.query_roofline(b - a, ms, pf, ps_)
+    rl24 = roofline.query_roofline((b - a) * 16, ms24, pf, ps_)
+    bytes_q = roofline.QUERY_BYTES
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+    cpu = None
+    if n == 1 and not args.no_cpu:
+        v, workers, sample = cpu_queries(args.cpu_seconds)
+        cpu = {"value": v, "unit": QMETRIC, "cores": workers, "kind": "port", "sample": sample}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+    return {
+        "metric": QMETRIC, "value": value, "unit": QMETRIC, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "config1: 2^20 coefficient queries (sigma_t, phase value + pdf, "
+                               "one phase sample; GENERALIZED sigma 0.05, l 0.1), seed 0 "
+                               "(BASELINE configs[0])",
+                   "timing": f"{reps} back-to-back launches per step between CUDA events",
+                   "l2": "flushed between steps (256 MiB device write)"},
+        "roofline": {"bound": rl["bound"], "achieved": rl["frac"] * (pf if rl["bound"] == "fp32"
+                                                                     else ps_),
+                     "peak": pf if rl["bound"] == "fp32" else ps_, "unit": "Ginst/s",
+                     "frac": rl["frac"], "fp32_frac": rl["fp32_frac"], "sfu_frac": rl["sfu_frac"],
+                     "traffic": ncu_traffic("config1"), "kernel": "query_kernel",
+                     "kernel_ms": ms,
+                     "hbm_GB_s": (b - a) * bytes_q / (ms * 1e-3) / 1e9,
+                     "hbm_frac": ((b - a) * bytes_q / (ms * 1e-3) / 1e9 / hbm) if hbm else None,
+                     "at_2^24": {"kernel_ms": ms24, "frac": rl24["frac"],
+                                 "Mqueries_s": (b - a) * 16 / (ms24 * 1e-3) / 1e6,
+                                 "hbm_GB_s": (b - a) * 16 * bytes_q / (ms24 * 1e-3) / 1e9}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": (b - a) * n / e2e_s / 1e6, "unit": QMETRIC, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "paper_2603_00280_b200.query_batch()"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus and ws > 1:
+        print(f"warning: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
+    n = ws
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if n > 1:
+        if rank == 0:
+            # communicator lines (rank count, transport) to stderr, so the
+            # N-rank run is checkable without disturbing the JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=dev)
+        chk = torch.ones(1, device=dev)
+        dist.all_reduce(chk)
+        if rank == 0:
+            print(f"nccl communicator: world_size={dist.get_world_size()} "
+                  f"all_reduce(ones)={int(chk.item())} nccl={torch.cuda.nccl.version()}",
+                  file=sys.stderr)
+    if args.workload == "config1":
+        result = run_queries(args, torch, n, rank, local, dev)
+    else:
+        result = run_render(args, torch, dist, n, rank, local, dev)
+    if result is not None:
+        if n > 1:
+            result["comm"] = {"backend": "nccl", "world_size": n,
+                              "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
         print(json.dumps(result))
     if n > 1:
         dist.barrier()
@@ -311,14 +576,17 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="config4",
+                    choices=("config4", "config1", "config2", "config3", "config5"))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

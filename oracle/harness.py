@@ -6,6 +6,10 @@ with counter block s * 2^28) through `oracle.tracer.render_tile`, fanned
 out over a process pool -- the reference's own thread pool is GIL-bound
 (SURVEY.md section 6), so processes are the fair CPU baseline.
 Used by bench.py's `cpu_baseline` leg and `--impl reference` arm only.
+
+A pool serves a LIST of scenes (the nine config-4 panels); every job names
+its scene, so one timed step can cover a workload mix with the same number
+of paths per scene as the GPU step.
 """
 
 from __future__ import annotations
@@ -14,12 +18,12 @@ import multiprocessing as mp
 import os
 import time
 
-_SCENE = None
+_SCENES = None
 
 
-def _init(scene):
-    global _SCENE
-    _SCENE = scene
+def _init(scenes):
+    global _SCENES
+    _SCENES = scenes
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
 
@@ -27,8 +31,8 @@ def _init(scene):
 def _job(args):
     from .tracer import render_tile
 
-    spp, seed, max_bounces, ys, xs, tile = args
-    ye, xe, img = render_tile(_SCENE, spp, seed, max_bounces, ys, xs, tile)
+    k, spp, seed, max_bounces, ys, xs, tile = args
+    ye, xe, img = render_tile(_SCENES[k], spp, seed, max_bounces, ys, xs, tile)
     return (ye - ys) * (xe - xs) * spp, float(img.sum())
 
 
@@ -39,47 +43,61 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def tile_jobs(scene, spp, seed, max_bounces, n_tiles, tile=32):
+def _tiles(scene, tile):
     cam = scene.camera
-    jobs = []
-    for ys in range(0, cam.height, tile):
-        for xs in range(0, cam.width, tile):
-            jobs.append((spp, seed, max_bounces, ys, xs, tile))
-    return jobs[:n_tiles]
+    return [(ys, xs) for ys in range(0, cam.height, tile) for xs in range(0, cam.width, tile)]
 
 
-def timed_render(scene, spp, seed, max_bounces, n_tiles, workers, tile=32, pool=None):
-    """Render the first n_tiles tiles at `spp`; returns (paths, seconds)."""
-    jobs = tile_jobs(scene, spp, seed, max_bounces, n_tiles, tile)
+def run_jobs(jobs, pool=None, scenes=None):
+    """Run (scene index, spp, seed, depth, ys, xs, tile) jobs; returns
+    (paths, seconds)."""
     t0 = time.perf_counter()
     if pool is not None:
         res = pool.map(_job, jobs, chunksize=1)
     else:
-        _init(scene)
+        _init(scenes)
         res = [_job(j) for j in jobs]
     dt = time.perf_counter() - t0
     return sum(r[0] for r in res), dt
 
 
-def make_pool(scene, workers):
+def make_pool(scenes, workers):
     ctx = mp.get_context("fork")
-    return ctx.Pool(processes=workers, initializer=_init, initargs=(scene,))
+    return ctx.Pool(processes=workers, initializer=_init, initargs=(list(scenes),))
 
 
-def calibrated_sample(scene, max_bounces, seed, budget_s, workers, tile=32, pool=None):
-    """Pick (spp, n_tiles) so one timed_render takes about budget_s on
-    `workers` processes.  Per-tile jobs use the reference's own wavefront
-    size (render.py:141-142: 131072 paths = 128 spp of a 32x32 tile), so
-    numpy batching is as efficient as in the reference's render()."""
-    per_tile = tile * tile
-    spp = max(1, 131072 // per_tile)
-    paths, dt = timed_render(scene, max(1, spp // 4), seed, max_bounces, 1, 1, tile)
-    rate1 = paths / max(dt, 1e-6)           # paths/s on one core
-    target = rate1 * workers * budget_s      # paths in the budget
-    n_img = ((scene.camera.height + tile - 1) // tile) * ((scene.camera.width + tile - 1) // tile)
-    n_tiles = int(max(1, min(n_img, round(target / (spp * per_tile)))))
-    if n_tiles < workers:
-        # fewer jobs than cores: keep every core busy with smaller sample blocks
-        n_tiles = min(n_img, workers)
-        spp = max(1, int(target / (n_tiles * per_tile)))
-    return spp, n_tiles, rate1
+def mix_jobs(scenes, seed, max_bounces, paths_per_scene, jobs_per_scene, tile=32):
+    """Equal paths per scene, each scene's share split into jobs_per_scene
+    tile jobs (distinct tiles, the reference's wavefront size at most)."""
+    jobs = []
+    for k, sc in enumerate(scenes):
+        tiles = _tiles(sc, tile)
+        per_job = max(1, paths_per_scene // jobs_per_scene)
+        spp = max(1, round(per_job / (tile * tile)))
+        for j in range(jobs_per_scene):
+            ys, xs = tiles[(j * 7919) % len(tiles)]
+            jobs.append((k, spp, seed, max_bounces, ys, xs, tile))
+    return jobs
+
+
+def calibrated_mix(scenes, seed, max_bounces, budget_s, workers, tile=32):
+    """Jobs for one step of about budget_s on `workers` processes with
+    equal paths per scene: the single-core rate of every scene is measured
+    on a small tile job first."""
+    secs_per_path = 0.0
+    for k in range(len(scenes)):
+        p, dt = run_jobs([(k, 4, seed, max_bounces, 0, 0, tile)], scenes=scenes)
+        secs_per_path += dt / p
+    secs_per_path /= len(scenes)                   # mean single-core cost
+    total = workers * budget_s / secs_per_path     # paths in the budget
+    per_scene = int(max(tile * tile, total / len(scenes)))
+    jobs_per_scene = max(1, -(-2 * workers // len(scenes)))
+    return mix_jobs(scenes, seed, max_bounces, per_scene, jobs_per_scene, tile), 1.0 / secs_per_path
+
+
+def describe(jobs, scenes_label, workers):
+    paths = sum(j[1] * j[6] * j[6] for j in jobs)
+    return (f"{len(jobs)} tile jobs ({jobs[0][6]}x{jobs[0][6]} px, spp {jobs[0][1]}) over "
+            f"{scenes_label}, {paths} paths, oracle/tracer.py (float64 numpy restatement of the "
+            f"reference walk/trace_paths/render_tile, identical RNG consumption) on {workers} "
+            "processes")

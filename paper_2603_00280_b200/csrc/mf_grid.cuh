@@ -127,6 +127,8 @@ MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir,
   return mills<true>(fs.v * frcp(sg)) * frcp(sg) * area;
 }
 
+constexpr int kGridIterCap = 1000000;
+
 struct GridWalk {
   int outcome;   // kEscaped / kAbsorbed / kCollided (values of mf_transport.cuh)
   V3 pos;
@@ -195,7 +197,8 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   U4 bits = U4{0, 0, 0, 0};
   int avail = 0;
   uint32_t call = call0;
-  for (int iter = 0; iter < 1000000; ++iter) {
+  int iter = 0;
+  for (; iter < kGridIterCap; ++iter) {
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
     float mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
 #if defined(MF_GRID_DEBUG) && !defined(__CUDA_ARCH__)
@@ -304,6 +307,13 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
     }
   }
   w.pos = fma3(dir, t, pos);
+  if (iter >= kGridIterCap) {
+    // iteration cap (transport.py:297 raises): a distinct result, counted
+    // by the callers as capped, never taken for an escape
+    w.outcome = 1;
+    w.weight = 0.0f;
+    w.steps = -1;
+  }
   return w;
 }
 

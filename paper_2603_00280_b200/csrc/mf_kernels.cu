@@ -9,9 +9,9 @@
 //                     segment (warp-level compaction / path regeneration),
 //                     so path state never leaves registers
 //                     (render.py:32-108, transport.py:144-297)
-//   accumulate_kernel deterministic fixed-order per-pixel sum of the pass's
-//                     per-path radiance into the caller's fp32 buffer
-//                     (render.py:150,165-166)
+//   finalize_kernel   per-pixel 64-bit fixed-point sums (accumulated by the
+//                     render kernels themselves, accumulate_fx) -> the
+//                     caller's fp32 buffer (render.py:150,165-166)
 //   ratio_kernel      ratio-tracking transmittance samples (transport.py:300-313)
 #include <cuda_runtime.h>
 
@@ -278,8 +278,13 @@ struct PassDev {
   uint32_t sample_begin; // global sample index of the pass's first sample
   uint32_t n_local;      // local pixels of this rank (render mode)
   int shard, rank, nranks, tile, tiles_x;
-  int mono;              // the pass buffer holds channel 0 only (grey pool kernel)
-  float* rad;            // SoA [3][n_paths]
+  int mono;              // grey scene: the accumulator holds channel 0 only
+  // render mode: per-pixel fixed-point sums (accumulate_fx), channel-major
+  // per local pixel: fx[lp * (mono ? 1 : 3) + c] += rint(L_c * fx_scale)
+  unsigned long long* fx;
+  float fx_scale;        // 2^k (host-chosen, mf_render)
+  float fx_limit;        // per-path bound of L * fx_scale: the sums cannot overflow
+  float* rad;            // caller-ray mode (trace_paths): SoA [3][n_paths]
   unsigned int* counter;
   unsigned long long* stats;
   // caller-ray mode (trace_paths)
@@ -311,7 +316,7 @@ struct PathState {
   float u_br, u_s2, u_rr;  // the segment's branch / slope / RR uniforms
   float lphi;            // single plane: log Phi(f / sigma) at pos, NaN when unknown
   int bounce;
-  uint32_t pid;          // result slot: caller-ray index, or s * n_local + lp (render)
+  uint32_t pid;          // result slot: caller-ray index, or the local pixel (render)
   PathRng rng;
 };
 
@@ -353,15 +358,17 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
   } else if constexpr (kMode == 2) {
     GridWalk w = grid_walk_path(sc.grid, sc.media[0], st.rng, (uint32_t)st.bounce, kCallShadow,
                                 pos, wl, true, t_max, kShadowRR);
-    cn.v[kStTrackSteps] += (uint32_t)w.steps;
+    cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
-    return w.weight;
+    if (w.steps < 0) cn.v[kStCapped]++;   // iteration cap: raised by the host
+    return w.steps < 0 ? 0.0f : w.weight;
   } else {
     WalkResult w = walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max,
                         kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
-    return w.weight;
+    if (w.steps < 0) cn.v[kStCapped]++;
+    return w.steps < 0 ? 0.0f : w.weight;
   }
 }
 
@@ -439,10 +446,10 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& 
   if constexpr (kMode == 2) {
     GridWalk w = grid_walk_path(sc.grid, sc.media[0], st.rng, (uint32_t)st.bounce, 1u, st.pos,
                                 st.dir, false, INFINITY, 0.0f);
-    cn.v[kStTrackSteps] += (uint32_t)w.steps;
+    cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
     st.cpos = w.pos;
-    outcome = w.outcome;
+    outcome = w.steps < 0 ? -1 : w.outcome;
   } else if constexpr (kMode == 0) {
     const MediumK& m = sc.media[0];
     float sig = proj_area<kSpec, true>(m, st.dir);
@@ -605,17 +612,14 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
     st.dir = v3(ps.dir[my], ps.dir[ps.n_paths + my], ps.dir[2u * ps.n_paths + my]);
     return true;
   }
-  uint32_t lp = my / ps.S;
-  uint32_t s = my - lp * ps.S;
-  // sample-major result slots: accumulate_kernel reads them coalesced
-  st.pid = s * ps.n_local + lp;
+  // sample-major path order: the 32 paths a warp starts together belong to
+  // 32 consecutive pixels, so the fixed-point adds of paths finishing
+  // together hit distinct (adjacent) accumulator words instead of one
+  uint32_t s = my / ps.n_local;
+  uint32_t lp = my - s * ps.n_local;
+  st.pid = lp;   // the path's radiance goes to its local pixel's sums
   int pixel = local_to_pixel(sc, ps, lp);
-  if (pixel < 0) {
-    ps.rad[st.pid] = 0.0f;
-    ps.rad[ps.n_paths + st.pid] = 0.0f;
-    ps.rad[2u * ps.n_paths + st.pid] = 0.0f;
-    return false;
-  }
+  if (pixel < 0) return false;   // tile padding
   st.rng.pixel = (uint32_t)pixel;
   st.rng.sample = ps.sample_begin + s;
   U4 jb = philox_rk(U4{st.rng.pixel, st.rng.sample, kSegCamera, 0u}, ps.rk);
@@ -623,14 +627,46 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   return true;
 }
 
+// Per-pixel accumulation fused into the render kernels (render.py:150,
+// 165-166): a finished path adds rint(L * 2^k) to its pixel's 64-bit
+// fixed-point sum with one fire-and-forget atomic (RED.ADD.64) per channel.
+// Integer addition is associative, so the sums -- and the image -- do not
+// depend on the order in which paths finish (any launch geometry, pool
+// schedule or tile / rank split), and no per-path radiance ever goes to HBM.
+// L * 2^k is exact in fp32 (a power-of-two scale), so every value >= 2^(24-k)
+// enters the sum with its full fp32 mantissa and the sum itself is exact;
+// fx_limit keeps spp such values below 2^63.  A path whose radiance is
+// non-finite, negative or beyond the limit is counted (the host raises
+// NumericFailureError, RadianceImage.validate, image.py:38-42) and adds 0.
+__device__ __forceinline__ void accumulate_fx(const PassDev& ps, uint32_t slot, float v,
+                                              Counters& cn) {
+  float q = v * ps.fx_scale;
+  if (!(q >= 0.0f && q < ps.fx_limit)) {   // also catches NaN
+    cn.v[kStNonfinite]++;
+    return;
+  }
+  unsigned long long iq = __float2ull_rn(q);
+  if (iq) atomicAdd(ps.fx + slot, iq);
+}
+
+template <bool kCallerRays>
 __device__ __forceinline__ void finish_path(const PassDev& ps, const PathState& st, Counters& cn) {
   float r = st.L.x, g = st.L.y, bl = st.L.z;
-  if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
-    cn.v[kStNonfinite]++;
+  if constexpr (kCallerRays) {
+    if (!(isfinite(r) && isfinite(g) && isfinite(bl)) || r < 0.0f || g < 0.0f || bl < 0.0f) {
+      cn.v[kStNonfinite]++;
+    }
+    ps.rad[st.pid] = r;
+    ps.rad[ps.n_paths + st.pid] = g;
+    ps.rad[2u * ps.n_paths + st.pid] = bl;
+  } else if (ps.mono) {
+    // grey scene: the three channels are equal by construction
+    accumulate_fx(ps, st.pid, r, cn);
+  } else {
+    accumulate_fx(ps, st.pid * 3u, r, cn);
+    accumulate_fx(ps, st.pid * 3u + 1u, g, cn);
+    accumulate_fx(ps, st.pid * 3u + 2u, bl, cn);
   }
-  ps.rad[st.pid] = r;
-  ps.rad[ps.n_paths + st.pid] = g;
-  ps.rad[2u * ps.n_paths + st.pid] = bl;
 }
 
 // Warp-level regeneration: the dead lanes of the warp take popc(dead) path
@@ -677,7 +713,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
     if (active) {
       coll = flight_stage<kMode>(sc, ps, st, cn);
       if (!coll) {
-        finish_path(ps, st, cn);
+        finish_path<kCallerRays>(ps, st, cn);
         active = false;
       }
     }
@@ -686,7 +722,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
     unsigned smask = __ballot_sync(full, active && coll);
     if (active && coll) {
       if (scatter_stage<kMode>(sc, ps, st, cn, smask)) {
-        finish_path(ps, st, cn);
+        finish_path<kCallerRays>(ps, st, cn);
         active = false;
       }
     }
@@ -809,14 +845,6 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int
   st.bounce = (int)P.u[3][s];
 }
 
-// a finished path of a grey scene: channel x only (ps.mono)
-__device__ __forceinline__ void finish_path_mono(const PassDev& ps, const PathState& st,
-                                                 Counters& cn) {
-  float r = st.L.x;
-  if (!isfinite(r) || r < 0.0f) cn.v[kStNonfinite]++;
-  ps.rad[st.pid] = r;   // one channel; accumulate_kernel (ps.mono) reads only it
-}
-
 // next-event estimation at a collision of the single plane (the stage-2
 // block of scatter_stages<0>, same arithmetic); kPoint: the scene has a point
 // light (its code is compiled out otherwise).  The plane frame is the
@@ -858,8 +886,9 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
 #pragma unroll
   for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
   auto finish = [&](const PathState& q) {
-    if constexpr (kMono) finish_path_mono(ps, q, cn);
-    else finish_path(ps, q, cn);
+    // grey scenes (kMono): channel x only, ps.mono is set
+    if constexpr (kMono) accumulate_fx(ps, q.pid, q.L.x, cn);
+    else finish_path<false>(ps, q, cn);
   };
 #pragma unroll
   for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
@@ -988,61 +1017,36 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
   }
 }
 
-// per-pixel fixed-order sum of a pass (render.py:150,165-166)
-// Block = 8 warps x 32 consecutive local pixels.  Warp w sums the samples
-// of chunk w (S/8 consecutive samples, fixed order; each load of the warp is
-// one coalesced 128-byte row of the sample-major slots), then the eight
-// partial sums combine through shared memory in a fixed tree.  Eight times
-// the memory-level parallelism of one thread per pixel; the order depends on
-// S only, so the image stays deterministic.
-constexpr int kAccWarps = 8;
-__global__ void __launch_bounds__(256) accumulate_kernel(const __grid_constant__ SceneDev sc,
-                                                          const __grid_constant__ PassDev ps,
-                                                          uint32_t n_local, float inv_spp,
-                                                          float* accum) {
-  __shared__ float part[3][kAccWarps][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t lp = blockIdx.x * 32u + (uint32_t)lane;
-  uint32_t chunk = (ps.S + kAccWarps - 1) / kAccWarps;
-  uint32_t s_lo = min(ps.S, (uint32_t)w * chunk), s_hi = min(ps.S, s_lo + chunk);
-  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
-  if (lp < n_local) {
-    const float* r = ps.rad + lp;
-    if (ps.mono) {
-      // grey pool kernel: channel 0 only, the same sum for all three
-      for (uint32_t s = s_lo; s < s_hi; ++s) s0 += __ldg(r + (size_t)s * n_local);
-      s1 = s0;
-      s2 = s0;
-    } else {
-      for (uint32_t s = s_lo; s < s_hi; ++s) {
-        size_t o = (size_t)s * n_local;
-        s0 += __ldg(r + o);
-        s1 += __ldg(r + ps.n_paths + o);
-        s2 += __ldg(r + 2u * ps.n_paths + o);
-      }
-    }
-  }
-  part[0][w][lane] = s0;
-  part[1][w][lane] = s1;
-  part[2][w][lane] = s2;
-  __syncthreads();
-  if (w != 0 || lp >= n_local) return;
+// fixed-point pixel sums -> the caller's fp32 image (render.py:165-166):
+// one thread per local pixel, sum * 2^-k / spp in double, added to (or
+// written into) accum[pixel][c]
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ SceneDev sc,
+                                                        const __grid_constant__ PassDev ps,
+                                                        uint32_t n_local, double inv_scale_spp,
+                                                        int add, float* accum) {
+  uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lp >= n_local) return;
   int pixel = local_to_pixel(sc, ps, lp);
   if (pixel < 0) return;
   float t[3];
+  if (ps.mono) {
+    t[0] = t[1] = t[2] = (float)((double)ps.fx[lp] * inv_scale_spp);
+  } else {
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    float q0 = part[c][0][lane] + part[c][1][lane], q1 = part[c][2][lane] + part[c][3][lane];
-    float q2 = part[c][4][lane] + part[c][5][lane], q3 = part[c][6][lane] + part[c][7][lane];
-    t[c] = (q0 + q1) + (q2 + q3);
+    for (int c = 0; c < 3; ++c) t[c] = (float)((double)ps.fx[(size_t)lp * 3 + c] * inv_scale_spp);
   }
   float* a = accum + (size_t)pixel * 3;
-  float v0 = a[0] + t[0] * inv_spp, v1 = a[1] + t[1] * inv_spp, v2 = a[2] + t[2] * inv_spp;
+  float v0 = t[0], v1 = t[1], v2 = t[2];
+  if (add) {
+    v0 += a[0];
+    v1 += a[1];
+    v2 += a[2];
+  }
   a[0] = v0;
   a[1] = v1;
   a[2] = v2;
-  // RadianceImage.validate (image.py:38-42) on the device: the per-path
-  // check in finish_path cannot see a sum that overflows
+  // RadianceImage.validate (image.py:38-42) of the stored value (an added
+  // caller value may be anything)
   if (!(isfinite(v0) && isfinite(v1) && isfinite(v2)) || v0 < 0.0f || v1 < 0.0f || v2 < 0.0f)
     atomicAdd(ps.stats + kStNonfinite, 1ull);
 }
@@ -1053,7 +1057,7 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
                                                         V3 org, V3 dir, uint32_t n, float* w_out,
                                                         unsigned long long* stats) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t steps = 0, viol = 0;
+  uint32_t steps = 0, viol = 0, capped = 0;
   if (i < n) {
     PathRng rng{k0, k1, stream_lo, i};
     if (sc.has_grid) {
@@ -1061,20 +1065,24 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
                              [&](uint32_t call) { return rng_block(rng, 0u, call); },
                              kCallShadow, org, dir, true, INFINITY);
       w_out[i] = w.weight;
-      steps = (uint32_t)w.steps;
+      steps = (uint32_t)max(w.steps, 0);
       viol = (uint32_t)w.violations;
+      capped = w.steps < 0 ? 1u : 0u;
     } else {
       WalkResult w = walk(sc, rng, 0u, kCallShadow, org, dir, true, INFINITY);
       w_out[i] = w.weight;
       steps = (uint32_t)max(w.steps, 0);
       viol = (uint32_t)w.violations;
+      capped = w.steps < 0 ? 1u : 0u;
     }
   }
   unsigned a = __reduce_add_sync(0xffffffffu, steps);
   unsigned b = __reduce_add_sync(0xffffffffu, viol);
+  unsigned c = __reduce_add_sync(0xffffffffu, capped);
   if ((threadIdx.x & 31) == 0) {
     if (a) atomicAdd(stats + kStTrackSteps, (unsigned long long)a);
     if (b) atomicAdd(stats + kStViolations, (unsigned long long)b);
+    if (c) atomicAdd(stats + kStCapped, (unsigned long long)c);
   }
 }
 
@@ -1260,14 +1268,15 @@ int check_stats(const mf_stats& s) {
                                      std::to_string(s.majorant_violations) + " events)");
   if (s.capped) return fail(MF_ERR_CAP, "walker exceeded its iteration cap");
   if (s.nonfinite)
-    return fail(MF_ERR_NUMERIC, "non-finite or negative radiance in " +
-                                    std::to_string(s.nonfinite) + " paths");
+    return fail(MF_ERR_NUMERIC, "non-finite, negative or out-of-range (above 2^20 x the "
+                                "brightest emitter) radiance in " +
+                                    std::to_string(s.nonfinite) + " paths / pixels");
   return MF_OK;
 }
 
-// scratch: per-path radiance, work counter, stats
+// scratch: per-pixel fixed-point sums, work counter, stats
 struct Scratch {
-  float* rad = nullptr;
+  unsigned long long* fx = nullptr;
   unsigned int* counter = nullptr;
   unsigned long long* stats = nullptr;
 };
@@ -1290,10 +1299,13 @@ int retain_pool_memory() {
   return MF_OK;
 }
 
-int scratch_alloc(Scratch* s, size_t n_paths, cudaStream_t st) {
+int scratch_alloc(Scratch* s, size_t n_fx, cudaStream_t st) {
   int rc = retain_pool_memory();
   if (rc) return rc;
-  MF_CUDA(cudaMallocAsync((void**)&s->rad, std::max<size_t>(n_paths, 1) * 3 * sizeof(float), st));
+  if (n_fx) {
+    MF_CUDA(cudaMallocAsync((void**)&s->fx, n_fx * sizeof(unsigned long long), st));
+    MF_CUDA(cudaMemsetAsync(s->fx, 0, n_fx * sizeof(unsigned long long), st));
+  }
   MF_CUDA(cudaMallocAsync((void**)&s->counter, 64 * sizeof(unsigned int), st));
   MF_CUDA(cudaMallocAsync((void**)&s->stats, kStCount * sizeof(unsigned long long), st));
   MF_CUDA(cudaMemsetAsync(s->stats, 0, kStCount * sizeof(unsigned long long), st));
@@ -1301,7 +1313,7 @@ int scratch_alloc(Scratch* s, size_t n_paths, cudaStream_t st) {
 }
 
 int scratch_free(Scratch* s, cudaStream_t st) {
-  if (s->rad) MF_CUDA(cudaFreeAsync(s->rad, st));
+  if (s->fx) MF_CUDA(cudaFreeAsync(s->fx, st));
   if (s->counter) MF_CUDA(cudaFreeAsync(s->counter, st));
   if (s->stats) MF_CUDA(cudaFreeAsync(s->stats, st));
   *s = Scratch();
@@ -1365,7 +1377,33 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   return MF_OK;
 }
 
-constexpr size_t kMaxPassPaths = size_t(1) << 26;  // 64 Mi paths (768 MiB of radiance)
+// paths per launch: path indices are 32-bit (one launch covers a whole
+// render unless it exceeds this; the fixed-point sums carry across launches)
+constexpr size_t kMaxPassPaths = size_t(1) << 31;
+
+// Fixed-point scale 2^k of the pixel sums (accumulate_fx) for a render of
+// `spp` samples per pixel whose brightest emitter (environment, sun, point
+// light channel) is e_max: each path may carry up to 2^20 e_max of radiance
+// and the sum of spp of them stays below 2^63.  Returns k and the per-path
+// limit of L * 2^k.
+void fx_scale(double e_max, uint64_t spp, float* scale, float* limit, int* k_out) {
+  int lg_s = 0;
+  while (lg_s < 62 && (uint64_t(1) << lg_s) < spp) ++lg_s;
+  int lg_e = (int)std::ceil(std::log2(std::max(e_max, 1e-30)));
+  int k = 63 - lg_s - 20 - lg_e;
+  k = std::max(-100, std::min(100, k));
+  *scale = std::ldexp(1.0f, k);
+  *limit = std::ldexp(1.0f, 63 - lg_s);
+  *k_out = k;
+}
+
+double scene_emax(const SceneDev& sc) {
+  double e = std::max({(double)sc.env.x, (double)sc.env.y, (double)sc.env.z});
+  if (sc.has_sun) e = std::max({e, (double)sc.sun_L.x, (double)sc.sun_L.y, (double)sc.sun_L.z});
+  if (sc.has_point)
+    e = std::max({e, (double)sc.point_I.x, (double)sc.point_I.y, (double)sc.point_I.z});
+  return e;
+}
 
 }  // namespace
 
@@ -1601,22 +1639,25 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     if (stats) std::memset(stats, 0, sizeof(*stats));
     return MF_OK;
   }
-  uint32_t S_pass = (uint32_t)std::max<size_t>(1, std::min<size_t>(s_count, kMaxPassPaths / n_local));
-  size_t max_pass_paths = n_local * S_pass;
-  if (max_pass_paths > 0xffffffffull) return fail(MF_ERR_PARAM, "image too large for one pass");
+  size_t max_pass = kMaxPassPaths;
+  if (const char* e = std::getenv("MF_MAX_PASS_PATHS")) {   // test hook: force several launches
+    long long v = std::atoll(e);
+    if (v > 0) max_pass = std::min<size_t>(max_pass, (size_t)v);
+  }
+  uint32_t S_pass = (uint32_t)std::max<size_t>(1, std::min<size_t>(s_count, max_pass / n_local));
+  if (n_local * S_pass > 0xffffffffull) return fail(MF_ERR_PARAM, "image too large for one pass");
+  // grey scenes keep one channel per pixel (all kernels; channels are equal)
+  ps.mono = sc.mono;
+  size_t n_fx = n_local * (ps.mono ? 1 : 3);
   Scratch scr;
-  rc = scratch_alloc(&scr, max_pass_paths, st);
+  rc = scratch_alloc(&scr, n_fx, st);
   if (rc) return rc;
-  ps.rad = scr.rad;
+  ps.fx = scr.fx;
   ps.counter = scr.counter;
   ps.stats = scr.stats;
-#ifndef MF_NO_POOL
-  // the grey pool kernel writes one channel per path (finish_path_mono)
-  ps.mono = (sc.single_plane && !sc.has_grid && sc.mono && !megakernel_requested()) ? 1 : 0;
-#endif
-  float inv_spp = (float)(1.0 / p.spp);
-  // path-kernel timing: one event pair per pass, read after the final sync
-  // (no host round trip between the path and accumulate kernels)
+  int k = 0;
+  fx_scale(scene_emax(sc), s_count, &ps.fx_scale, &ps.fx_limit, &k);
+  // path-kernel timing: one event pair per launch, read after the final sync
   std::vector<cudaEvent_t> ev;
   double kernel_ms = 0.0;
   for (uint32_t s0 = 0; s0 < s_count; s0 += S_pass) {
@@ -1626,39 +1667,40 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.n_paths = (uint32_t)(n_local * S);
     ps.n_local = (uint32_t)n_local;
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
-    if (stats) {
-      ev.resize(ev.size() + 2, nullptr);
-      MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));
-      MF_CUDA(cudaEventCreate(&ev[ev.size() - 1]));
-      MF_CUDA(cudaEventRecord(ev[ev.size() - 2], st));
-    }
+    ev.resize(ev.size() + 2, nullptr);
+    MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));
+    MF_CUDA(cudaEventCreate(&ev[ev.size() - 1]));
+    MF_CUDA(cudaEventRecord(ev[ev.size() - 2], st));
     rc = launch_paths(sc, ps, false, st);
-    if (stats && !rc) MF_CUDA(cudaEventRecord(ev[ev.size() - 1], st));
+    if (!rc) MF_CUDA(cudaEventRecord(ev[ev.size() - 1], st));
     if (rc) {
       for (cudaEvent_t e : ev) cudaEventDestroy(e);
       scratch_free(&scr, st);
       return rc;
     }
-    accumulate_kernel<<<(uint32_t)((n_local + 31) / 32), 256, 0, st>>>(sc, ps, (uint32_t)n_local,
-                                                                      inv_spp, d_accum);
-    g_launches++;
-    MF_CUDA(cudaGetLastError());
   }
-  int out = MF_OK;
-  if (stats) {
-    unsigned long long h[kStCount];
-    MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
-    MF_CUDA(cudaStreamSynchronize(st));
-    fill_stats(h, stats);
-    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
-      float ms = 0.0f;
-      MF_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-      kernel_ms += ms;
-    }
-    for (cudaEvent_t e : ev) cudaEventDestroy(e);
-    stats->path_kernel_ms = kernel_ms;
-    out = check_stats(*stats);
+  ps.n_local = (uint32_t)n_local;
+  finalize_kernel<<<(uint32_t)((n_local + 255) / 256), 256, 0, st>>>(
+      sc, ps, (uint32_t)n_local, std::ldexp(1.0, -k) / (double)p.spp, p.accumulate ? 1 : 0, d_accum);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  // the event counters always come back: majorant violations, iteration caps
+  // and invalid radiance raise, as the reference's render() always
+  // validates (transport.py:264-268,297; image.py:38-42)
+  unsigned long long h[kStCount];
+  MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+  MF_CUDA(cudaStreamSynchronize(st));
+  mf_stats local;
+  mf_stats& out_st = stats ? *stats : local;
+  fill_stats(h, &out_st);
+  for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+    float ms = 0.0f;
+    MF_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+    kernel_ms += ms;
   }
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  out_st.path_kernel_ms = kernel_ms;
+  int out = check_stats(out_st);
   rc = scratch_free(&scr, st);
   return out ? out : rc;
 }
@@ -1704,12 +1746,15 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
   MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
   rc = launch_paths(sc, ps, true, st);
   int out = rc;
-  if (!rc && stats) {
+  if (!rc) {
+    // always validated, as render()
     unsigned long long h[kStCount];
     MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     MF_CUDA(cudaStreamSynchronize(st));
-    fill_stats(h, stats);
-    out = check_stats(*stats);
+    mf_stats local;
+    mf_stats& o = stats ? *stats : local;
+    fill_stats(h, &o);
+    out = check_stats(o);
   }
   int rc2 = scratch_free(&scr, st);
   return out ? out : rc2;
@@ -1751,6 +1796,9 @@ int mf_transmittance(const mf_scene* scene, const double origin[3], const double
   MF_CUDA(cudaStreamSynchronize(st));
   if (hs[kStViolations])
     return fail(MF_ERR_MAJORANT, "extinction exceeded its majorant in ratio tracking");
+  if (hs[kStCapped])
+    return fail(MF_ERR_CAP, "ratio tracking exceeded its iteration cap in " +
+                                std::to_string(hs[kStCapped]) + " samples");
   // mean and standard error in double, fixed order (transport.py:310-313)
   double s = 0.0;
   for (float v : hw) s += v;

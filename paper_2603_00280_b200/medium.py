@@ -105,11 +105,13 @@ _QUERY_OUTS = ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx", "wsy", 
 
 
 def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None, frame=None,
-                outputs=_QUERY_OUTS, stream=None):
+                outputs=_QUERY_OUTS, stream=None, out=None):
     """Fused coefficient query (BASELINE config 1) on device tensors.
 
     p, wo, wi: (3, n) float32 CUDA tensors (SoA rows); u1, u2: (n,).
     Optional f (n,) and frame (9, n) override the field-derived values.
+    `out`: caller-allocated {name: (n,) CUDA tensor} (float32, flags int32)
+    to write into instead of allocating.
     Returns {name: CUDA tensor} for the requested outputs."""
     torch = _lib.require_cuda()
     lib = _lib.load()
@@ -126,11 +128,18 @@ def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None,
     qi.f = f.data_ptr() if f is not None else None
     qi.frame = frame.data_ptr() if frame is not None else None
     qo = _lib.MfQueryOut()
-    out = {}
-    for name in outputs:
-        dt = torch.int32 if name == "flags" else torch.float32
-        t = torch.empty(n, dtype=dt, device=dev)
-        out[name] = t
+    if out is None:
+        out = {}
+        for name in outputs:
+            dt = torch.int32 if name == "flags" else torch.float32
+            out[name] = torch.empty(n, dtype=dt, device=dev)
+    for name, t in out.items():
+        if name not in _QUERY_OUTS:
+            raise ParameterDomainError(f"unknown query output {name!r}")
+        want = torch.int32 if name == "flags" else torch.float32
+        if t.dtype != want or not t.is_cuda or not t.is_contiguous() or t.numel() != n:
+            raise ParameterDomainError(f"output {name!r} must be a contiguous ({n},) "
+                                       f"{want} CUDA tensor")
         setattr(qo, name, t.data_ptr())
     fld = field if field is not None else _plane_field()
     cm = to_c_medium(medium)

@@ -102,20 +102,36 @@ def query_roofline(n_queries, kernel_ms, peak_fp32_ginst, peak_sfu_ginst):
             "sfu_frac": fs, "fp32_per_query": QUERY[0], "sfu_per_query": QUERY[1]}
 
 
-def algorithmic_ops(stats, planar=False):
+# bytes one config-1 query moves: 11 float32 inputs + 13 outputs (sigma_t,
+# phase rgb, pdf, sampled direction, pdf_s, weight rgb, flags)
+QUERY_BYTES = 11 * 4 + 13 * 4
+
+# Beckmann media (config-4 panels with l_z = inf) evaluate the height-field
+# NDF instead of the generalized one in phase_eval (NEE) and in the sample
+# weight (scatter): the difference of the two NDF costs per such event
+_BECK_DIFF = (PRIMS["ndf_generalized"][0] - PRIMS["ndf_beckmann"][0],
+              PRIMS["ndf_generalized"][1] - PRIMS["ndf_beckmann"][1])
+
+
+def algorithmic_ops(stats, planar=False, kind=None):
     """(fp32 lane ops, sfu lane ops) of a render from its mf_stats counters;
-    planar=True: the sun-lit single-plane event costs (PLANAR_EVENTS)."""
+    planar=True: the sun-lit single-plane event costs (PLANAR_EVENTS);
+    kind: the medium's NdfKind (BECKMANN media count the cheaper NDF)."""
     f = s = 0.0
     for ev, (cf, cs) in (PLANAR_EVENTS if planar else EVENTS).items():
         n = float(stats.get(ev, 0))
         f += n * cf
         s += n * cs
+    if kind is not None and getattr(kind, "value", kind) == "beckmann":
+        n = float(stats.get("nee", 0)) + float(stats.get("scatters", 0))
+        f -= n * _BECK_DIFF[0]
+        s -= n * _BECK_DIFF[1]
     return f, s
 
 
-def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, planar=False):
-    """Achieved issue rates and the roofline fraction of the path kernel."""
-    f, s = algorithmic_ops(stats, planar)
+def from_ops(f, s, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, paths=1):
+    """Achieved issue rates and the roofline fraction for f / s algorithmic
+    lane ops executed in kernel_ms."""
     t = kernel_ms * 1e-3
     af = f / t / 1e9
     asf = s / t / 1e9
@@ -130,6 +146,12 @@ def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, planar=False):
         "frac": max(ff, fs),
         "fp32_frac": ff,
         "sfu_frac": fs,
-        "fp32_per_path": f / max(float(stats.get("paths", 1)), 1.0),
-        "sfu_per_path": s / max(float(stats.get("paths", 1)), 1.0),
+        "fp32_per_path": f / max(float(paths), 1.0),
+        "sfu_per_path": s / max(float(paths), 1.0),
     }
+
+
+def roofline(stats, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, planar=False, kind=None):
+    """Achieved issue rates and the roofline fraction of the path kernel."""
+    f, s = algorithmic_ops(stats, planar, kind)
+    return from_ops(f, s, kernel_ms, peak_fp32_ginst, peak_sfu_ginst, stats.get("paths", 1))
