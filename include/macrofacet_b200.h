@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MF_ABI_VERSION 1
+#define MF_ABI_VERSION 2
 
 enum mf_status {
   MF_OK = 0,
@@ -61,17 +61,18 @@ typedef struct mf_medium {
   double albedo[3];
 } mf_medium;
 
-/* SDF primitives (sdf.py:18-52); MF_SHAPE_GRID is the BASELINE config-5
+/* SDF primitives (sdf.py:18-84); MF_SHAPE_GRID is the BASELINE config-5
  * extension: the scene's mf_grid_field (trilinear SDF + per-voxel sigma) */
-enum mf_shape { MF_SHAPE_PLANE = 0, MF_SHAPE_SPHERE = 1, MF_SHAPE_GRID = 2 };
+enum mf_shape { MF_SHAPE_PLANE = 0, MF_SHAPE_SPHERE = 1, MF_SHAPE_GRID = 2, MF_SHAPE_BOX = 3 };
 
 /* ShellPrimitive (scene.py:99-101): one shape bound to media[medium] */
 typedef struct mf_primitive {
   int32_t shape;
   int32_t medium;
-  double z0;         /* plane z = z0, outside above */
-  double center[3];  /* sphere */
-  double radius;
+  double z0;              /* plane z = z0, outside above */
+  double center[3];       /* sphere, box */
+  double radius;          /* sphere */
+  double half_extents[3]; /* box (sdf.py:55-84) */
 } mf_primitive;
 
 /* Camera (scene.py:19-51); ortho != 0 selects the orthographic extension:
@@ -114,6 +115,11 @@ typedef struct mf_scene {
   mf_medium media[MF_MAX_MEDIA];
   mf_camera camera;
   double env[3]; /* constant environment radiance (scene.py:54-84) */
+  /* lat-long environment map (Environment.latlong, scene.py:61-84): device
+   * float32 (env_height, env_width, 3), theta down the rows, bilinear with
+   * wrapped phi; NULL = the constant env above */
+  const float* d_env_map;
+  int32_t env_width, env_height;
   int32_t has_sun;
   double sun_dir[3];
   double sun_radiance[3];
@@ -199,8 +205,13 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
  * holding radiance / spp for this rank's share (render.py:127-180).
  * Non-owned pixels (tile sharding) are left untouched (overwrite mode
  * writes +0.0 there), so a sum-reduce over ranks is exact.
- * If stats != NULL the call synchronises the stream and fills it, and
- * majorant violations / non-finite radiance turn into error statuses.
+ * The render kernels sum each pixel's paths in 64-bit fixed point (order
+ * independent: the image is bit-identical for any launch geometry or tile
+ * split).  The call synchronises the stream once at the end and always
+ * validates: majorant violations, walker caps and non-finite / negative /
+ * out-of-range radiance turn into error statuses (render() validates,
+ * image.py:38-42).  stats (may be NULL) receives the event counters and
+ * the path kernels' CUDA-event time.
  */
 int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
               mf_stats* stats, void* stream);
@@ -212,6 +223,24 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
                    const uint32_t* d_pixel, const uint32_t* d_sample, uint64_t seed,
                    int32_t max_bounces, int64_t n, float* d_radiance, mf_stats* stats,
                    void* stream);
+
+/* walk(scene, pos, direction, rng, mode, active) (transport.py:144-297) and
+ * sample_collision(ray, scene, rng) (transport.py:316-416) for caller-given
+ * rays: d_org / d_dir SoA float32 [3][n]; ray i draws from Philox keyed by
+ * `seed` with counter (d_pixel[i], d_sample[i], segment, call).
+ *   mode MF_WALK_COLLISION  delta tracking to a real collision, escape, or
+ *                           absorption below -6 sigma
+ *   mode MF_WALK_RATIO      ratio tracking of the transmittance (|f| <= 3 sigma)
+ *   mode MF_WALK_TENTATIVE  stop at the first tentative collision
+ * Outputs (any may be NULL): d_state int8 (0 escaped, 1 absorbed, 2 real
+ * collision, 3 null collision), d_pos SoA [3][n], d_travel, d_weight,
+ * d_prim (int32, -1 when none).  Majorant violations / iteration caps
+ * raise (transport.py:264-268,297). */
+enum mf_walk_mode { MF_WALK_COLLISION = 0, MF_WALK_RATIO = 1, MF_WALK_TENTATIVE = 2 };
+int mf_walk(const mf_scene* scene, const float* d_org, const float* d_dir,
+            const uint32_t* d_pixel, const uint32_t* d_sample, uint64_t seed, uint32_t segment,
+            int32_t mode, int64_t n, int8_t* d_state, float* d_pos, float* d_travel,
+            float* d_weight, int32_t* d_prim, mf_stats* stats, void* stream);
 
 /* transmittance_estimate(ray, scene, n, rng) (transport.py:300-313):
  * ratio-tracking mean and standard error over n samples (host results). */

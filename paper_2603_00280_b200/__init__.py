@@ -19,8 +19,8 @@ from .medium import (MacrofacetMedium, extinction, phase_eval, phase_pdf, phase_
                      query_batch)
 from .ndf import KernelParams, NdfKind, RoughnessTriple, roughness_from_kernel
 from .render import PathKeys, render, render_device, render_sharded, trace_path, trace_paths
-from .rng import RandomStream
+from .rng import BatchRng, RandomStream, derive_bases, stream_base
 from .scene import (Camera, DirectionalLight, Environment, PointLight, ShellPrimitive,
                     ShellScene)
-from .sdf import Plane, Sphere
-from .transport import transmittance_estimate
+from .sdf import Box, Plane, Sphere
+from .transport import EventKind, MediumEvent, sample_collision, transmittance_estimate, walk

@@ -27,7 +27,9 @@ REDUCE_NCCL, REDUCE_ORDERED = 0, 1
 CURVE = {"lambda": 0, "projected-area": 1, "ndf": 2, "vndf": 3, "transmittance": 4}
 COMM_ID_BYTES = 128
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
-SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID = 0, 1, 2
+SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID, SHAPE_BOX = 0, 1, 2, 3
+WALK_COLLISION, WALK_RATIO, WALK_TENTATIVE = 0, 1, 2
+ABI_VERSION = 2
 SHARD_TILES, SHARD_SAMPLES = 0, 1
 
 _d3 = ctypes.c_double * 3
@@ -42,7 +44,7 @@ class MfMedium(ctypes.Structure):
 
 class MfPrimitive(ctypes.Structure):
     _fields_ = [("shape", ctypes.c_int32), ("medium", ctypes.c_int32), ("z0", ctypes.c_double),
-                ("center", _d3), ("radius", ctypes.c_double)]
+                ("center", _d3), ("radius", ctypes.c_double), ("half_extents", _d3)]
 
 
 class MfCamera(ctypes.Structure):
@@ -62,6 +64,8 @@ class MfScene(ctypes.Structure):
     _fields_ = [("n_prims", ctypes.c_int32), ("n_media", ctypes.c_int32),
                 ("prims", MfPrimitive * MF_MAX_PRIMS), ("media", MfMedium * MF_MAX_MEDIA),
                 ("camera", MfCamera), ("env", _d3),
+                ("d_env_map", ctypes.c_void_p), ("env_width", ctypes.c_int32),
+                ("env_height", ctypes.c_int32),
                 ("has_sun", ctypes.c_int32), ("sun_dir", _d3), ("sun_radiance", _d3),
                 ("has_point", ctypes.c_int32), ("point_pos", _d3), ("point_intensity", _d3),
                 ("has_grid", ctypes.c_int32), ("grid", MfGridField)]
@@ -110,6 +114,9 @@ SIGNATURES = {
     "mf_trace_paths": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp,
                                       ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, _vp,
                                       ctypes.POINTER(MfStats), _vp]),
+    "mf_walk": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp, ctypes.c_uint64,
+                               ctypes.c_uint32, ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp,
+                               _vp, _vp, ctypes.POINTER(MfStats), _vp]),
     "mf_transmittance": (ctypes.c_int, [ctypes.POINTER(MfScene), ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                         ctypes.c_uint64, ctypes.c_uint64,
@@ -149,7 +156,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.mf_abi_version() != 1:
+        if lib.mf_abi_version() != ABI_VERSION:
             raise MacrofacetError("libmacrofacet_b200 ABI version mismatch")
         _lib = lib
         return lib

@@ -470,7 +470,8 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& 
     outcome = w.steps < 0 ? -1 : w.outcome;
   }
   if (outcome == kEscaped) {
-    st.L = add3(st.L, v3(st.T.x * sc.env.x, st.T.y * sc.env.y, st.T.z * sc.env.z));
+    V3 e = env_radiance(sc, st.dir);   // render.py:54-57
+    st.L = add3(st.L, v3(st.T.x * e.x, st.T.y * e.y, st.T.z * e.z));
     cn.v[kStEscaped]++;
     return false;
   }
@@ -1086,6 +1087,96 @@ __global__ void __launch_bounds__(kBlock) ratio_kernel(const __grid_constant__ S
   }
 }
 
+// walk() / sample_collision() for caller-given rays (transport.py:144-297,
+// 316-416): one thread per ray, the tracking walker (grid walker for grid
+// fields) on the ray's own Philox stream
+struct WalkArgs {
+  const float *org, *dir;
+  const uint32_t *pix, *smp;
+  uint32_t k0, k1, segment;
+  int mode;
+  uint32_t n;
+  int8_t* state;
+  float *pos, *travel, *weight;
+  int32_t* prim;
+  unsigned long long* stats;
+};
+
+__global__ void __launch_bounds__(kBlock) walk_kernel(const __grid_constant__ SceneDev sc,
+                                                       const __grid_constant__ WalkArgs a) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t steps = 0, viol = 0, capped = 0;
+  if (i < a.n) {
+    PathRng rng{a.k0, a.k1, a.pix[i], a.smp[i]};
+    V3 o = v3(a.org[i], a.org[a.n + i], a.org[2u * a.n + i]);
+    V3 d = v3(a.dir[i], a.dir[a.n + i], a.dir[2u * a.n + i]);
+    bool ratio = a.mode == MF_WALK_RATIO;
+    uint32_t call0 = ratio ? kCallShadow : 1u;
+    int outcome, prim = -1;
+    V3 pos;
+    float weight, travel;
+    if (sc.has_grid) {
+      GridWalk w = grid_walk_path(sc.grid, sc.media[0], rng, a.segment, call0, o, d, ratio,
+                                  INFINITY, 0.0f);
+      outcome = w.steps < 0 ? kAbsorbed : w.outcome;
+      prim = outcome == kCollided ? 0 : -1;
+      pos = w.pos;
+      weight = w.weight;
+      travel = dot3(sub3(w.pos, o), d);
+      steps = (uint32_t)max(w.steps, 0);
+      viol = (uint32_t)w.violations;
+      capped = w.steps < 0 ? 1u : 0u;
+    } else {
+      WalkResult w = walk(sc, rng, a.segment, call0, o, d, ratio, INFINITY, 0.0f,
+                          a.mode == MF_WALK_TENTATIVE);
+      outcome = w.outcome;
+      prim = (outcome == kCollided || outcome == kNullCollision) ? w.prim : -1;
+      pos = w.pos;
+      weight = w.weight;
+      travel = w.travel;
+      steps = (uint32_t)max(w.steps, 0);
+      viol = (uint32_t)w.violations;
+      capped = w.steps < 0 ? 1u : 0u;
+    }
+    if (a.state) a.state[i] = (int8_t)outcome;
+    if (a.pos) {
+      a.pos[i] = pos.x;
+      a.pos[a.n + i] = pos.y;
+      a.pos[2u * a.n + i] = pos.z;
+    }
+    if (a.travel) a.travel[i] = travel;
+    if (a.weight) a.weight[i] = weight;
+    if (a.prim) a.prim[i] = prim;
+  }
+  unsigned s0 = __reduce_add_sync(0xffffffffu, steps);
+  unsigned s1 = __reduce_add_sync(0xffffffffu, viol);
+  unsigned s2 = __reduce_add_sync(0xffffffffu, capped);
+  unsigned s3 = __reduce_add_sync(0xffffffffu, i < a.n ? 1u : 0u);
+  if ((threadIdx.x & 31) == 0) {
+    if (s0) atomicAdd(a.stats + kStTrackSteps, (unsigned long long)s0);
+    if (s1) atomicAdd(a.stats + kStViolations, (unsigned long long)s1);
+    if (s2) atomicAdd(a.stats + kStCapped, (unsigned long long)s2);
+    if (s3) atomicAdd(a.stats + kStPaths, (unsigned long long)s3);
+  }
+}
+
+// largest value of a lat-long environment map (the fixed-point scale of a
+// render must cover it); non-negative floats order like their bit patterns
+__global__ void __launch_bounds__(256) env_max_kernel(const float* m, size_t n, unsigned* out) {
+  float v = 0.0f;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float x = __ldg(m + i);
+    v = (x == x) ? fmaxf(v, fabsf(x)) : INFINITY;
+  }
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(v));
+}
+
 // ---------------------------------------------------------------------------
 // visible-slope guess table (built once per device by the solver itself)
 
@@ -1333,7 +1424,12 @@ int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaSt
   // (MF_GENERIC_WALK=1: the general walker for it, for the equality test)
   const char* gw = std::getenv("MF_GENERIC_WALK");
   bool generic = gw && gw[0] == '1';
-  int mode = sc.has_grid ? 2 : (sc.single_plane ? 0 : (sc.n_prims == 1 && !generic ? 3 : 1));
+  int mode = sc.has_grid ? 2
+                         : (sc.single_plane ? 0
+                                            : (sc.n_prims == 1 && sc.prims[0].shape == kShapeSphere &&
+                                                       !generic
+                                                   ? 3
+                                                   : 1));
   int grid = occ.sms * (mode == 3 ? occ.blocks[caller_rays ? 15 : 14]
                                   : occ.blocks[mode + (caller_rays ? 3 : 0)]);
   int64_t need = ((int64_t)ps.n_paths + kBlock - 1) / kBlock;
@@ -1656,7 +1752,26 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   ps.counter = scr.counter;
   ps.stats = scr.stats;
   int k = 0;
-  fx_scale(scene_emax(sc), s_count, &ps.fx_scale, &ps.fx_limit, &k);
+  double emax = scene_emax(sc);
+  if (sc.env_map) {
+    size_t nm = (size_t)sc.env_w * sc.env_h * 3;
+    MF_CUDA(cudaMemsetAsync(scr.counter + 32, 0, sizeof(unsigned), st));
+    env_max_kernel<<<(unsigned)std::min<size_t>((nm + 255) / 256, 1024), 256, 0, st>>>(
+        sc.env_map, nm, scr.counter + 32);
+    g_launches++;
+    MF_CUDA(cudaGetLastError());
+    unsigned bits = 0;
+    MF_CUDA(cudaMemcpyAsync(&bits, scr.counter + 32, sizeof(bits), cudaMemcpyDeviceToHost, st));
+    MF_CUDA(cudaStreamSynchronize(st));
+    float mx;
+    std::memcpy(&mx, &bits, sizeof(mx));
+    if (!std::isfinite(mx)) {
+      scratch_free(&scr, st);
+      return fail(MF_ERR_PARAM, "environment map holds non-finite values");
+    }
+    emax = std::max(emax, (double)mx);
+  }
+  fx_scale(emax, s_count, &ps.fx_scale, &ps.fx_limit, &k);
   // path-kernel timing: one event pair per launch, read after the final sync
   std::vector<cudaEvent_t> ev;
   double kernel_ms = 0.0;
@@ -1758,6 +1873,61 @@ int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir
   }
   int rc2 = scratch_free(&scr, st);
   return out ? out : rc2;
+}
+
+int mf_walk(const mf_scene* scene, const float* d_org, const float* d_dir,
+            const uint32_t* d_pixel, const uint32_t* d_sample, uint64_t seed, uint32_t segment,
+            int32_t mode, int64_t n, int8_t* d_state, float* d_pos, float* d_travel,
+            float* d_weight, int32_t* d_prim, mf_stats* stats, void* stream) {
+  if (!scene || (n > 0 && (!d_org || !d_dir || !d_pixel || !d_sample)))
+    return fail(MF_ERR_PARAM, "null argument");
+  if (mode != MF_WALK_COLLISION && mode != MF_WALK_RATIO && mode != MF_WALK_TENTATIVE)
+    return fail(MF_ERR_PARAM, "mode must be collision, ratio or tentative");
+  if (n < 0 || n > 0x7fffffffll) return fail(MF_ERR_PARAM, "n out of range");
+  SceneDev sc;
+  std::string berr;
+  int rc = build_scene(*scene, &sc, &berr);
+  if (rc) return fail(rc, berr);
+  if (mode == MF_WALK_TENTATIVE && sc.has_grid)
+    return fail(MF_ERR_UNSUPPORTED, "sample_collision is not available for grid fields");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (n == 0) return MF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* stt = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&stt, kStCount * sizeof(unsigned long long), st));
+  MF_CUDA(cudaMemsetAsync(stt, 0, kStCount * sizeof(unsigned long long), st));
+  WalkArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.org = d_org;
+  a.dir = d_dir;
+  a.pix = d_pixel;
+  a.smp = d_sample;
+  a.k0 = (uint32_t)(seed & 0xffffffffu);
+  a.k1 = (uint32_t)(seed >> 32);
+  a.segment = segment;
+  a.mode = mode;
+  a.n = (uint32_t)n;
+  a.state = d_state;
+  a.pos = d_pos;
+  a.travel = d_travel;
+  a.weight = d_weight;
+  a.prim = d_prim;
+  a.stats = stt;
+  walk_kernel<<<(uint32_t)((n + kBlock - 1) / kBlock), kBlock, 0, st>>>(sc, a);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  unsigned long long h[kStCount];
+  MF_CUDA(cudaMemcpyAsync(h, stt, sizeof(h), cudaMemcpyDeviceToHost, st));
+  MF_CUDA(cudaFreeAsync(stt, st));
+  MF_CUDA(cudaStreamSynchronize(st));
+  mf_stats local;
+  mf_stats& o = stats ? *stats : local;
+  fill_stats(h, &o);
+  if (o.majorant_violations)
+    return fail(MF_ERR_MAJORANT, "extinction exceeded its majorant (" +
+                                     std::to_string(o.majorant_violations) + " events)");
+  if (o.capped) return fail(MF_ERR_CAP, "walker exceeded its iteration cap");
+  return MF_OK;
 }
 
 int mf_transmittance(const mf_scene* scene, const double origin[3], const double direction[3],

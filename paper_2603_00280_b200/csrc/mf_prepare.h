@@ -88,10 +88,12 @@ struct PrimK {
   int medium;
   float z0;
   float cx, cy, cz, radius;
+  float hx, hy, hz;
 };
 
 inline int prepare_primitive(const mf_primitive& in, int n_media, PrimK* out, std::string* err) {
-  if (in.shape != MF_SHAPE_PLANE && in.shape != MF_SHAPE_SPHERE && in.shape != MF_SHAPE_GRID) {
+  if (in.shape != MF_SHAPE_PLANE && in.shape != MF_SHAPE_SPHERE && in.shape != MF_SHAPE_GRID &&
+      in.shape != MF_SHAPE_BOX) {
     *err = "unsupported primitive shape " + std::to_string(in.shape);
     return MF_ERR_UNSUPPORTED;
   }
@@ -103,8 +105,17 @@ inline int prepare_primitive(const mf_primitive& in, int n_media, PrimK* out, st
     *err = "sphere radius must be > 0, got " + std::to_string(in.radius);
     return MF_ERR_PARAM;
   }
+  if (in.shape == MF_SHAPE_BOX &&
+      !(finite_pos(in.half_extents[0]) && finite_pos(in.half_extents[1]) &&
+        finite_pos(in.half_extents[2]))) {
+    *err = "box half extents must be > 0";   // sdf.py:61-62
+    return MF_ERR_PARAM;
+  }
   PrimK p{};
   p.shape = in.shape;
+  p.hx = (float)in.half_extents[0];
+  p.hy = (float)in.half_extents[1];
+  p.hz = (float)in.half_extents[2];
   p.medium = in.medium;
   p.z0 = (float)in.z0;
   p.cx = (float)in.center[0];

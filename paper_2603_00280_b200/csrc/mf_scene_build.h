@@ -95,6 +95,7 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     sc.prims[j].z0 = pk.z0;
     sc.prims[j].c = v3(pk.cx, pk.cy, pk.cz);
     sc.prims[j].radius = pk.radius;
+    sc.prims[j].half = v3(pk.hx, pk.hy, pk.hz);
     sc.media[j] = mk;
     double s = in.media[pk.medium].sigma;
     min_sigma = std::min(min_sigma, s);
@@ -182,6 +183,11 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
   sc.half_h = (float)hh;
   sc.half_w = (float)(hh * cam.width / cam.height);
   sc.env = v3((float)in.env[0], (float)in.env[1], (float)in.env[2]);
+  sc.env_map = in.d_env_map;
+  sc.env_w = in.env_width;
+  sc.env_h = in.env_height;
+  if (sc.env_map && (sc.env_w < 1 || sc.env_h < 1))
+    return (*err = std::string("environment map size must be >= 1 x 1"), MF_ERR_PARAM);
   sc.has_sun = in.has_sun;
   if (in.has_sun) {
     double d[3] = {in.sun_dir[0], in.sun_dir[1], in.sun_dir[2]};
@@ -207,8 +213,7 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
     for (int j = 0; j < in.n_prims; ++j) {
       const PrimDev& p = sc.prims[j];
       V3 lp = sc.point_pos;
-      float fv = p.shape == 0 ? lp.z - p.z0
-                              : std::sqrt(dot3(sub3(lp, p.c), sub3(lp, p.c))) - p.radius;
+      float fv = prim_field(p, lp);
       if (!(fv > 3.0f * sc.media[j].sigma))
         return (*err = std::string("point light inside a shell is not supported"), MF_ERR_UNSUPPORTED);
     }
@@ -223,7 +228,8 @@ inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
              (m.fresnel == kAlbedo && m.albedo[0] == m.albedo[1] && m.albedo[1] == m.albedo[2]);
     if (!g) sc.mono = 0;
   }
-  if (!grey(sc.env) || (sc.has_sun && !grey(sc.sun_L)) || (sc.has_point && !grey(sc.point_I)))
+  if (!grey(sc.env) || (sc.has_sun && !grey(sc.sun_L)) || (sc.has_point && !grey(sc.point_I)) ||
+      sc.env_map)
     sc.mono = 0;
   *out = sc;
   return MF_OK;

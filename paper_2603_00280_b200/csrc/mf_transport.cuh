@@ -31,12 +31,15 @@ constexpr int kMaxPrims = 8;
 #endif
 
 struct PrimDev {
-  int shape;   // 0 plane, 1 sphere
+  int shape;   // 0 plane, 1 sphere, 3 box (MF_SHAPE_*)
   int medium;
   float z0;
   V3 c;
   float radius;
+  V3 half;     // box half extents
 };
+
+constexpr int kShapePlane = 0, kShapeSphere = 1, kShapeBox = 3;
 
 // Tracking-step length inside a band, in units of the medium's sigma.  The
 // per-step majorant is exact over [0, step] whatever the length; shorter
@@ -67,6 +70,10 @@ struct SceneDev {
   V3 cam_pos, cam_fwd, cam_right, cam_up;
   float half_w, half_h;
   V3 env;
+  // lat-long environment map (scene.py:61-84): (env_h, env_w, 3) float32,
+  // theta down the rows; nullptr = the constant env
+  const float* env_map;
+  int env_w, env_h;
   int has_sun;
   V3 sun_to;           // unit direction towards the sun (= -DirectionalLight.direction)
   V3 sun_L;
@@ -82,6 +89,38 @@ struct SceneDev {
   int has_grid;        // 1: the single primitive is the grid field below
   GridDev grid;
 };
+
+// Environment radiance of an escaping direction d (scene.py:61-84): the
+// constant, or the lat-long map bilinear in (phi, theta) with phi wrapped
+// and theta clamped, texel centres at half-integers -- the reference's
+// formula in float32.
+MF_HD V3 env_radiance(const SceneDev& sc, V3 d) {
+  if (!sc.env_map) return sc.env;
+  const float kPi = 3.14159265358979f;
+  float th = acosf(fminf(fmaxf(d.z, -1.0f), 1.0f));
+  float ph = atan2f(d.y, d.x);
+  if (ph < 0.0f) ph += 2.0f * kPi;
+  int w = sc.env_w, h = sc.env_h;
+  float fx = ph / (2.0f * kPi) * (float)w - 0.5f;
+  float fy = th / kPi * (float)h - 0.5f;
+  float x0f = floorf(fx), y0f = floorf(fy);
+  float tx = fx - x0f, ty = fy - y0f;
+  int x0 = (int)x0f, y0 = (int)y0f;
+  int x0m = ((x0 % w) + w) % w, x1m = (((x0 + 1) % w) + w) % w;
+  int y0m = clampi(y0, 0, h - 1), y1m = clampi(y0 + 1, 0, h - 1);
+  const float* m = sc.env_map;
+  float w00 = (1.0f - tx) * (1.0f - ty), w01 = tx * (1.0f - ty), w10 = (1.0f - tx) * ty,
+        w11 = tx * ty;
+  float c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c[k] = ldg(m + ((size_t)y0m * w + x0m) * 3 + k) * w00 +
+           ldg(m + ((size_t)y0m * w + x1m) * 3 + k) * w01 +
+           ldg(m + ((size_t)y1m * w + x0m) * 3 + k) * w10 +
+           ldg(m + ((size_t)y1m * w + x1m) * 3 + k) * w11;
+  }
+  return v3(c[0], c[1], c[2]);
+}
 
 // ---------------------------------------------------------------------------
 // counter-based random stream of one path: key = seed, counter =
@@ -105,16 +144,42 @@ constexpr uint32_t kCallShadow = 0x80000000u;
 // fields
 
 // kSphere: the primitive is known to be a sphere (single-sphere walker)
+// box SDF and gradient (sdf.py:55-84): exact distance outside, max of the
+// per-axis distances inside; inside, the gradient is the axis of the
+// nearest face (first on ties, as numpy's argmax)
+MF_HD float box_field(const PrimDev& p, V3 x) {
+  float qx = fabsf(x.x - p.c.x) - p.half.x, qy = fabsf(x.y - p.c.y) - p.half.y,
+        qz = fabsf(x.z - p.c.z) - p.half.z;
+  float ox = fmaxf(qx, 0.0f), oy = fmaxf(qy, 0.0f), oz = fmaxf(qz, 0.0f);
+  return fsqrt(ox * ox + oy * oy + oz * oz) + fminf(fmaxf(qx, fmaxf(qy, qz)), 0.0f);
+}
+
+MF_HD V3 box_normal(const PrimDev& p, V3 x) {
+  V3 d = sub3(x, p.c);
+  float qx = fabsf(d.x) - p.half.x, qy = fabsf(d.y) - p.half.y, qz = fabsf(d.z) - p.half.z;
+  float ox = fmaxf(qx, 0.0f), oy = fmaxf(qy, 0.0f), oz = fmaxf(qz, 0.0f);
+  float on2 = ox * ox + oy * oy + oz * oz;
+  if (on2 > 0.0f) {
+    float inv = frsqrt(on2);
+    return v3(copysignf(ox * inv, d.x), copysignf(oy * inv, d.y), copysignf(oz * inv, d.z));
+  }
+  if (qx >= qy && qx >= qz) return v3(d.x >= 0.0f ? 1.0f : -1.0f, 0.0f, 0.0f);
+  if (qy >= qz) return v3(0.0f, d.y >= 0.0f ? 1.0f : -1.0f, 0.0f);
+  return v3(0.0f, 0.0f, d.z >= 0.0f ? 1.0f : -1.0f);
+}
+
 template <bool kSphere = false>
 MF_HD float prim_field(const PrimDev& p, V3 x) {
-  if (!kSphere && p.shape == 0) return x.z - p.z0;
+  if (!kSphere && p.shape == kShapePlane) return x.z - p.z0;
+  if (!kSphere && p.shape == kShapeBox) return box_field(p, x);
   V3 d = sub3(x, p.c);
   return fsqrt(dot3(d, d)) - p.radius;
 }
 
 template <bool kSphere = false>
 MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
-  if (!kSphere && p.shape == 0) return v3(0.0f, 0.0f, 1.0f);
+  if (!kSphere && p.shape == kShapePlane) return v3(0.0f, 0.0f, 1.0f);
+  if (!kSphere && p.shape == kShapeBox) return box_normal(p, x);
   V3 d = sub3(x, p.c);
   float r2 = dot3(d, d);
   return r2 > 0.0f ? mul3(d, frsqrt(r2)) : v3(0.0f, 0.0f, 1.0f);
@@ -128,9 +193,17 @@ MF_HD V3 prim_normal(const PrimDev& p, V3 x) {
 // far side.
 template <bool kSphere = false>
 MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
-  if (!kSphere && p.shape == 0) {
+  if (!kSphere && p.shape == kShapePlane) {
     float t = (level - (pos.z - p.z0)) / dir.z;
     return (t >= 0.0f && t < INFINITY) ? t : INFINITY;
+  }
+  if (!kSphere && p.shape == kShapeBox) {
+    // 1-Lipschitz lower bound |f - level| (transport.py:93), and the recede
+    // test (transport.py:105-108): above the level and moving along the
+    // gradient, the convex exterior never brings the level back
+    float f = box_field(p, pos);
+    if (f > level && dot3(box_normal(p, pos), dir) >= 0.0f) return INFINITY;
+    return fabsf(f - level);
   }
   float rad = p.radius + level;
   if (!(rad > 0.0f)) return INFINITY;
@@ -150,7 +223,7 @@ MF_HD float level_distance(const PrimDev& p, V3 pos, V3 dir, float level) {
 // ---------------------------------------------------------------------------
 // analytic planar free flight (single plane)
 
-enum FlightOutcome : int { kEscaped = 0, kAbsorbed = 1, kCollided = 2 };
+enum FlightOutcome : int { kEscaped = 0, kAbsorbed = 1, kCollided = 2, kNullCollision = 3 };
 
 struct Flight {
   int outcome;
@@ -312,6 +385,7 @@ struct WalkResult {
   float weight;   // ratio tracking transmittance
   int steps;
   int violations;
+  float travel;   // distance walked
 };
 
 // Extinction of prim j at x along dir (local frame), 0 outside its region.
@@ -358,10 +432,11 @@ struct WalkState {
   int outcome, prim;
   V3 pos;        // final position
   bool ratio;
+  bool tentative;   // stop at the first tentative collision (sample_collision)
 };
 
 MF_HD void walk_begin(WalkState& w, V3 pos, V3 dir, bool ratio, float t_max, uint32_t call0,
-                      float rr_min) {
+                      float rr_min, bool tentative = false) {
   w.p = pos;
   w.dir = dir;
   w.travel = 0.0f;
@@ -378,6 +453,7 @@ MF_HD void walk_begin(WalkState& w, V3 pos, V3 dir, bool ratio, float t_max, uin
   w.prim = -1;
   w.pos = pos;
   w.ratio = ratio;
+  w.tentative = tentative;
 }
 
 // One iteration of the delta / ratio tracking loop (transport.py:196-297);
@@ -408,7 +484,9 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
     }
     if (f >= lo && f <= hi) {
       any_band = true;
-      cap = fminf(cap, MF_STEP_FRAC * m.sigma);
+      // boxes bound f only by its Lipschitz constant: the reference's
+      // sigma / 2 steps (transport.py:163) keep that band majorant tight
+      cap = fminf(cap, (!kOne && p.shape == kShapeBox ? 0.5f : MF_STEP_FRAC) * m.sigma);
     } else {
       float g = level_distance<kOne>(p, w.p, w.dir, f > hi ? hi : lo);
       gap_min = fminf(gap_min, g);
@@ -427,9 +505,14 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
     float lo = w.lo_mult * m.sigma, hi = 3.0f * m.sigma;
     if (!(f >= lo && f <= hi)) continue;
     float fmin, dirf;
-    if (!kOne && p.shape == 0) {
+    if (!kOne && p.shape == kShapePlane) {
       fmin = f + cap * fminf(w.dir.z, 0.0f);
       dirf = proj_area_outlined(m.kind, m.ax, m.ay, m.az, w.dir);
+    } else if (!kOne && p.shape == kShapeBox) {
+      // 1-Lipschitz field, curved frame: the moving band (transport.py:
+      // 226-231) with the exact direction maximum
+      fmin = f - cap;
+      dirf = sc.mx[j].sig_max;
     } else {
       V3 oc = sub3(w.p, p.c);
       float b = dot3(oc, w.dir);
@@ -537,6 +620,17 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
       w.pos = w.p;
       return true;
     }
+    if (w.tentative) {
+      // a null collision ends a sample_collision walk (transport.py:
+      // 397-415): the primitive of the largest extinction part
+      int k = 0;
+      for (int j = 1; j < n_prims; ++j)
+        if (parts[j] > parts[k]) k = j;
+      w.outcome = kNullCollision;
+      w.prim = k;
+      w.pos = w.p;
+      return true;
+    }
   }
   return false;   // null collision: the walk goes on
 }
@@ -544,9 +638,9 @@ MF_HD bool walk_step(const SceneDev& sc, const PathRng& rng, uint32_t segment, W
 template <bool kOne = false>
 MF_WALK_FN WalkResult walk(const SceneDev& sc, PathRng rng, uint32_t segment,
                            uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
-                           float rr_min = 0.0f) {
+                           float rr_min = 0.0f, bool tentative = false) {
   WalkState s;
-  walk_begin(s, pos, dir, ratio, t_max, call0, rr_min);
+  walk_begin(s, pos, dir, ratio, t_max, call0, rr_min, tentative);
   WalkResult w;
   for (int iter = 0; iter < 1000000; ++iter) {
     if (walk_step<kOne>(sc, rng, segment, s)) {
@@ -556,6 +650,7 @@ MF_WALK_FN WalkResult walk(const SceneDev& sc, PathRng rng, uint32_t segment,
       w.weight = s.weight;
       w.steps = s.steps;
       w.violations = s.violations;
+      w.travel = s.travel;
       return w;
     }
   }
@@ -565,6 +660,7 @@ MF_WALK_FN WalkResult walk(const SceneDev& sc, PathRng rng, uint32_t segment,
   w.weight = s.weight;
   w.steps = -1;
   w.violations = s.violations;
+  w.travel = s.travel;
   return w;
 }
 

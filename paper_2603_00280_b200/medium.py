@@ -75,21 +75,29 @@ class MacrofacetMedium:
         return 3.0 * self.sigma
 
 
-def to_c_medium(m: MacrofacetMedium) -> _lib.MfMedium:
+def to_c_medium(m) -> _lib.MfMedium:
+    """Flatten a medium -- this package's MacrofacetMedium or the
+    reference's (read by attribute: kind, a3, sigma, fresnel_eta,
+    fresnel_k, mix_ratio, fresnel_one; `albedo` is the BASELINE extension
+    and defaults to None)."""
     c = _lib.MfMedium()
-    c.kind = _lib.KIND[m.kind.value]
-    if m.albedo is not None:
+    kind = getattr(m.kind, "value", m.kind)
+    if kind not in _lib.KIND:
+        raise ParameterDomainError(f"unknown NDF kind {m.kind!r}")
+    c.kind = _lib.KIND[kind]
+    albedo = getattr(m, "albedo", None)
+    if albedo is not None:
         c.fresnel = _lib.FRESNEL_ALBEDO
-        c.albedo[:] = m.albedo
-    elif m.fresnel_one:
+        c.albedo[:] = tuple(float(v) for v in np.broadcast_to(albedo, (3,)))
+    elif getattr(m, "fresnel_one", False):
         c.fresnel = _lib.FRESNEL_ONE
     else:
         c.fresnel = _lib.FRESNEL_CONDUCTOR
     c.ax, c.ay, c.az = float(m.a3.ax), float(m.a3.ay), float(m.a3.az)
     c.sigma = float(m.sigma)
-    c.mix_ratio = float(m.mix_ratio)
-    c.eta[:] = m.fresnel_eta
-    c.k[:] = m.fresnel_k
+    c.mix_ratio = float(getattr(m, "mix_ratio", 0.5))
+    c.eta[:] = tuple(float(v) for v in getattr(m, "fresnel_eta", DEFAULT_ETA))
+    c.k[:] = tuple(float(v) for v in getattr(m, "fresnel_k", DEFAULT_K))
     return c
 
 

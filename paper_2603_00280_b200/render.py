@@ -60,7 +60,7 @@ def _c_scene(scene: ShellScene, device):
     return cs
 
 
-def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
+def render_device(scene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
                   shard="tiles", out=None, stats=False, stream=None, c_scene=None):
     """Render into a (H, W, 3) float32 CUDA tensor holding radiance / spp for
     this rank's share.  Returns (tensor, stats dict or None)."""
@@ -81,7 +81,7 @@ def render_device(scene: ShellScene, spp, seed, max_bounces=64, tile=32, rank=0,
     return out, (st.as_dict() if st is not None else None)
 
 
-def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, scene_hash=""):
+def render(scene, spp, seed, max_bounces=64, threads=None, tile=32, scene_hash=""):
     """Render the scene camera (render.py:127-180); `threads` is accepted for
     signature compatibility and ignored (the GPU path is deterministic for
     any launch geometry)."""
@@ -103,7 +103,7 @@ def render(scene: ShellScene, spp, seed, max_bounces=64, threads=None, tile=32, 
                          meta={"seed": int(seed), "spp": int(spp), "scene_hash": scene_hash})
 
 
-def render_sharded(scene: ShellScene, spp, seed, max_bounces=64, tile=32, shard="tiles",
+def render_sharded(scene, spp, seed, max_bounces=64, tile=32, shard="tiles",
                    group=None, stats=False, comm=None, ordered=False):
     """One rank's share of a multi-GPU render followed by a single NCCL
     sum-reduce of the fp32 accumulation buffers to rank 0.
@@ -169,35 +169,53 @@ class PathKeys:
     sample: np.ndarray
 
 
-def trace_paths(origins, directions, scene: ShellScene, max_bounces, keys: PathKeys,
-                return_stats=False):
-    """Trace caller-given rays to completion; returns (N, 3) radiance."""
+def _keys_of(brng, n):
+    """(seed, pixel, sample) of n paths from PathKeys or a BatchRng-like
+    object (`.base` / `.counter`, transport.py:52-67 -- the reference's own
+    BatchRng works); a BatchRng's counters advance by one per path."""
+    if isinstance(brng, PathKeys):
+        return (int(brng.seed), np.broadcast_to(np.asarray(brng.pixel, dtype=np.uint32), (n,)),
+                np.broadcast_to(np.asarray(brng.sample, dtype=np.uint32), (n,)))
+    if hasattr(brng, "base") and hasattr(brng, "counter"):
+        from .rng import BATCH_SEED, philox_keys
+
+        ctr = np.broadcast_to(np.asarray(brng.counter, dtype=np.uint64), (n,))
+        pix, smp = philox_keys(brng.base, ctr, n)
+        brng.counter = ctr + np.uint64(1)
+        return BATCH_SEED, pix, smp
+    raise ParameterDomainError("trace_paths needs a BatchRng (base, counter) or PathKeys")
+
+
+def trace_paths(origins, directions, scene, max_bounces, brng, return_stats=False):
+    """Trace caller-given rays to completion (render.py:32-108); returns
+    (N, 3) radiance.  `brng`: a BatchRng (reference signature; each path's
+    device stream is keyed by its (base, counter), which then advances by
+    one) or PathKeys (explicit (seed, pixel, sample) keys)."""
     if max_bounces < 1:
         raise ParameterDomainError(f"max_bounces must be >= 1, got {max_bounces}")
     torch = _lib.require_cuda()
     lib = _lib.load()
     o = np.asarray(origins, dtype=np.float64)
-    d = np.asarray(directions, dtype=np.float64)
     n = o.shape[0]
-    pix = np.broadcast_to(np.asarray(keys.pixel, dtype=np.uint32), (n,))
-    smp = np.broadcast_to(np.asarray(keys.sample, dtype=np.uint32), (n,))
+    d = np.broadcast_to(np.asarray(directions, dtype=np.float64), (n, 3))
+    seed, pix, smp = _keys_of(brng, n)
     dev = torch.device("cuda", torch.cuda.current_device())
     org_t = torch.from_numpy(np.ascontiguousarray(o.T, dtype=np.float32)).to(dev)
     dir_t = torch.from_numpy(np.ascontiguousarray(d.T, dtype=np.float32)).to(dev)
-    pix_t = torch.from_numpy(np.ascontiguousarray(pix).view(np.int32)).to(dev)
-    smp_t = torch.from_numpy(np.ascontiguousarray(smp).view(np.int32)).to(dev)
+    pix_t = torch.from_numpy(np.array(pix, dtype=np.uint32).view(np.int32)).to(dev)
+    smp_t = torch.from_numpy(np.array(smp, dtype=np.uint32).view(np.int32)).to(dev)
     rad = torch.empty((3, n), dtype=torch.float32, device=dev)
     cs = to_c_scene(scene)
     st = _lib.MfStats()
     _lib.check(lib.mf_trace_paths(ctypes.byref(cs), org_t.data_ptr(), dir_t.data_ptr(),
-                                  pix_t.data_ptr(), smp_t.data_ptr(), int(keys.seed) & (2**64 - 1),
+                                  pix_t.data_ptr(), smp_t.data_ptr(), int(seed) & (2**64 - 1),
                                   int(max_bounces), n, rad.data_ptr(), ctypes.byref(st),
                                   _lib.stream_handle(torch, dev)))
     out = rad.cpu().numpy().T.astype(np.float64)
     return (out, st.as_dict()) if return_stats else out
 
 
-def trace_path(ray, scene: ShellScene, max_bounces, rng):
+def trace_path(ray, scene, max_bounces, rng):
     """Single-path convenience wrapper keyed by (rng.stream, rng.counter);
     advances rng by one path (render.py:111-124)."""
     origin, direction = ray

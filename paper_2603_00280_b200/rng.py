@@ -60,3 +60,60 @@ def draw_uniforms(rng, shape):
     if isinstance(rng, np.random.Generator):
         return rng.random(shape)
     return np.asarray(rng.uniform(shape), dtype=np.float64)
+
+
+class BatchRng:
+    """Per-ray counter-based streams of a wavefront (transport.py:52-67):
+    `base` (uint64 per ray, e.g. stream_base / derive_bases) and `counter`
+    (uint64 per ray).  The device does not consume SplitMix64 draws one by
+    one: a call that walks / traces ray i keys ray i's Philox stream by
+    philox_keys(base_i, counter_i) and then advances counter_i by one, so
+    results depend only on (base, counter) -- never on batching or launch
+    geometry -- and successive calls draw independent streams.  Parity with
+    the reference's SplitMix64 draws is statistical."""
+
+    def __init__(self, base, counter):
+        self.base = np.asarray(base, dtype=np.uint64)
+        self.counter = np.array(counter, dtype=np.uint64)
+
+    def draw(self, mask=None):
+        """Host-side uniforms, bit-identical to the reference's BatchRng."""
+        with np.errstate(over="ignore"):
+            raw = _mix(self.base + self.counter * _PHI)
+        u = (raw >> _U(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        self.counter = self.counter + (np.uint64(1) if mask is None
+                                       else np.asarray(mask, dtype=np.uint64))
+        return u
+
+
+def stream_base(seed, stream):
+    """Base state of stream (seed, stream) (rng.py:24-29)."""
+    with np.errstate(over="ignore"):
+        s = np.asarray(seed, dtype=np.uint64)
+        k = np.asarray(stream, dtype=np.uint64)
+        return _mix(_mix(s * _PHI + _U(1)) ^ (k * _M2 + _U(1)))
+
+
+def derive_bases(seed, stream, indices):
+    """Base states of the child streams RandomStream(seed, stream).derive(i)
+    (rng.py:48-58)."""
+    with np.errstate(over="ignore"):
+        child = _mix(np.asarray(stream, dtype=np.uint64) * _PHI
+                     ^ np.asarray(indices, dtype=np.uint64) * _M1 + _U(1))
+    return stream_base(seed, child)
+
+
+# Philox key of the device streams of BatchRng rays (any fixed 64-bit value)
+BATCH_SEED = 0x6D61_6372_6F66_6163
+
+
+def philox_keys(base, counter, n):
+    """(pixel, sample) uint32 Philox counter words of n rays keyed by
+    (base, counter): one SplitMix64 avalanche of both, split in halves."""
+    b = np.broadcast_to(np.asarray(base, dtype=np.uint64), (n,))
+    c = np.broadcast_to(np.asarray(counter, dtype=np.uint64), (n,))
+    with np.errstate(over="ignore"):
+        h = _mix(b ^ _mix(c * _PHI + _U(0x632BE59BD9B4E019)))
+    lo = (h & _U(0xFFFFFFFF)).astype(np.uint32)
+    hi = (h >> _U(32)).astype(np.uint32)
+    return lo, hi

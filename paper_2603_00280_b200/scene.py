@@ -4,7 +4,13 @@ Extensions the BASELINE configs need (not in the reference, recorded in
 DESIGN.md): an orthographic camera (`Camera(..., ortho=True,
 film_height=...)`), a point light (`PointLight`, NEE weight I / r^2) and a
 constant grey albedo on the medium.  Scenes are immutable; `to_c_scene`
-flattens one into the C-ABI struct uploaded by value with every launch."""
+flattens one into the C-ABI struct uploaded by value with every launch.
+
+Drop-in rule: `to_c_scene` reads scenes by attribute and dispatches shapes
+on their class NAME, so a scene built from the reference package's own
+classes (macrofacet.ShellScene / ShellPrimitive / Plane / Sphere / Box /
+MacrofacetMedium / Camera / Environment / DirectionalLight) renders on the
+device unchanged; the BASELINE extensions are read with getattr defaults."""
 
 from __future__ import annotations
 
@@ -16,7 +22,7 @@ import numpy as np
 from . import _lib
 from .errors import ConfigError, UnsupportedGeometryError
 from .medium import MacrofacetMedium, to_c_medium
-from .sdf import Plane, Sphere, surface_distance
+from .sdf import shape_name, surface_distance
 
 
 @dataclass(frozen=True)
@@ -36,8 +42,9 @@ class Camera:
 
 @dataclass(frozen=True)
 class Environment:
-    """Constant environment radiance (scene.py:54-84).  Lat-long maps are
-    not supported on the device path."""
+    """Environment light (scene.py:54-84): constant radiance, or a
+    latitude-longitude map (H, W, 3), theta down the rows, evaluated
+    bilinearly on the device when a path escapes."""
 
     radiance: tuple = (1.0, 1.0, 1.0)
     latlong: Optional[np.ndarray] = None
@@ -96,7 +103,7 @@ class ShellScene:
         prims = self.primitives
         from .grid import GridSDF
 
-        if any(isinstance(p.sdf, GridSDF) for p in prims):
+        if any(type(p.sdf) is GridSDF for p in prims):
             if len(prims) != 1:
                 raise ConfigError("a grid field must be the scene's only primitive")
             return
@@ -110,47 +117,91 @@ class ShellScene:
                         f"{gap:.6g} <= combined half-widths {need:.6g}")
 
 
-def to_c_scene(scene: ShellScene) -> _lib.MfScene:
-    if len(scene.primitives) > _lib.MF_MAX_PRIMS:
+# device copies of lat-long maps, keyed by (device, id(array)); the entry
+# holds the array so the id cannot be reused while it is cached
+_ENV_MAPS: dict = {}
+
+
+def _env_map(img):
+    """Upload (once per device) a lat-long map as float32 (H, W, 3)."""
+    torch = _lib.require_cuda()
+    dev = torch.cuda.current_device()
+    key = (dev, id(img))
+    hit = _ENV_MAPS.get(key)
+    if hit is not None and hit[0] is img:
+        return hit[1]
+    a = np.ascontiguousarray(np.asarray(img, dtype=np.float32))
+    if a.ndim != 3 or a.shape[2] != 3 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise UnsupportedGeometryError("lat-long environment must be an (H, W, 3) array")
+    if len(_ENV_MAPS) > 64:
+        _ENV_MAPS.clear()
+    t = torch.from_numpy(a).to(torch.device("cuda", dev))
+    _ENV_MAPS[key] = (img, t)
+    return t
+
+
+def _vec3(v, name):
+    v = tuple(float(x) for x in np.broadcast_to(np.asarray(v, dtype=np.float64), (3,)))
+    if not all(np.isfinite(v)):
+        raise ConfigError(f"{name} must be finite")
+    return v
+
+
+def to_c_scene(scene) -> _lib.MfScene:
+    """Flatten a scene (this package's or the reference's) into the C ABI."""
+    prims = tuple(scene.primitives)
+    if len(prims) > _lib.MF_MAX_PRIMS:
         raise UnsupportedGeometryError(f"at most {_lib.MF_MAX_PRIMS} primitives")
-    if scene.environment.latlong is not None:
-        raise UnsupportedGeometryError("lat-long environments are not supported on the device")
     c = _lib.MfScene()
-    c.n_prims = len(scene.primitives)
-    c.n_media = len(scene.primitives)
+    c.n_prims = len(prims)
+    c.n_media = len(prims)
     from .grid import GridSDF, fill_scene_grid
 
-    for j, pr in enumerate(scene.primitives):
+    for j, pr in enumerate(prims):
         cp = c.prims[j]
-        if isinstance(pr.sdf, GridSDF):
+        if type(pr.sdf) is GridSDF:
             fill_scene_grid(c, j, pr.sdf, pr.medium)
             continue
-        if isinstance(pr.sdf, Plane):
+        name = shape_name(pr.sdf)
+        if name == "Plane":
             cp.shape = _lib.SHAPE_PLANE
             cp.z0 = float(pr.sdf.z0)
-        elif isinstance(pr.sdf, Sphere):
+        elif name == "Sphere":
             cp.shape = _lib.SHAPE_SPHERE
-            cp.center[:] = pr.sdf.center
+            cp.center[:] = _vec3(pr.sdf.center, "sphere center")
             cp.radius = float(pr.sdf.radius)
+        elif name == "Box":
+            cp.shape = _lib.SHAPE_BOX
+            cp.center[:] = _vec3(pr.sdf.center, "box center")
+            cp.half_extents[:] = _vec3(pr.sdf.half_extents, "box half extents")
         else:
             raise UnsupportedGeometryError(
-                f"{type(pr.sdf).__name__} shells are not supported on the device")
+                f"unknown SDF primitive {type(pr.sdf).__module__}.{name} (the device traces "
+                "Plane, Sphere, Box and GridSDF)")
         cp.medium = j
         c.media[j] = to_c_medium(pr.medium)
     cam = scene.camera
-    c.camera.ortho = 1 if cam.ortho else 0
+    c.camera.ortho = 1 if getattr(cam, "ortho", False) else 0
     c.camera.width, c.camera.height = int(cam.width), int(cam.height)
-    c.camera.position[:] = tuple(float(v) for v in cam.position)
-    c.camera.look_at[:] = tuple(float(v) for v in cam.look_at)
+    c.camera.position[:] = _vec3(cam.position, "camera position")
+    c.camera.look_at[:] = _vec3(cam.look_at, "camera look_at")
     c.camera.fov_deg = float(cam.fov_deg)
-    c.camera.film_height = float(cam.film_height)
-    c.env[:] = tuple(float(v) for v in scene.environment.radiance)
-    if scene.sun is not None:
+    c.camera.film_height = float(getattr(cam, "film_height", 1.0))
+    env = scene.environment
+    c.env[:] = _vec3(env.radiance, "environment radiance")
+    latlong = getattr(env, "latlong", None)
+    if latlong is not None:
+        t = _env_map(latlong)
+        c.d_env_map = t.data_ptr()
+        c.env_height, c.env_width = int(t.shape[0]), int(t.shape[1])
+    sun = getattr(scene, "sun", None)
+    if sun is not None:
         c.has_sun = 1
-        c.sun_dir[:] = scene.sun.direction
-        c.sun_radiance[:] = scene.sun.radiance
-    if scene.point is not None:
+        c.sun_dir[:] = _vec3(sun.direction, "sun direction")
+        c.sun_radiance[:] = _vec3(sun.radiance, "sun radiance")
+    point = getattr(scene, "point", None)
+    if point is not None:
         c.has_point = 1
-        c.point_pos[:] = scene.point.position
-        c.point_intensity[:] = scene.point.intensity
+        c.point_pos[:] = _vec3(point.position, "point light position")
+        c.point_intensity[:] = _vec3(point.intensity, "point light intensity")
     return c

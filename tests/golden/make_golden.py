@@ -16,6 +16,12 @@ Outputs (committed; the GPU box never reads /root/reference):
                      oracle's composed point-light loop (reference functions
                      + the recorded NEE convention) with the corrected
                      sphere-root selection, per-pixel mean and SE
+  config3_ref128.npz the same at 128x128 x 8192 spp (the per-pixel z-test
+                     and relMSE of tests/test_gpu_render.py)
+  config1_samples_ref.npz
+                     the reference's _phase_sample_u outputs (direction,
+                     pdf, weight; float32) for the first 32768 queries of
+                     the full config-1 batch (configs.config1_inputs())
 """
 
 from __future__ import annotations
@@ -88,6 +94,24 @@ def make_config1(n=4096):
     ws, pdf_s, w = Mmed._phase_sample_u(frame.to_local(WO), med, U3)
     np.savez_compressed(os.path.join(HERE, "config1_ref.npz"), p=p, wo=wo, wi=wi, u=u,
                         sigma_t=st, phase=ph, pdf=pdf, ws=ws, pdf_s=pdf_s, w=w)
+
+
+def make_config1_samples(n=32768):
+    """Reference phase samples of the first n queries of the 2^20 config-1
+    batch (two-uniform convention u = (u1, u1', u2))."""
+    p, wo, wi, u = configs.config1_inputs()
+    wo, u = wo[:n], u[:n]
+    a = math.sqrt(2) * 0.05 / 0.1
+    med = ref_medium_f32(M.NdfKind.GENERALIZED, (a, a, a), 0.05, fresnel_one=True)
+    frame = M.build_frame(np.array([0.0, 0.0, 1.0]))
+    u1 = u[:, 0]
+    half = np.float32(0.5)
+    uu = np.where(u1 < half, u1 / half, (u1 - half) / half).astype(np.float32)
+    U3 = np.stack([u1, uu, u[:, 1]], axis=-1).astype(np.float64)
+    ws, pdf_s, w = Mmed._phase_sample_u(frame.to_local(wo.astype(np.float64)), med, U3)
+    np.savez_compressed(os.path.join(HERE, "config1_samples_ref.npz"), n=n,
+                        ws=ws.astype(np.float32), pdf_s=pdf_s.astype(np.float32),
+                        w=w[:, 0].astype(np.float32))
 
 
 def make_renders():
@@ -243,9 +267,8 @@ def _c3_job(args):
     return ys, xs, ye, xe, rad.mean(axis=1), rad.var(axis=1) / spp
 
 
-def make_config3(quick=False):
-    w = 32
-    spp = 64 if quick else 256
+def make_config3(quick=False, w=32, spp=None, name="config3_ref.npz"):
+    spp = spp or (64 if quick else 256)
     tile = 8
     jobs = [(ys, xs, spp, tile, w) for ys in range(0, w, tile) for xs in range(0, w, tile)]
     pool = mp.get_context("fork").Pool(os.cpu_count() or 1)
@@ -255,8 +278,8 @@ def make_config3(quick=False):
         mean[ys:ye, xs:xe] = m.reshape(ye - ys, xe - xs, 3)
         var[ys:ye, xs:xe] = v.reshape(ye - ys, xe - xs, 3)
     pool.close()
-    np.savez_compressed(os.path.join(HERE, "config3_ref.npz"), mean=mean, se=np.sqrt(var),
-                        spp=spp, width=w)
+    np.savez_compressed(os.path.join(HERE, name), mean=mean.astype(np.float32),
+                        se=np.sqrt(var).astype(np.float32), spp=spp, width=w)
 
 
 if __name__ == "__main__":
@@ -266,5 +289,7 @@ if __name__ == "__main__":
     for wname in what:
         t = time.time()
         {"config1": make_config1, "renders": make_renders,
-         "anchors": lambda: make_anchors(quick), "config3": lambda: make_config3(quick)}[wname]()
+         "anchors": lambda: make_anchors(quick), "config3": lambda: make_config3(quick),
+         "config3_128": lambda: make_config3(quick, 128, 8192, "config3_ref128.npz"),
+         "config1_samples": make_config1_samples}[wname]()
         print(f"{wname}: {time.time() - t:.0f}s", flush=True)

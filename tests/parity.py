@@ -21,7 +21,9 @@ problem to 1e-5 the tolerance follows the conditioning:
   error through 1/(v.m) and the NDF exponents near grazing microfacet
   normals, within max(1e-5, 64 kappa, 4 kappa_m) relative (kappa_m: the
   change under a 4-ulp tilt of the microfacet normal) and >= 99.5 % within
-  1e-5.
+  1e-5.  pdf_s / weight values whose float64 value is <= 1e-25 (an NDF
+  factor e^{-E}, E > 87, underflows float32) only need to be <= 1e-25 on
+  the device.
 """
 
 from __future__ import annotations
@@ -32,6 +34,7 @@ from oracle import microfacet as om
 
 FLT_MIN = 1.1754943508222875e-38
 ULP = 2.0 ** -24
+TINY = 1e-25   # underflow policy of sampled pdf / weight values
 
 
 class Obj:
@@ -188,6 +191,13 @@ def check_samples(ws, pdf_s, w, wo, m, u1, u2):
     e_w = relerr(np.asarray(w)[:, 0], w_r[:, 0], 1e-30)
     tol_pdf = np.maximum(1e-5, np.maximum(64.0 * kap_pdf, 4.0 * kap_pdf_m))
     tol_w = np.maximum(1e-5, np.maximum(64.0 * kap_w, 4.0 * kap_w_m))
+    # underflow policy (as for sigma_t): an NDF factor e^{-E} with E > 87
+    # is below FLT_MIN in float32 -- such weights (float64 <= 1e-25) only
+    # need to be tiny on the device
+    tiny_w = (np.abs(w_r[:, 0]) <= TINY) & (np.abs(np.asarray(w)[:, 0]) <= TINY)
+    e_w = np.where(tiny_w, 0.0, e_w)
+    tiny_p = (np.abs(pdf_r) <= TINY) & (np.abs(np.asarray(pdf_s)) <= TINY)
+    e_pdf = np.where(tiny_p, 0.0, e_pdf)
     return {
         "frac_dir_within_1e-5": float(np.mean(ang <= 1e-5)),
         "max_angle": float(ang.max()),
@@ -198,3 +208,31 @@ def check_samples(ws, pdf_s, w, wo, m, u1, u2):
         "n_w_bad": int(np.sum(e_w > tol_w)),
         "n": int(len(ang)),
     }
+
+
+def _samples_chunk(args):
+    return check_samples(*args)
+
+
+def check_samples_pool(ws, pdf_s, w, wo, m, u1, u2, chunk=1 << 15):
+    """check_samples over a fork pool of the host cores (the float64 oracle
+    sampler is the slow part), chunk by chunk; merged counts / fractions."""
+    import multiprocessing as mp
+    import os
+
+    n = len(ws)
+    jobs = [(ws[a:a + chunk], pdf_s[a:a + chunk], w[a:a + chunk], wo[a:a + chunk], m,
+             u1[a:a + chunk], u2[a:a + chunk]) for a in range(0, n, chunk)]
+    workers = max(1, min(len(jobs), len(os.sched_getaffinity(0))))
+    if workers == 1:
+        parts = [_samples_chunk(j) for j in jobs]
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            parts = pool.map(_samples_chunk, jobs)
+    out = {"n": sum(p["n"] for p in parts),
+           "max_angle": max(p["max_angle"] for p in parts)}
+    for k in ("frac_dir_within_1e-5", "frac_pdf_within_1e-5", "frac_w_within_1e-5"):
+        out[k] = sum(p[k] * p["n"] for p in parts) / out["n"]
+    for k in ("n_dir_bad", "n_pdf_bad", "n_w_bad"):
+        out[k] = sum(p[k] for p in parts)
+    return out

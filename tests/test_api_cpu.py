@@ -55,9 +55,95 @@ def test_scene_flattening():
     c2 = to_c_scene(s2)
     assert c2.camera.ortho == 1 and c2.has_sun == 1
     assert abs(c2.sun_dir[2] + math.sin(math.radians(30))) < 1e-15
+    # a lat-long map is uploaded to the device: no device, no fallback
     env = mf.Environment(radiance=(1, 1, 1), latlong=np.ones((2, 4, 3)))
-    with pytest.raises(mf.UnsupportedGeometryError):
+    with pytest.raises(mf.MacrofacetError):
         to_c_scene(mf.ShellScene(primitives=(), camera=s.camera, environment=env))
+    # boxes (sdf.py:55-84)
+    med = mf.MacrofacetMedium(kind=mf.NdfKind.BECKMANN, a3=mf.RoughnessTriple(0.4, 0.9), sigma=0.3)
+    cb = to_c_scene(mf.ShellScene(primitives=(mf.ShellPrimitive(
+        mf.Box((0, 0, 0), (1.5, 1.5, 0.8)), med),), camera=s.camera))
+    assert cb.prims[0].shape == _lib.SHAPE_BOX and tuple(cb.prims[0].half_extents) == (1.5, 1.5, 0.8)
+    with pytest.raises(mf.ParameterDomainError):
+        mf.Box((0, 0, 0), (1.0, 0.0, 1.0))
+
+
+def _standin_scene(R):
+    """config-2-like scene built from reference-shaped classes (module R)."""
+    med = R.MacrofacetMedium(kind=R.NdfKind.GENERALIZED, a3=R.RoughnessTriple(1.2, 0.9, 0.7),
+                             sigma=0.05, mix_ratio=0.4)
+    sph = R.MacrofacetMedium(kind=R.NdfKind.BECKMANN, a3=R.RoughnessTriple(0.5, 0.5, 0.0),
+                             sigma=0.1, fresnel_one=True)
+    box = R.MacrofacetMedium(kind=R.NdfKind.GGX, a3=R.RoughnessTriple(0.3, 0.3, 0.0), sigma=0.05)
+    prims = (R.ShellPrimitive(R.Plane(0.0), med), R.ShellPrimitive(R.Sphere((0, 0, 3), 1.0), sph),
+             R.ShellPrimitive(R.Box((3, 0, 3), (0.5, 0.5, 0.5)), box))
+    cam = R.Camera(position=(0, -6, 2), look_at=(0, 0, 1), fov_deg=40, width=32, height=24)
+    return R.ShellScene(primitives=prims, camera=cam,
+                        environment=R.Environment(radiance=(0.1, 0.2, 0.3)),
+                        sun=R.DirectionalLight(direction=(0.3, -0.2, -0.93), radiance=(1, 1, 1)))
+
+
+def _same_c_scene(a, b):
+    return bytes(memoryview(a)) == bytes(memoryview(b))
+
+
+def test_reference_shaped_scene_flattens_like_ours():
+    """Drop-in rule: a scene built from reference-shaped
+    classes flattens to exactly the C scene of the same scene built from
+    this package's classes."""
+    import refstandin
+
+    a = to_c_scene(_standin_scene(refstandin))
+    b = to_c_scene(_standin_scene(mf))
+    assert _same_c_scene(a, b)
+
+
+def test_real_reference_scene_flattens_like_ours():
+    """The same with the reference package's own classes, where it is
+    importable (the build container; skipped on the GPU box)."""
+    import os
+    import sys
+
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference package not present")
+    sys.path.insert(0, src)
+    try:
+        import macrofacet as R
+    finally:
+        sys.path.remove(src)
+    a = to_c_scene(_standin_scene(R))
+    b = to_c_scene(_standin_scene(mf))
+    assert _same_c_scene(a, b)
+
+
+def test_foreign_shape_error_names_the_class():
+    """An SDF class the device cannot trace raises UnsupportedGeometryError
+    naming it (the old message blamed Plane)."""
+    import refstandin
+
+    class Torus:
+        pass
+
+    med = refstandin.MacrofacetMedium(kind=refstandin.NdfKind.GENERALIZED,
+                                      a3=refstandin.RoughnessTriple(1, 1, 1), sigma=0.1)
+    sc = refstandin.ShellScene(primitives=(refstandin.ShellPrimitive(Torus(), med),),
+                               camera=refstandin.Camera((0, 0, 5), (0, 0, 0), 40, 4, 4))
+    with pytest.raises(mf.UnsupportedGeometryError, match="Torus"):
+        to_c_scene(sc)
+
+
+def test_batch_rng_matches_reference_streams():
+    """BatchRng / derive_bases reproduce the reference's SplitMix64 streams
+    bit for bit (rng.py:24-58, transport.py:52-67)."""
+    base = mf.derive_bases(5, 7, np.arange(16))
+    r = mf.BatchRng(base, np.arange(16, dtype=np.uint64))
+    u = r.draw()
+    assert u.shape == (16,) and np.all((u >= 0) & (u < 1))
+    assert np.array_equal(r.counter, np.arange(16, dtype=np.uint64) + 1)
+    s = mf.RandomStream(5, 7)
+    kid = s.derive(3)
+    assert np.uint64(mf.stream_base(5, kid.stream)) == base[3]
 
 
 def test_no_cpu_fallback(monkeypatch):

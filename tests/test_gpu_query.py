@@ -41,11 +41,11 @@ def test_config1_full_batch(cuda):
                            tol=parity.pdf_tolerance(WO, WI))
     assert res["n_bad"] == 0, res
     assert np.all(r["flags"] == 0)
-    # sampled directions / pdf / weight on the first 2^16 queries
-    n = 1 << 16
-    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)[:n]
-    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)[:n]
-    res = parity.check_samples(ws, r["pdf_s"][:n], w, WO[:n], m, u[:n, 0], u[:n, 1])
+    # sampled directions / pdf / weight of all 2^20 queries
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)
+    res = parity.check_samples_pool(ws, r["pdf_s"], w, WO, m, u[:, 0], u[:, 1])
+    assert res["n"] == 1 << 20
     assert res["frac_dir_within_1e-5"] >= 0.9999, res
     assert res["frac_pdf_within_1e-5"] >= 0.995 and res["frac_w_within_1e-5"] >= 0.995, res
     assert res["n_dir_bad"] == 0 and res["n_pdf_bad"] == 0 and res["n_w_bad"] == 0, res
@@ -68,12 +68,38 @@ def test_config1_against_reference_outputs(cuda):
     assert res["n_bad"] == 0, res
     ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)
     ang = parity.angle(ws.astype(np.float64), g["ws"])
-    assert np.mean(ang <= 1e-5) >= 0.999, float(np.max(ang))
+    assert np.mean(ang <= 1e-5) >= 0.9999, (float(np.mean(ang <= 1e-5)), float(np.max(ang)))
 
 
-@pytest.mark.parametrize("sigma,lz", [(0.01, 0.02), (0.2, 0.02), (0.05, 0.1), (0.2, 0.1),
-                                      (0.05, float("inf")), (0.2, float("inf"))])
+def test_config1_samples_against_reference_outputs(cuda):
+    """Sampled directions, pdf and weight of the first 32768 queries of the
+    full config-1 batch vs the reference's own _phase_sample_u
+    (medium.py:181-193; fixture from make_golden.py): >= 99.99 % of the
+    directions within 1e-5 rad (north_star), pdf / weight within 1e-5
+    relative for >= 99.9 %."""
+    g = np.load(os.path.join(GOLDEN, "config1_samples_ref.npz"))
+    n = int(g["n"])
+    p, wo, wi, u = configs.config1_inputs()
+    p, wo, wi, u = p[:n], wo[:n], wi[:n], u[:n]
+    r = dev_query(cuda, configs.config1_medium(), p, wo, wi, u)
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1).astype(np.float64)
+    ang = parity.angle(ws, g["ws"].astype(np.float64))
+    frac = float(np.mean(ang <= 1e-5))
+    assert frac >= 0.9999, (frac, float(np.max(ang)))
+    e_pdf = parity.relerr(r["pdf_s"], g["pdf_s"].astype(np.float64), 1e-30)
+    e_w = parity.relerr(r["w_r"], g["w"].astype(np.float64), 1e-30)
+    # float32 fixture rounding (6e-8) is far below the bar
+    assert np.mean(e_pdf <= 1e-5) >= 0.999 and np.mean(e_w <= 1e-5) >= 0.999, (
+        float(np.mean(e_pdf <= 1e-5)), float(np.mean(e_w <= 1e-5)))
+
+
+@pytest.mark.parametrize("sigma", configs.CONFIG4_SIGMAS)
+@pytest.mark.parametrize("lz", configs.CONFIG4_LZ)
 def test_config4_media(cuda, sigma, lz):
+    """sigma_t, phase value / pdf AND the phase sample (direction, pdf_s,
+    weight: ndf.py:318-406, medium.py:181-193) for every config-4 medium
+    (alpha_xy 0.283 ... 5.657; Beckmann and generalized), same bar as
+    config 1."""
     med = configs.planar_medium(sigma, 0.05, lz, 0.8)
     m = parity.f32_medium(med)
     rs = np.random.default_rng(44)
@@ -99,6 +125,22 @@ def test_config4_media(cuda, sigma, lz):
                           tol=np.maximum(parity.pdf_tolerance(WO, WI),
                                          parity.phase_tolerance(WO, WI, m)))
     assert r1["n_bad"] == 0 and r2["n_bad"] == 0 and r3["n_bad"] == 0, (r1, r2, r3)
+    # phase samples: directions within 1e-5 rad for >= 99.99 %, every one
+    # within its conditioning bound, pdf_s / weight likewise
+    ws = np.stack([r["wsx"], r["wsy"], r["wsz"]], axis=-1)
+    w = np.stack([r["w_r"], r["w_g"], r["w_b"]], axis=-1)
+    res = parity.check_samples_pool(ws, r["pdf_s"], w, WO, m, u[:, 0], u[:, 1], chunk=1 << 13)
+    assert res["frac_dir_within_1e-5"] >= 0.9999, res
+    assert res["n_dir_bad"] == 0 and res["n_pdf_bad"] == 0 and res["n_w_bad"] == 0, res
+    # weights D_v / pdf_m of normals far in the NDF tail (hemisphere branch
+    # at alpha_xy = 0.28, or sharp Beckmann lobes) carry e^{-E} with E up to
+    # ~1e2: their float32 rounding is E ulps, inside the per-sample bound
+    # above but beyond 1e-5 for a few percent of the queries
+    assert res["frac_pdf_within_1e-5"] >= 0.995 and res["frac_w_within_1e-5"] >= 0.95, res
+    # how many queries rely on the conditioning-scaled phase tolerance
+    # (report it) -- most must meet 1e-5 outright
+    e2 = parity.relerr(r["phase_r"], om.phase_eval_local(WO, WI, m)[:, 0], 1e-25)
+    assert np.mean(e2 <= 1e-5) >= 0.99, float(np.mean(e2 <= 1e-5))
 
 
 def test_sphere_field_and_frames(cuda):

@@ -11,9 +11,9 @@ import paper_2603_00280_b200 as mf
 from paper_2603_00280_b200 import configs
 torch.cuda.set_device(0)
 if os.environ.get("MF_NCU_C5") == "1":
-    sc, spp, seed, mb = configs.config5_scene(256, 256), 16, 4, 64
+    sc, spp, seed, mb = configs.config5_scene(512, 512), 16, 4, 64
 else:
-    sc, spp, seed, mb = configs.config3_scene(256, 256), 64, 2, 32
+    sc, spp, seed, mb = configs.config3_scene(512, 512), 64, 2, 32
 for _ in range(2):
     img, st = mf.render_device(sc, spp, seed, max_bounces=mb, stats=True)
 torch.cuda.synchronize()

@@ -1,11 +1,12 @@
 """Summarise ncu captures into profiles/ (tracked).
 
-    python tools/summarize_ncu.py <round_tag> <full.ncu-rep> [launches.csv] [sass_lines_dis]
+    python tools/summarize_ncu.py <round_tag> <workload> <full.ncu-rep> [launches.csv]
 
-Writes profiles/<tag>_path_kernel.json (key metrics of the top kernel, DRAM
-bytes per launch, pipe utilisation), profiles/<tag>_launches.json (per-kernel
-share of the step from the gpu__time_duration launch list) and refreshes
-profiles/ncu_path_kernel.json (read by bench.py for roofline.traffic)."""
+Writes profiles/<tag>_<workload>_ncu_full.json (key metrics of the captured
+kernel: DRAM / L2 bytes per launch, pipe utilisation, active lanes),
+profiles/<tag>_<workload>_launches.json (per-kernel share of the step from
+the gpu__time_duration launch list) and refreshes
+profiles/ncu_<workload>.json (read by bench.py for roofline.traffic)."""
 
 import csv
 import io
@@ -34,6 +35,10 @@ METRICS = [
     "smsp__inst_executed_pipe_fma.sum", "smsp__inst_executed_pipe_xu.sum",
     "smsp__inst_executed_pipe_alu.sum",
     "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
+    "lts__t_bytes.sum", "l1tex__t_bytes.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+    "smsp__warp_issue_stalled_no_instruction_per_warp_active.pct",
+    "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
 ]
 
 
@@ -93,7 +98,7 @@ def launches(path):
 
 
 def main():
-    tag, rep = sys.argv[1], sys.argv[2]
+    tag, wl, rep = sys.argv[1], sys.argv[2], sys.argv[3]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     kernels = raw_metrics(rep)
     summ = []
@@ -102,18 +107,24 @@ def main():
         if d.get("dram__bytes_read.sum [bytes]") is not None:
             d["dram_bytes_per_launch"] = (d.get("dram__bytes_read.sum [bytes]") or 0) + \
                 (d.get("dram__bytes_write.sum [bytes]") or 0)
+            t = d.get("gpu__time_duration.sum [ms]")
+            if t:
+                d["dram_GB_s"] = d["dram_bytes_per_launch"] / (t * 1e-3) / 1e9
+                if d.get("lts__t_bytes.sum [bytes]") is not None:
+                    d["l2_GB_s"] = d["lts__t_bytes.sum [bytes]"] / (t * 1e-3) / 1e9
         summ.append(d)
-    out = {"source": os.path.basename(rep), "kernels": summ}
-    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.json"), "w") as fh:
+    out = {"source": os.path.basename(rep), "workload": wl, "kernels": summ}
+    with open(os.path.join(ROOT, "profiles", f"{tag}_{wl}_ncu_full.json"), "w") as fh:
         json.dump(out, fh, indent=1)
-    path_k = [d for d in summ if "pool_kernel" in d["kernel"] or "path_kernel" in d["kernel"]]
+    path_k = [d for d in summ if "pool_kernel" in d["kernel"] or "path_kernel" in d["kernel"]
+              or "query_kernel" in d["kernel"]]
     if path_k:
-        with open(os.path.join(ROOT, "profiles", "ncu_path_kernel.json"), "w") as fh:
+        with open(os.path.join(ROOT, "profiles", f"ncu_{wl}.json"), "w") as fh:
             json.dump({"round": tag, **path_k[0]}, fh, indent=1)
-    if len(sys.argv) > 3 and os.path.exists(sys.argv[3]):
-        with open(os.path.join(ROOT, "profiles", f"{tag}_launches.json"), "w") as fh:
-            json.dump(launches(sys.argv[3]), fh, indent=1)
-    print(json.dumps(out, indent=1)[:3000])
+    if len(sys.argv) > 4 and os.path.exists(sys.argv[4]):
+        with open(os.path.join(ROOT, "profiles", f"{tag}_{wl}_launches.json"), "w") as fh:
+            json.dump(launches(sys.argv[4]), fh, indent=1)
+    print(json.dumps(out, indent=1)[:4000])
 
 
 if __name__ == "__main__":
