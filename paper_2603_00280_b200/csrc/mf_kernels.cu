@@ -267,6 +267,27 @@ __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 // path megakernel
 
+// Division by a runtime constant d: q = floor(n * ceil(2^64 / d) / 2^64),
+// exact for every 32-bit n and d (the error n (ceil - 2^64/d) / 2^64 < 2^-32
+// never carries past the next multiple of 1/d); d = 1 is special-cased.
+// Three integer instructions instead of the ~20 of a 32-bit IDIV sequence
+// (raygen maps a path index to (sample, tile, pixel) with four of them).
+struct FastDiv {
+  unsigned long long m;   // ceil(2^64 / d), 0 for d == 1
+  uint32_t d;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.m = d > 1 ? (~0ull / d) + 1ull : 0ull;
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.m ? (uint32_t)__umul64hi((unsigned long long)n, f.m) : n;
+}
+
 struct PassDev {
   uint32_t k0, k1;
   // Philox round keys (k0 + r W0, k1 + r W1), so the unrolled rounds of the
@@ -278,6 +299,7 @@ struct PassDev {
   uint32_t sample_begin; // global sample index of the pass's first sample
   uint32_t n_local;      // local pixels of this rank (render mode)
   int shard, rank, nranks, tile, tiles_x;
+  FastDiv div_local, div_t2, div_tiles_x, div_tile, div_width;
   int mono;              // grey scene: the accumulator holds channel 0 only
   // render mode: per-pixel fixed-point sums (accumulate_fx), channel-major
   // per local pixel: fx[lp * (mono ? 1 : 3) + c] += rint(L_c * fx_scale)
@@ -294,17 +316,28 @@ struct PassDev {
   const uint32_t* smp;
 };
 
-// local pixel index -> global pixel index, or -1 (tile padding)
-__device__ __forceinline__ int local_to_pixel(const SceneDev& sc, const PassDev& ps, uint32_t lp) {
-  if (ps.shard == MF_SHARD_SAMPLES) return (int)lp;
-  uint32_t t2 = (uint32_t)(ps.tile * ps.tile);
-  uint32_t k = lp / t2;
-  uint32_t j = lp - k * t2;
-  uint32_t t = (uint32_t)ps.rank + k * (uint32_t)ps.nranks;
-  uint32_t ty = t / (uint32_t)ps.tiles_x, tx = t - ty * (uint32_t)ps.tiles_x;
-  uint32_t jy = j / (uint32_t)ps.tile, jx = j - jy * (uint32_t)ps.tile;
-  uint32_t x = tx * ps.tile + jx, y = ty * ps.tile + jy;
-  if (x >= (uint32_t)sc.width || y >= (uint32_t)sc.height) return -1;
+// local pixel index -> global pixel index (and its x, y), or -1 (tile
+// padding)
+__device__ __forceinline__ int local_to_pixel(const SceneDev& sc, const PassDev& ps, uint32_t lp,
+                                              uint32_t* px = nullptr, uint32_t* py = nullptr) {
+  uint32_t x, y;
+  if (ps.shard == MF_SHARD_SAMPLES) {
+    y = fdiv(lp, ps.div_width);
+    x = lp - y * (uint32_t)sc.width;
+  } else {
+    uint32_t k = fdiv(lp, ps.div_t2);
+    uint32_t j = lp - k * ps.div_t2.d;
+    uint32_t t = (uint32_t)ps.rank + k * (uint32_t)ps.nranks;
+    uint32_t ty = fdiv(t, ps.div_tiles_x), tx = t - ty * (uint32_t)ps.tiles_x;
+    uint32_t jy = fdiv(j, ps.div_tile), jx = j - jy * (uint32_t)ps.tile;
+    x = tx * ps.tile + jx;
+    y = ty * ps.tile + jy;
+    if (x >= (uint32_t)sc.width || y >= (uint32_t)sc.height) return -1;
+  }
+  if (px) {
+    *px = x;
+    *py = y;
+  }
   return (int)(y * (uint32_t)sc.width + x);
 }
 
@@ -324,10 +357,8 @@ struct Counters {
   uint32_t v[kStCount];
 };
 
-__device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t pixel, float jx, float jy,
-                                           V3* o, V3* d) {
-  uint32_t py = pixel / (uint32_t)sc.width;
-  uint32_t px = pixel - py * (uint32_t)sc.width;
+__device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t px, uint32_t py, float jx,
+                                           float jy, V3* o, V3* d) {
   float nx = ((float)px + jx) / (float)sc.width * 2.0f - 1.0f;
   float ny = 1.0f - ((float)py + jy) / (float)sc.height * 2.0f;
   if (sc.ortho) {
@@ -616,15 +647,16 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   // sample-major path order: the 32 paths a warp starts together belong to
   // 32 consecutive pixels, so the fixed-point adds of paths finishing
   // together hit distinct (adjacent) accumulator words instead of one
-  uint32_t s = my / ps.n_local;
+  uint32_t s = fdiv(my, ps.div_local);
   uint32_t lp = my - s * ps.n_local;
   st.pid = lp;   // the path's radiance goes to its local pixel's sums
-  int pixel = local_to_pixel(sc, ps, lp);
+  uint32_t px, py;
+  int pixel = local_to_pixel(sc, ps, lp, &px, &py);
   if (pixel < 0) return false;   // tile padding
   st.rng.pixel = (uint32_t)pixel;
   st.rng.sample = ps.sample_begin + s;
   U4 jb = philox_rk(U4{st.rng.pixel, st.rng.sample, kSegCamera, 0u}, ps.rk);
-  camera_ray(sc, (uint32_t)pixel, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
+  camera_ray(sc, px, py, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
   return true;
 }
 
@@ -1695,7 +1727,8 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     return fail(MF_ERR_PARAM, "bad rank / nranks");
   if (p.shard != MF_SHARD_TILES && p.shard != MF_SHARD_SAMPLES)
     return fail(MF_ERR_PARAM, "unknown shard mode");
-  if (p.shard == MF_SHARD_TILES && p.tile < 1) return fail(MF_ERR_PARAM, "tile must be >= 1");
+  if (p.shard == MF_SHARD_TILES && (p.tile < 1 || p.tile > 65535))
+    return fail(MF_ERR_PARAM, "tile must lie in [1, 65535]");
   SceneDev sc;
   std::string berr;
   int rc = build_scene(*scene, &sc, &berr);
@@ -1716,12 +1749,16 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   ps.rank = p.rank;
   ps.nranks = p.nranks;
   ps.tile = p.tile;
+  ps.div_width = make_fastdiv((uint32_t)sc.width);
+  ps.div_tile = make_fastdiv((uint32_t)std::max(p.tile, 1));
+  ps.div_t2 = make_fastdiv((uint32_t)std::max(p.tile, 1) * (uint32_t)std::max(p.tile, 1));
   // local pixels and this rank's sample range
   size_t n_local;
   uint32_t s_begin = 0, s_count = (uint32_t)p.spp;
   if (p.shard == MF_SHARD_TILES) {
     int tx = (sc.width + p.tile - 1) / p.tile, ty = (sc.height + p.tile - 1) / p.tile;
     ps.tiles_x = tx;
+    ps.div_tiles_x = make_fastdiv((uint32_t)tx);
     int n_tiles = tx * ty;
     int mine = n_tiles > p.rank ? (n_tiles - p.rank + p.nranks - 1) / p.nranks : 0;
     n_local = (size_t)mine * p.tile * p.tile;
@@ -1781,6 +1818,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.sample_begin = s_begin + s0;
     ps.n_paths = (uint32_t)(n_local * S);
     ps.n_local = (uint32_t)n_local;
+    ps.div_local = make_fastdiv((uint32_t)n_local);
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
     ev.resize(ev.size() + 2, nullptr);
     MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));
