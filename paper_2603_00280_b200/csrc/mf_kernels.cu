@@ -394,8 +394,11 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
     if (w.steps < 0) cn.v[kStCapped]++;   // iteration cap: raised by the host
     return w.steps < 0 ? 0.0f : w.weight;
   } else {
-    WalkResult w = walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true, t_max,
-                        kShadowRR);
+    WalkResult w = kMode == 3 && !sc.generic_walk
+                       ? sphere_walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true,
+                                     t_max, kShadowRR)
+                       : walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl,
+                                          true, t_max, kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
     if (w.steps < 0) cn.v[kStCapped]++;
@@ -492,8 +495,11 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& 
     st.lphi = fl.lphi;
     outcome = fl.outcome;
   } else {
-    WalkResult w = walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false,
-                                    INFINITY);
+    WalkResult w = kMode == 3 && !sc.generic_walk
+                       ? sphere_walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false,
+                                     INFINITY)
+                       : walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir,
+                                          false, INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
     cn.v[kStViolations] += (uint32_t)w.violations;
     st.cpos = w.pos;
@@ -1159,8 +1165,12 @@ __global__ void __launch_bounds__(kBlock) walk_kernel(const __grid_constant__ Sc
       viol = (uint32_t)w.violations;
       capped = w.steps < 0 ? 1u : 0u;
     } else {
-      WalkResult w = walk(sc, rng, a.segment, call0, o, d, ratio, INFINITY, 0.0f,
-                          a.mode == MF_WALK_TENTATIVE);
+      // a single sphere uses the renderer's tangent-majorant walker
+      bool one_sphere = sc.n_prims == 1 && sc.prims[0].shape == kShapeSphere &&
+                        a.mode != MF_WALK_TENTATIVE;
+      WalkResult w = one_sphere ? sphere_walk(sc, rng, a.segment, call0, o, d, ratio, INFINITY)
+                                : walk(sc, rng, a.segment, call0, o, d, ratio, INFINITY, 0.0f,
+                                       a.mode == MF_WALK_TENTATIVE);
       outcome = w.outcome;
       prim = (outcome == kCollided || outcome == kNullCollision) ? w.prim : -1;
       pos = w.pos;
@@ -1448,14 +1458,18 @@ bool megakernel_requested() {
   return e && e[0] == '1';
 }
 
-int launch_paths(const SceneDev& sc, const PassDev& ps, bool caller_rays, cudaStream_t st) {
+int launch_paths(const SceneDev& sc_in, const PassDev& ps, bool caller_rays, cudaStream_t st) {
   Occupancy occ;
   int rc = device_occupancy(&occ);
   if (rc) return rc;
+  SceneDev sc = sc_in;
   // modes: 0 single plane, 1 general shells, 2 grid field, 3 one sphere
-  // (MF_GENERIC_WALK=1: the general walker for it, for the equality test)
+  // MF_GENERIC_WALK=1: the general tracking walker for a single sphere
+  // (mode 1), =2: the single-sphere instantiation of that walker (mode 3 with
+  // sc.generic_walk) instead of the tangent-majorant sphere_walk
   const char* gw = std::getenv("MF_GENERIC_WALK");
   bool generic = gw && gw[0] == '1';
+  sc.generic_walk = gw && gw[0] == '2';
   int mode = sc.has_grid ? 2
                          : (sc.single_plane ? 0
                                             : (sc.n_prims == 1 && sc.prims[0].shape == kShapeSphere &&

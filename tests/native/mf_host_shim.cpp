@@ -104,6 +104,17 @@ extern "C" {
 // org/dir SoA [3][n]; path i keyed (pixel = i, sample = 0, segment 0).
 // out: state[n] (0 escaped, 1 absorbed, 2 collided), pos SoA [3][n], weight[n]
 // rr_min: Russian-roulette threshold of ratio weights (0: plain ratio tracking)
+static int g_sphere_walk = 0;
+static int32_t* steps = nullptr;
+
+// select the walker of mfh_walk: 0 the general tracking walker, 1 the
+// single-sphere tangent-majorant walker (sphere_walk); optional per-ray
+// iteration counts
+void mfh_set_walker(int sphere, int32_t* steps_out) {
+  g_sphere_walk = sphere;
+  steps = steps_out;
+}
+
 int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t n, uint64_t seed,
              int ratio, int32_t* state, float* pos, float* weight, float majorant_scale,
              int64_t* violations, float rr_min) {
@@ -129,7 +140,11 @@ int mfh_walk(const mf_scene* scene, const float* org, const float* dir, int64_t 
       *violations += w.violations;
       continue;
     }
-    WalkResult w = walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0, INFINITY, rr_min);
+    WalkResult w = g_sphere_walk ? sphere_walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d,
+                                               ratio != 0, INFINITY, rr_min)
+                                 : walk(sc, r, 0u, ratio ? kCallShadow : 1u, o, d, ratio != 0,
+                                        INFINITY, rr_min);
+    if (steps) steps[i] = w.steps;
     state[i] = w.outcome;
     pos[i] = w.pos.x;
     pos[n + i] = w.pos.y;
