@@ -197,6 +197,24 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   U4 bits = U4{0, 0, 0, 0};
   int avail = 0;
   uint32_t call = call0;
+  auto draw = [&]() {
+    if (avail == 0) {
+      bits = rng_block(call++);
+      avail = 4;
+    }
+    float u = u01(bits.x);
+    bits.x = bits.y;
+    bits.y = bits.z;
+    bits.z = bits.w;
+    --avail;
+    return u;
+  };
+  // optical depth left to the next tentative collision: sampled once per
+  // tentative and used up cell by cell (tau -= mu dt), instead of a fresh
+  // exponential (a uniform and a log) in every cell the ray crosses -- the
+  // same process (the majorant is piecewise constant along the ray), a
+  // fraction of the random numbers and logs
+  float tau = -flog(draw());
   int iter = 0;
   for (; iter < kGridIterCap; ++iter) {
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
@@ -205,18 +223,9 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
     printf("it %d t %g cell %d %d %d mu %g tx %g ty %g tz %g t1 %g\n", iter, t, cx, cy, cz, mu, tx, ty, tz, t1);
 #endif
     if (mu > 0.0f) {
-      if (avail == 0) {
-        bits = rng_block(call++);
-        avail = 4;
-      }
-      float u = u01(bits.x);
-      bits.x = bits.y;
-      bits.y = bits.z;
-      bits.z = bits.w;
-      --avail;
-      float ts = t - flog(u) / mu;
-      if (ts < t_exit) {
-        t = ts;
+      float need = mu * (t_exit - t);
+      if (tau < need) {
+        t += tau / mu;
         w.steps++;
         V3 p = fma3(dir, t, pos);
         float f, sg;
@@ -226,15 +235,7 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
           w.weight *= fmaxf(1.0f - st / mu, 0.0f);
           if (w.weight < rr_min && w.weight > 0.0f) {
             // Russian roulette on the weight (see walk() in mf_transport.cuh)
-            if (avail == 0) {
-              bits = rng_block(call++);
-              avail = 4;
-            }
-            float ur = u01(bits.x);
-            bits.x = bits.y;
-            bits.y = bits.z;
-            bits.z = bits.w;
-            --avail;
+            float ur = draw();
             w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
           }
           if (!(w.weight > 0.0f)) {
@@ -247,23 +248,16 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
             w.pos = p;
             return w;
           }
-          if (avail == 0) {
-            bits = rng_block(call++);
-            avail = 4;
-          }
-          float u2 = u01(bits.x);
-          bits.x = bits.y;
-          bits.y = bits.z;
-          bits.z = bits.w;
-          --avail;
-          if (u2 * mu < st) {
+          if (draw() * mu < st) {
             w.outcome = 2;
             w.pos = p;
             return w;
           }
         }
+        tau = -flog(draw());
         continue;
       }
+      tau -= need;
     }
     // leave the cell
     if (t_exit >= t1) {

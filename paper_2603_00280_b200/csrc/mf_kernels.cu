@@ -299,7 +299,8 @@ struct PassDev {
   uint32_t sample_begin; // global sample index of the pass's first sample
   uint32_t n_local;      // local pixels of this rank (render mode)
   int shard, rank, nranks, tile, tiles_x;
-  FastDiv div_local, div_t2, div_tiles_x, div_tile, div_width;
+  FastDiv div_local, div_t2, div_tiles_x, div_tile, div_width, div_S;
+  int pixel_major;       // path order: 1 all samples of a pixel together, 0 sample-major
   int mono;              // grey scene: the accumulator holds channel 0 only
   // render mode: per-pixel fixed-point sums (accumulate_fx), channel-major
   // per local pixel: fx[lp * (mono ? 1 : 3) + c] += rint(L_c * fx_scale)
@@ -650,11 +651,20 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
     st.dir = v3(ps.dir[my], ps.dir[ps.n_paths + my], ps.dir[2u * ps.n_paths + my]);
     return true;
   }
-  // sample-major path order: the 32 paths a warp starts together belong to
-  // 32 consecutive pixels, so the fixed-point adds of paths finishing
-  // together hit distinct (adjacent) accumulator words instead of one
-  uint32_t s = fdiv(my, ps.div_local);
-  uint32_t lp = my - s * ps.n_local;
+  // path order.  Sample-major (the path pool): the 32 paths a warp starts
+  // together belong to 32 consecutive pixels, so the fixed-point adds of
+  // paths finishing together hit distinct (adjacent) accumulator words
+  // instead of one.  Pixel-major (the tracking megakernels, whose paths are
+  // long and whose adds rarely collide): a warp's paths share their camera
+  // ray up to the jitter, so their first walks stay coherent.
+  uint32_t s, lp;
+  if (ps.pixel_major) {
+    lp = fdiv(my, ps.div_S);
+    s = my - lp * ps.S;
+  } else {
+    s = fdiv(my, ps.div_local);
+    lp = my - s * ps.n_local;
+  }
   st.pid = lp;   // the path's radiance goes to its local pixel's sums
   uint32_t px, py;
   int pixel = local_to_pixel(sc, ps, lp, &px, &py);
@@ -1795,6 +1805,8 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   if (n_local * S_pass > 0xffffffffull) return fail(MF_ERR_PARAM, "image too large for one pass");
   // grey scenes keep one channel per pixel (all kernels; channels are equal)
   ps.mono = sc.mono;
+  ps.pixel_major = sc.single_plane ? 0 : 1;
+  if (const char* e = std::getenv("MF_PATH_ORDER")) ps.pixel_major = e[0] == 'p' ? 1 : 0;
   size_t n_fx = n_local * (ps.mono ? 1 : 3);
   Scratch scr;
   rc = scratch_alloc(&scr, n_fx, st);
@@ -1833,6 +1845,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.n_paths = (uint32_t)(n_local * S);
     ps.n_local = (uint32_t)n_local;
     ps.div_local = make_fastdiv((uint32_t)n_local);
+    ps.div_S = make_fastdiv(S);
     MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
     ev.resize(ev.size() + 2, nullptr);
     MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));

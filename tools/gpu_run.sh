@@ -1,5 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -s -k "not nothing" 2>&1 | grep -vE "^  |Warning|warnings.warn" | grep -E "config3 128|passed|failed|Error|^E |FAIL" | tail -30 > gpurun_out/gpu_tests.log
-timeout 600 python bench.py --workload config3 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_config3.json 2> gpurun_out/bench_config3.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_config3.json')); r=d['roofline']
-print('c3', d['value'], d['ms_per_step'], r['frac'], d['stats_per_path']['track_steps'])" >> gpurun_out/gpu_tests.log
+for v in pix smp pix smp; do MF_PATH_ORDER=$v python tools/c5_quick.py 2>&1 | cut -c1-60 | sed "s/^/$v /"; done > gpurun_out/c5.log
+for v in pix smp; do MF_PATH_ORDER=$v python bench.py --workload config3 --steps 3 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$v c3', d['value'], d['roofline']['frac'])"; done >> gpurun_out/c5.log
