@@ -57,7 +57,7 @@ constexpr int kBlock = 128;
 constexpr int kMinBlocks = MF_MIN_BLOCKS;
 // the same for the path pool (its smem pools allow up to 7 blocks per SM)
 #ifndef MF_POOL_MIN_BLOCKS
-#define MF_POOL_MIN_BLOCKS 6
+#define MF_POOL_MIN_BLOCKS 8
 #endif
 constexpr int kPoolMinBlocks = MF_POOL_MIN_BLOCKS;
 
@@ -459,6 +459,42 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
                                                float sig_known, bool done, float u_br,
                                                float u_s2, float u_rr);
 
+// next-event estimation at a collision on a curved shell / grid field (sun
+// and point light, shadow rays walked in ratio mode): the megakernel's
+// stage 2 and the sphere pool's visits run this one copy, so their images
+// agree bit for bit
+template <int kMode>
+__device__ __forceinline__ void curved_nee(const SceneDev& sc, PathState& st, Counters& cn,
+                                           const MediumK& m, const Frame& fr, V3 wo, float sig_o,
+                                           V3 pos) {
+  if (sc.has_sun) {
+    V3 wl = to_local(fr, sc.sun_to);
+    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
+                                  sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
+                           st.T.z * ph.z * sc.sun_L.z * tr));
+    }
+  }
+  if (sc.has_point) {
+    V3 d = sub3(sc.point_pos, pos);
+    float r2 = dot3(d, d);
+    float ir = frsqrt(r2);
+    V3 wlw = mul3(d, ir);
+    V3 wl = to_local(fr, wlw);
+    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+      cn.v[kStNee]++;
+      float tr = shadow_tr<kMode>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
+      float s = tr * frcp(r2);
+      st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
+                           st.T.z * ph.z * sc.point_I.z * s));
+    }
+  }
+}
+
 // Stage 1 of a segment: draw the segment's uniforms and fly to the next real
 // collision (transport.py:144-297).  Returns true on a collision (state kept
 // in st.cpos / st.ck / st.csig for the scatter stage); on escape / absorption
@@ -573,37 +609,24 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
   }
   // ---- stage 2: next-event estimation (render.py:71-82; point light:
   //      BASELINE extension)
-  if (!done && sc.has_sun) {
-    V3 wl = to_local(fr, sc.sun_to);
-    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
-    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
-      cn.v[kStNee]++;
-      float tr = kMode == 0 ? planar_sun_tr(sc, st.lphi, pos)
-                            : shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
-                                               sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn,
-                                               sc.sun_sig);
-      st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
-                           st.T.z * ph.z * sc.sun_L.z * tr));
+  if (kMode == 0) {
+    if (!done && sc.has_sun) {
+      V3 wl = to_local(fr, sc.sun_to);
+      V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+      if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+        cn.v[kStNee]++;
+        float tr = planar_sun_tr(sc, st.lphi, pos);
+        st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
+                             st.T.z * ph.z * sc.sun_L.z * tr));
+      }
     }
-  }
-  if (kMode == 0 && !done && sc.has_point) {
-    int nee = 0;
-    st.L = add3(st.L, planar_point_nee(sc, st, wo, sig_o, pos, &nee));
-    cn.v[kStNee] += (uint32_t)nee;
-  } else if (!done && sc.has_point) {
-    V3 d = sub3(sc.point_pos, pos);
-    float r2 = dot3(d, d);
-    float ir = frsqrt(r2);
-    V3 wlw = mul3(d, ir);
-    V3 wl = to_local(fr, wlw);
-    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
-    if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
-      cn.v[kStNee]++;
-      float tr = shadow_tr<kMode>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
-      float s = tr * frcp(r2);
-      st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
-                           st.T.z * ph.z * sc.point_I.z * s));
+    if (!done && sc.has_point) {
+      int nee = 0;
+      st.L = add3(st.L, planar_point_nee(sc, st, wo, sig_o, pos, &nee));
+      cn.v[kStNee] += (uint32_t)nee;
     }
+  } else if (!done) {
+    curved_nee<kMode>(sc, st, cn, m, fr, wo, sig_o, pos);
   }
   __syncwarp(amask);
   // ---- stage 3: phase sampling (render.py:84-90), two-uniform convention
@@ -1066,6 +1089,153 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
   }
 }
 
+// Path pool for one sphere (config 3): pool_kernel's slot rings and visit
+// kinds (R raygen + flight; B / H: NEE, the Beckmann / hemisphere visible
+// normal, the phase tail, depth cap / RR, the next flight) with the curved
+// shell's pieces: the local frame about the collision point's normal, NEE
+// with ratio-tracked shadow rays (curved_nee, sphere_walk) and the
+// tangent-majorant flight (flight_stage<3>).  Every path runs the
+// megakernel's arithmetic on the same random stream, so the image is
+// bit-identical to path_kernel<3> (MF_MEGAKERNEL=1) -- only the order in
+// which paths advance changes.  The slot layout is pool_kernel's with a
+// point light (positions stored).
+#ifndef MF_SPHERE_POOL_MIN_BLOCKS
+#define MF_SPHERE_POOL_MIN_BLOCKS 7
+#endif
+template <bool kMono>
+__global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) sphere_pool_kernel(
+    const __grid_constant__ SceneDev sc, const __grid_constant__ PassDev ps) {
+  __shared__ PoolSlots<true, kMono> pools[kWarpsPerBlock];
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  PoolSlots<true, kMono>& P = pools[threadIdx.x >> 5];
+  const MediumK& m = sc.media[0];
+  Counters cn;
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
+  auto finish = [&](const PathState& q) {
+    if constexpr (kMono) accumulate_fx(ps, q.pid, q.L.x, cn);
+    else finish_path<false>(ps, q, cn);
+  };
+#pragma unroll
+  for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
+  __syncwarp();
+  unsigned he = 0, hb = 0, hh = 0, te = kPool, tb = 0, th = 0;
+  bool exhausted = false;
+  while (true) {
+    int ne = exhausted ? 0 : (int)(te - he), nb = (int)(tb - hb), nh = (int)(th - hh);
+    int stage;
+    if (nb >= 32) stage = kStageBeck;
+    else if (nh >= 32) stage = kStageHemi;
+    else if (ne >= 32) stage = kStageRaygen;
+    else if (nb > 0 && nb >= nh) stage = kStageBeck;
+    else if (nh > 0) stage = kStageHemi;
+    else if (ne > 0) stage = kStageRaygen;
+    else break;
+    int cnt = stage == kStageBeck ? nb : (stage == kStageHemi ? nh : ne);
+    unsigned head = stage == kStageBeck ? hb : (stage == kStageHemi ? hh : he);
+    int n = cnt < 32 ? cnt : 32;
+    int slot = lane < n ? (int)P.ring[stage][(head + (unsigned)lane) & (kRing - 1)] : -1;
+    if (stage == kStageBeck) hb += (unsigned)n;
+    else if (stage == kStageHemi) hh += (unsigned)n;
+    else he += (unsigned)n;
+
+    uint8_t tag = kTagEmpty;
+    PathState st;
+    float sig_o = 0.0f;
+    bool fly = false;
+    if (stage == kStageRaygen) {
+      unsigned need = __ballot_sync(full, slot >= 0);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(ps.counter, (unsigned)__popc(need));
+      base = __shfl_sync(full, base, 0);
+      if (base + (unsigned)__popc(need) >= ps.n_paths) exhausted = true;
+      uint32_t my = base + (uint32_t)lane;
+      if (slot >= 0 && my < ps.n_paths && start_path<false>(sc, ps, st, my)) {
+        cn.v[kStPaths]++;
+        fly = true;
+      }
+    } else if (slot >= 0) {
+      pool_load<true, kMono>(P, slot, ps, st, sig_o);
+      // scatter_stages<3> at the stored collision: frame, NEE, phase sample
+      Frame fr = frame_about(prim_normal<true>(sc.prims[0], st.pos));
+      V3 wo = to_local(fr, st.dir);
+      curved_nee<3>(sc, st, cn, m, fr, wo, sig_o, st.pos);
+      V3 v = neg3(wo);
+      float uu = remap_branch_uniform_render(st.u_br, m);
+      float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
+      V3 wm;
+      float vm;
+      if (stage == kStageBeck && sig_b > 1e-12f) {
+        int iters = 0;
+        wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
+        vm = dot3(v, wm);
+        cn.v[kStSlopeIters] += (uint32_t)iters;
+      } else {
+        wm = hemisphere_about(v, uu, st.u_s2);
+        vm = uu;
+      }
+      PhaseSample smp = phase_sample_tail<kSpecRuntime, true>(m, v, wm, vm, sig_o, sig_b,
+                                                              sig_b > 1e-12f);
+      st.dir = to_world(fr, smp.wi);
+      st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
+      st.bounce++;
+      bool done = false;
+      if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+        done = true;
+      } else if (st.bounce > 8) {                    // render.py:96-105
+        float q = kMono ? fminf(st.T.x, 1.0f) : fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+        if (st.u_rr >= q) {
+          done = true;
+        } else {
+          st.T = mul3(st.T, 1.0f / q);
+        }
+      }
+      if (done) finish(st);
+      else fly = true;
+    }
+    __syncwarp();
+    if (fly) {
+      if (!flight_stage<3>(sc, ps, st, cn)) {
+        finish(st);
+      } else {
+        // the collision's frame and sigma(wo), as scatter_stages<3>
+        st.pos = st.cpos;
+        Frame fr = frame_about(prim_normal<true>(sc.prims[0], st.pos));
+        sig_o = proj_area<kSpecRuntime, true>(m, to_local(fr, st.dir));
+        cn.v[kStScatters]++;
+        if (!(sig_o >= 1e-12f)) {
+          cn.v[kStDegenerate]++;
+          finish(st);
+        } else {
+          tag = st.u_br < m.mix ? kTagBeck : kTagHemi;
+        }
+      }
+    }
+    if (slot >= 0 && tag != kTagEmpty) pool_store<true, kMono>(P, slot, st, sig_o);
+    {
+      unsigned me = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
+      unsigned mb = __ballot_sync(full, slot >= 0 && tag == kTagBeck);
+      unsigned mh = __ballot_sync(full, slot >= 0 && tag == kTagHemi);
+      if (slot >= 0) {
+        unsigned mine = tag == kTagEmpty ? me : (tag == kTagBeck ? mb : mh);
+        unsigned tail = tag == kTagEmpty ? te : (tag == kTagBeck ? tb : th);
+        P.ring[tag][(tail + (unsigned)__popc(mine & lt)) & (kRing - 1)] = (uint8_t)slot;
+      }
+      te += (unsigned)__popc(me);
+      tb += (unsigned)__popc(mb);
+      th += (unsigned)__popc(mh);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) {
+    unsigned v = __reduce_add_sync(full, cn.v[i]);
+    if (lane == 0 && v) atomicAdd(ps.stats + i, (unsigned long long)v);
+  }
+}
+
 // fixed-point pixel sums -> the caller's fp32 image (render.py:165-166):
 // one thread per local pixel, sum * 2^-k / spp in double, added to (or
 // written into) accum[pixel][c]
@@ -1323,7 +1493,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[20] = {};
+  int blocks[22] = {};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1376,6 +1546,10 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_pool<true, false, 1>(&o.blocks[11])));
   MF_CUDA((occ_pool<false, true, 1>(&o.blocks[12])));
   MF_CUDA((occ_pool<true, true, 1>(&o.blocks[13])));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[20], sphere_pool_kernel<false>,
+                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[21], sphere_pool_kernel<true>,
+                                                        kBlock, 0));
   MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
   MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
   MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));
@@ -1519,7 +1693,15 @@ int launch_paths(const SceneDev& sc_in, const PassDev& ps, bool caller_rays, cud
     else path_kernel<1, false><<<grid, kBlock, 0, st>>>(sc, ps);
   } else if (mode == 3) {
     if (caller_rays) path_kernel<3, true><<<grid, kBlock, 0, st>>>(sc, ps);
-    else path_kernel<3, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    else if (megakernel_requested() || sc.generic_walk) path_kernel<3, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    else {
+      // the sphere path pool (MF_MEGAKERNEL=1: the megakernel, for the
+      // bit-exactness test)
+      int pk = sc.mono ? 21 : 20;
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
+      if (sc.mono) sphere_pool_kernel<true><<<grid, kBlock, 0, st>>>(sc, ps);
+      else sphere_pool_kernel<false><<<grid, kBlock, 0, st>>>(sc, ps);
+    }
   } else {
     if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
