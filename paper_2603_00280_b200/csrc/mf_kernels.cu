@@ -1089,28 +1089,61 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
   }
 }
 
-// Path pool for one sphere (config 3): pool_kernel's slot rings and visit
+// Path pool for one sphere (config 3) or a grid field (config 5, kMode 2):
+// pool_kernel's slot rings and visit
 // kinds (R raygen + flight; B / H: NEE, the Beckmann / hemisphere visible
 // normal, the phase tail, depth cap / RR, the next flight) with the curved
 // shell's pieces: the local frame about the collision point's normal, NEE
 // with ratio-tracked shadow rays (curved_nee, sphere_walk) and the
-// tangent-majorant flight (flight_stage<3>).  Every path runs the
-// megakernel's arithmetic on the same random stream, so the image is
-// bit-identical to path_kernel<3> (MF_MEGAKERNEL=1) -- only the order in
-// which paths advance changes.  The slot layout is pool_kernel's with a
+// tangent-majorant flight (flight_stage<3>) or the grid walker.  Every path
+// runs the megakernel's arithmetic on the same random stream and makes the
+// same decisions (identical event counts); the sphere image is
+// bit-identical to path_kernel<3> (MF_MEGAKERNEL=1), the grid image agrees
+// to float rounding (~1e-5 relative in a few percent of pixels: the
+// compiler contracts a few multiply-adds differently in the two inlining
+// contexts).  The slot layout is pool_kernel's with a
 // point light (positions stored).
 #ifndef MF_SPHERE_POOL_MIN_BLOCKS
 #define MF_SPHERE_POOL_MIN_BLOCKS 7
 #endif
-template <bool kMono>
-__global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) sphere_pool_kernel(
+// The medium and local frame at a collision point: the sphere's medium and
+// the frame about its normal (kMode 3), or the grid field's medium from
+// sigma(p) and the frame about the trilinear SDF gradient (kMode 2) -- the
+// same operations as scatter_stage<kMode>
+template <int kMode>
+struct CollisionLocal;
+
+template <>
+struct CollisionLocal<3> {
+  const MediumK& m;
+  Frame fr;
+  __device__ __forceinline__ CollisionLocal(const SceneDev& sc, V3 pos)
+      : m(sc.media[0]), fr(frame_about(prim_normal<true>(sc.prims[0], pos))) {}
+};
+
+template <>
+struct CollisionLocal<2> {
+  MediumK m;
+  Frame fr;
+  __device__ __forceinline__ CollisionLocal(const SceneDev& sc, V3 pos) {
+    TriSample fs = trilinear<true>(sc.grid.sdf, sc.grid.n_sdf,
+                                   grid_coord(sc.grid, pos, sc.grid.inv_h_sdf), sc.grid.inv_h_sdf);
+    float sg = fmaxf(grid_sigma(sc.grid, pos), 1e-6f);
+    m = grid_medium(sc.media[0], sg, sc.grid.k_xy, sc.grid.k_z);
+    float gn2 = dot3(fs.grad, fs.grad);
+    V3 nrm = gn2 > 0.0f ? mul3(fs.grad, frsqrt(gn2)) : v3(0.0f, 0.0f, 1.0f);
+    fr = frame_about(nrm);
+  }
+};
+
+template <int kMode, bool kMono>
+__global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool_kernel(
     const __grid_constant__ SceneDev sc, const __grid_constant__ PassDev ps) {
   __shared__ PoolSlots<true, kMono> pools[kWarpsPerBlock];
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   PoolSlots<true, kMono>& P = pools[threadIdx.x >> 5];
-  const MediumK& m = sc.media[0];
   Counters cn;
 #pragma unroll
   for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
@@ -1158,10 +1191,12 @@ __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) sphere_pool
       }
     } else if (slot >= 0) {
       pool_load<true, kMono>(P, slot, ps, st, sig_o);
-      // scatter_stages<3> at the stored collision: frame, NEE, phase sample
-      Frame fr = frame_about(prim_normal<true>(sc.prims[0], st.pos));
+      // scatter_stages<kMode> at the stored collision: frame, NEE, phase sample
+      CollisionLocal<kMode> loc(sc, st.pos);
+      const MediumK& m = loc.m;
+      const Frame& fr = loc.fr;
       V3 wo = to_local(fr, st.dir);
-      curved_nee<3>(sc, st, cn, m, fr, wo, sig_o, st.pos);
+      curved_nee<kMode>(sc, st, cn, m, fr, wo, sig_o, st.pos);
       V3 v = neg3(wo);
       float uu = remap_branch_uniform_render(st.u_br, m);
       float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
@@ -1197,19 +1232,19 @@ __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) sphere_pool
     }
     __syncwarp();
     if (fly) {
-      if (!flight_stage<3>(sc, ps, st, cn)) {
+      if (!flight_stage<kMode>(sc, ps, st, cn)) {
         finish(st);
       } else {
-        // the collision's frame and sigma(wo), as scatter_stages<3>
+        // the collision's medium, frame and sigma(wo), as scatter_stages
         st.pos = st.cpos;
-        Frame fr = frame_about(prim_normal<true>(sc.prims[0], st.pos));
-        sig_o = proj_area<kSpecRuntime, true>(m, to_local(fr, st.dir));
+        CollisionLocal<kMode> loc(sc, st.pos);
+        sig_o = proj_area<kSpecRuntime, true>(loc.m, to_local(loc.fr, st.dir));
         cn.v[kStScatters]++;
         if (!(sig_o >= 1e-12f)) {
           cn.v[kStDegenerate]++;
           finish(st);
         } else {
-          tag = st.u_br < m.mix ? kTagBeck : kTagHemi;
+          tag = st.u_br < loc.m.mix ? kTagBeck : kTagHemi;
         }
       }
     }
@@ -1493,7 +1528,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[22] = {};
+  int blocks[24] = {};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1546,10 +1581,14 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_pool<true, false, 1>(&o.blocks[11])));
   MF_CUDA((occ_pool<false, true, 1>(&o.blocks[12])));
   MF_CUDA((occ_pool<true, true, 1>(&o.blocks[13])));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[20], sphere_pool_kernel<false>,
-                                                        kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[21], sphere_pool_kernel<true>,
-                                                        kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[20],
+                                                        curved_pool_kernel<3, false>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[21],
+                                                        curved_pool_kernel<3, true>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[22],
+                                                        curved_pool_kernel<2, false>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[23],
+                                                        curved_pool_kernel<2, true>, kBlock, 0));
   MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
   MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
   MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));
@@ -1699,12 +1738,19 @@ int launch_paths(const SceneDev& sc_in, const PassDev& ps, bool caller_rays, cud
       // bit-exactness test)
       int pk = sc.mono ? 21 : 20;
       grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
-      if (sc.mono) sphere_pool_kernel<true><<<grid, kBlock, 0, st>>>(sc, ps);
-      else sphere_pool_kernel<false><<<grid, kBlock, 0, st>>>(sc, ps);
+      if (sc.mono) curved_pool_kernel<3, true><<<grid, kBlock, 0, st>>>(sc, ps);
+      else curved_pool_kernel<3, false><<<grid, kBlock, 0, st>>>(sc, ps);
     }
   } else {
     if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
-    else path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    else if (megakernel_requested()) path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    else {
+      // the grid-field path pool (MF_MEGAKERNEL=1: the megakernel)
+      int pk = sc.mono ? 23 : 22;
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
+      if (sc.mono) curved_pool_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
+      else curved_pool_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
+    }
   }
   g_launches++;
   MF_CUDA(cudaGetLastError());

@@ -175,3 +175,22 @@ def test_config5_full_grids(cuda):
     assert torch.isfinite(img).all() and (img >= 0).all()
     img2, _ = mf.render_device(sc, 64, 4, max_bounces=64, tile=16)
     assert torch.equal(img, img2)
+
+
+def test_grid_pool_matches_megakernel(cuda, monkeypatch):
+    """The grid-field path pool runs every path with the megakernel's
+    arithmetic and random stream: the same decisions (identical event
+    counts) and the same image to float rounding (a few multiply-adds are
+    contracted differently in the two inlining contexts); the pool itself
+    is deterministic."""
+    sc = configs.config5_scene(64, 48, n_sdf=96, n_sigma=48)
+    a, sa = mf.render_device(sc, 16, 4, max_bounces=64, stats=True)
+    a = a.cpu().numpy()
+    a2, _ = mf.render_device(sc, 16, 4, max_bounces=64, tile=8)
+    assert np.array_equal(a, a2.cpu().numpy())
+    monkeypatch.setenv("MF_MEGAKERNEL", "1")
+    b, sb = mf.render_device(sc, 16, 4, max_bounces=64, stats=True)
+    b = b.cpu().numpy()
+    np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-7)
+    sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
+    assert sa == sb
