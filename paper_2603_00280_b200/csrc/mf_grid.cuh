@@ -37,6 +37,15 @@ MF_HD float ldg(const float* p) {
 #endif
 }
 
+// host-only walk statistics (tools/grid_walk_stats.py builds the host shim
+// with -DMF_GRID_STATS): DDA iterations, tentative collisions, skips, walks
+#if defined(MF_GRID_STATS) && !defined(__CUDA_ARCH__)
+extern long long g_grid_stats[4];
+#define MF_GSTAT(i) (++g_grid_stats[i])
+#else
+#define MF_GSTAT(i) ((void)0)
+#endif
+
 MF_HD int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 struct TriSample {
@@ -216,7 +225,9 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   // fraction of the random numbers and logs
   float tau = -flog(draw());
   int iter = 0;
+  MF_GSTAT(3);
   for (; iter < kGridIterCap; ++iter) {
+    MF_GSTAT(0);
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
     float mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
 #if defined(MF_GRID_DEBUG) && !defined(__CUDA_ARCH__)
@@ -227,6 +238,7 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
       if (tau < need) {
         t += tau / mu;
         w.steps++;
+        MF_GSTAT(1);
         V3 p = fma3(dir, t, pos);
         float f, sg;
         float st = grid_extinction(g, base, p, dir, lo_mult, &f, &sg);
@@ -274,6 +286,7 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
         return w;
       }
       if (tj > t_exit) {
+        MF_GSTAT(2);
         t = tj;
         V3 q = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
         cx = clampi((int)q.x, 0, n - 1);

@@ -379,7 +379,10 @@ __device__ __forceinline__ void camera_ray(const SceneDev& sc, uint32_t px, uint
 constexpr float kShadowRR = MF_SHADOW_RR;
 
 // shadow transmittance from pos towards unit direction wl over distance t_max
-template <int kMode>
+// kSpec: the medium's kind / Fresnel known at compile time (proj_area);
+// kPool: the path-pool kernels, which never run the general walker for a
+// single sphere (MF_GENERIC_WALK selects the megakernel)
+template <int kMode, int kSpec = kSpecRuntime, bool kPool = false>
 __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& st, V3 pos, V3 wl,
                                            float t_max, float h_end, Counters& cn,
                                            float sig_known = -1.0f) {
@@ -395,9 +398,9 @@ __device__ __forceinline__ float shadow_tr(const SceneDev& sc, const PathState& 
     if (w.steps < 0) cn.v[kStCapped]++;   // iteration cap: raised by the host
     return w.steps < 0 ? 0.0f : w.weight;
   } else {
-    WalkResult w = kMode == 3 && !sc.generic_walk
-                       ? sphere_walk(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl, true,
-                                     t_max, kShadowRR)
+    WalkResult w = kMode == 3 && (kPool || !sc.generic_walk)
+                       ? sphere_walk<kSpec>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl,
+                                            true, t_max, kShadowRR)
                        : walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, kCallShadow, pos, wl,
                                           true, t_max, kShadowRR);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
@@ -463,16 +466,16 @@ __device__ __forceinline__ bool scatter_stages(const SceneDev& sc, const PassDev
 // and point light, shadow rays walked in ratio mode): the megakernel's
 // stage 2 and the sphere pool's visits run this one copy, so their images
 // agree bit for bit
-template <int kMode>
+template <int kMode, int kSpec = kSpecRuntime, bool kPool = false>
 __device__ __forceinline__ void curved_nee(const SceneDev& sc, PathState& st, Counters& cn,
                                            const MediumK& m, const Frame& fr, V3 wo, float sig_o,
                                            V3 pos) {
   if (sc.has_sun) {
     V3 wl = to_local(fr, sc.sun_to);
-    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+    V3 ph = phase_eval<kSpec, true>(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr<kMode>(sc, st, pos, sc.sun_to, INFINITY,
+      float tr = shadow_tr<kMode, kSpec, kPool>(sc, st, pos, sc.sun_to, INFINITY,
                                   sc.sun_to.z > 0.0f ? INFINITY : -INFINITY, cn, sc.sun_sig);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.sun_L.x * tr, st.T.y * ph.y * sc.sun_L.y * tr,
                            st.T.z * ph.z * sc.sun_L.z * tr));
@@ -484,10 +487,10 @@ __device__ __forceinline__ void curved_nee(const SceneDev& sc, PathState& st, Co
     float ir = frsqrt(r2);
     V3 wlw = mul3(d, ir);
     V3 wl = to_local(fr, wlw);
-    V3 ph = phase_eval<kSpecRuntime, true>(m, wo, wl, sig_o);
+    V3 ph = phase_eval<kSpec, true>(m, wo, wl, sig_o);
     if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
       cn.v[kStNee]++;
-      float tr = shadow_tr<kMode>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
+      float tr = shadow_tr<kMode, kSpec, kPool>(sc, st, pos, wlw, r2 * ir, sc.point_pos.z - sc.prims[0].z0, cn);
       float s = tr * frcp(r2);
       st.L = add3(st.L, v3(st.T.x * ph.x * sc.point_I.x * s, st.T.y * ph.y * sc.point_I.y * s,
                            st.T.z * ph.z * sc.point_I.z * s));
@@ -502,7 +505,7 @@ __device__ __forceinline__ void curved_nee(const SceneDev& sc, PathState& st, Co
 // kMode: 0 single plane (analytic), 1 general shells (tracking), 2 grid field
 // kNeedPos (single plane): 1 / 0 when the caller knows at compile time
 // whether a point light reads positions, -1 to ask the scene
-template <int kMode, int kSpec = kSpecRuntime, int kNeedPos = -1>
+template <int kMode, int kSpec = kSpecRuntime, int kNeedPos = -1, bool kPool = false>
 __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& ps, PathState& st,
                                              Counters& cn) {
   cn.v[kStSegments]++;
@@ -532,9 +535,9 @@ __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& 
     st.lphi = fl.lphi;
     outcome = fl.outcome;
   } else {
-    WalkResult w = kMode == 3 && !sc.generic_walk
-                       ? sphere_walk(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir, false,
-                                     INFINITY)
+    WalkResult w = kMode == 3 && (kPool || !sc.generic_walk)
+                       ? sphere_walk<kSpec>(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir,
+                                            false, INFINITY)
                        : walk<kMode == 3>(sc, st.rng, (uint32_t)st.bounce, 1u, st.pos, st.dir,
                                           false, INFINITY);
     cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
@@ -1136,7 +1139,7 @@ struct CollisionLocal<2> {
   }
 };
 
-template <int kMode, bool kMono>
+template <int kMode, bool kMono, int kSpec>
 __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool_kernel(
     const __grid_constant__ SceneDev sc, const __grid_constant__ PassDev ps) {
   __shared__ PoolSlots<true, kMono> pools[kWarpsPerBlock];
@@ -1196,10 +1199,11 @@ __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool
       const MediumK& m = loc.m;
       const Frame& fr = loc.fr;
       V3 wo = to_local(fr, st.dir);
-      curved_nee<kMode>(sc, st, cn, m, fr, wo, sig_o, st.pos);
+      curved_nee<kMode, kSpec, true>(sc, st, cn, m, fr, wo, sig_o, st.pos);
       V3 v = neg3(wo);
       float uu = remap_branch_uniform_render(st.u_br, m);
-      float sig_b = m.kind == kBeckmann ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
+      float sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann))
+                        ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
       V3 wm;
       float vm;
       if (stage == kStageBeck && sig_b > 1e-12f) {
@@ -1211,7 +1215,7 @@ __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool
         wm = hemisphere_about(v, uu, st.u_s2);
         vm = uu;
       }
-      PhaseSample smp = phase_sample_tail<kSpecRuntime, true>(m, v, wm, vm, sig_o, sig_b,
+      PhaseSample smp = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b,
                                                               sig_b > 1e-12f);
       st.dir = to_world(fr, smp.wi);
       st.T = v3(st.T.x * smp.weight.x, st.T.y * smp.weight.y, st.T.z * smp.weight.z);
@@ -1232,13 +1236,13 @@ __global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool
     }
     __syncwarp();
     if (fly) {
-      if (!flight_stage<kMode>(sc, ps, st, cn)) {
+      if (!flight_stage<kMode, kSpec, -1, true>(sc, ps, st, cn)) {
         finish(st);
       } else {
         // the collision's medium, frame and sigma(wo), as scatter_stages
         st.pos = st.cpos;
         CollisionLocal<kMode> loc(sc, st.pos);
-        sig_o = proj_area<kSpecRuntime, true>(loc.m, to_local(loc.fr, st.dir));
+        sig_o = proj_area<kSpec, true>(loc.m, to_local(loc.fr, st.dir));
         cn.v[kStScatters]++;
         if (!(sig_o >= 1e-12f)) {
           cn.v[kStDegenerate]++;
@@ -1528,7 +1532,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[24] = {};
+  int blocks[28] = {};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1540,6 +1544,31 @@ cudaError_t occ_pool(int* blocks) {
 template <bool kPoint, bool kMono, int kSpec>
 void launch_pool(int grid, const SceneDev& sc, const PassDev& ps, cudaStream_t st) {
   pool_kernel<kPoint, kMono, kSpec><<<grid, kBlock, 0, st>>>(sc, ps);
+}
+
+template <int kMode, bool kMono, int kSpec>
+cudaError_t occ_curved(int* blocks) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks,
+                                                       curved_pool_kernel<kMode, kMono, kSpec>,
+                                                       kBlock, 0);
+}
+
+// the curved pool (one sphere: kMode 3, grid field: kMode 2) for the scene:
+// kSpec 1 when the medium is GENERALIZED with albedo Fresnel (the grid
+// field's local media always are GENERALIZED), which folds the NDF /
+// projected-area / Fresnel dispatch away
+void launch_curved_pool(int mode, const SceneDev& sc, const PassDev& ps, const Occupancy& occ,
+                        int64_t need, cudaStream_t st) {
+  bool gen = mode == 2 || sc.media[0].kind == kGeneralized;
+  int spec = gen && sc.media[0].fresnel == kAlbedo ? 1 : 0;
+  int pk = 20 + (mode == 2 ? 2 : 0) + (sc.mono ? 1 : 0) + 4 * spec;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
+  using K = void (*)(SceneDev, PassDev);
+  static const K ks[8] = {curved_pool_kernel<3, false, 0>, curved_pool_kernel<3, true, 0>,
+                          curved_pool_kernel<2, false, 0>, curved_pool_kernel<2, true, 0>,
+                          curved_pool_kernel<3, false, 1>, curved_pool_kernel<3, true, 1>,
+                          curved_pool_kernel<2, false, 1>, curved_pool_kernel<2, true, 1>};
+  ks[pk - 20]<<<grid, kBlock, 0, st>>>(sc, ps);
 }
 
 int device_occupancy(Occupancy* occ) {
@@ -1581,14 +1610,15 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_pool<true, false, 1>(&o.blocks[11])));
   MF_CUDA((occ_pool<false, true, 1>(&o.blocks[12])));
   MF_CUDA((occ_pool<true, true, 1>(&o.blocks[13])));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[20],
-                                                        curved_pool_kernel<3, false>, kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[21],
-                                                        curved_pool_kernel<3, true>, kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[22],
-                                                        curved_pool_kernel<2, false>, kBlock, 0));
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[23],
-                                                        curved_pool_kernel<2, true>, kBlock, 0));
+  // curved pools: blocks[20 + 2 (mode == 2) + mono + 4 spec]
+  MF_CUDA((occ_curved<3, false, 0>(&o.blocks[20])));
+  MF_CUDA((occ_curved<3, true, 0>(&o.blocks[21])));
+  MF_CUDA((occ_curved<2, false, 0>(&o.blocks[22])));
+  MF_CUDA((occ_curved<2, true, 0>(&o.blocks[23])));
+  MF_CUDA((occ_curved<3, false, 1>(&o.blocks[24])));
+  MF_CUDA((occ_curved<3, true, 1>(&o.blocks[25])));
+  MF_CUDA((occ_curved<2, false, 1>(&o.blocks[26])));
+  MF_CUDA((occ_curved<2, true, 1>(&o.blocks[27])));
   MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
   MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
   MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));
@@ -1736,20 +1766,14 @@ int launch_paths(const SceneDev& sc_in, const PassDev& ps, bool caller_rays, cud
     else {
       // the sphere path pool (MF_MEGAKERNEL=1: the megakernel, for the
       // bit-exactness test)
-      int pk = sc.mono ? 21 : 20;
-      grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
-      if (sc.mono) curved_pool_kernel<3, true><<<grid, kBlock, 0, st>>>(sc, ps);
-      else curved_pool_kernel<3, false><<<grid, kBlock, 0, st>>>(sc, ps);
+      launch_curved_pool(3, sc, ps, occ, need, st);
     }
   } else {
     if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else if (megakernel_requested()) path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
     else {
       // the grid-field path pool (MF_MEGAKERNEL=1: the megakernel)
-      int pk = sc.mono ? 23 : 22;
-      grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
-      if (sc.mono) curved_pool_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
-      else curved_pool_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
+      launch_curved_pool(2, sc, ps, occ, need, st);
     }
   }
   g_launches++;

@@ -95,8 +95,9 @@ struct SceneDev {
 // constant, or the lat-long map bilinear in (phi, theta) with phi wrapped
 // and theta clamped, texel centres at half-integers -- the reference's
 // formula in float32.
-MF_HD V3 env_radiance(const SceneDev& sc, V3 d) {
-  if (!sc.env_map) return sc.env;
+// lat-long map lookup, out of line: one copy, off the instruction stream of
+// the hot render loops (constant environments never call it)
+MF_COLD V3 env_map_radiance(const SceneDev& sc, V3 d) {
   const float kPi = 3.14159265358979f;
   float th = acosf(fminf(fmaxf(d.z, -1.0f), 1.0f));
   float ph = atan2f(d.y, d.x);
@@ -121,6 +122,10 @@ MF_HD V3 env_radiance(const SceneDev& sc, V3 d) {
            ldg(m + ((size_t)y1m * w + x1m) * 3 + k) * w11;
   }
   return v3(c[0], c[1], c[2]);
+}
+
+MF_HD V3 env_radiance(const SceneDev& sc, V3 d) {
+  return sc.env_map ? env_map_radiance(sc, d) : sc.env;
 }
 
 // ---------------------------------------------------------------------------
@@ -696,14 +701,16 @@ MF_WALK_FN WalkResult walk(const SceneDev& sc, PathRng rng, uint32_t segment,
 // a constant majorant over a sigma-long window.
 constexpr float kSphereGmin = 1e-3f;
 
-template <bool kFast = true>
+template <bool kFast = true, int kSpec = kSpecRuntime>
 MF_HD float sphere_sigma_dir(const MediumK& m, float g) {
   // Sigma(cos theta): sigma(w) of a local direction with w.z = g
   float sn = fsqrt(fmaxf(1.0f - g * g, 0.0f));
-  return m.kind == kGGX ? proj_area_ggx(v3(sn, 0.0f, g), m.ax, m.ay)
+  return kSpec == kSpecRuntime && m.kind == kGGX ? proj_area_ggx(v3(sn, 0.0f, g), m.ax, m.ay)
                         : proj_area_erf<kFast>(v3(sn, 0.0f, g), m.ax, m.ay, m.az);
 }
 
+// kSpec (see proj_area): the medium's NDF kind known at compile time
+template <int kSpec = kSpecRuntime>
 MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segment,
                                   uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
                                   float rr_min = 0.0f) {
@@ -772,7 +779,7 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
     // majorant of the chord from here: Sigma at its start times rho of the
     // tangent line (the 1.0001 absorbs float rounding of f, g along radial
     // chords, where the bound is tight)
-    float sig0 = (mx.area_monotone ? sphere_sigma_dir(m, g) : mx.sig_max) * mscale;
+    float sig0 = (mx.area_monotone ? sphere_sigma_dir<true, kSpec>(m, g) : mx.sig_max) * mscale;
     float tau = -flog(draw());
     w.steps++;
     float t1, mubar1;
@@ -833,7 +840,7 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
     float g1 = fminf(fmaxf(dot3(oc1, dir) * ir1, -1.0f), 1.0f);
     float mu = 0.0f;
     if (f1 >= lo && f1 <= hi) {
-      float sg = mx.area_monotone ? sphere_sigma_dir(m, g1)
+      float sg = mx.area_monotone ? sphere_sigma_dir<true, kSpec>(m, g1)
                                   : proj_area_outlined(m.kind, m.ax, m.ay, m.az,
                                                        to_local(frame_about(mul3(oc1, ir1)), dir));
       mu = mills<true>(f1 * is) * is * sg;

@@ -210,3 +210,11 @@ int mfh_grid_probe(const mf_scene* scene, const float* p, const float* dir, int6
 extern "C" {
 float mfh_u01(uint32_t bits) { return u01(bits); }
 }
+
+#ifdef MF_GRID_STATS
+// walk statistics of the grid walker (tools/grid_walk_stats.py only)
+namespace mf {
+long long g_grid_stats[4];
+}
+extern "C" long long* mfh_grid_stats() { return mf::g_grid_stats; }
+#endif
