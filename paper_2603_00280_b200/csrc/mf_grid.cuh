@@ -40,7 +40,7 @@ MF_HD float ldg(const float* p) {
 // host-only walk statistics (tools/grid_walk_stats.py builds the host shim
 // with -DMF_GRID_STATS): DDA iterations, tentative collisions, skips, walks
 #if defined(MF_GRID_STATS) && !defined(__CUDA_ARCH__)
-extern long long g_grid_stats[4];
+extern long long g_grid_stats[8];
 #define MF_GSTAT(i) (++g_grid_stats[i])
 #else
 #define MF_GSTAT(i) ((void)0)
@@ -117,6 +117,10 @@ MF_HD MediumK grid_medium(const MediumK& base, float sigma, float k_xy, float k_
   return m;
 }
 
+#ifndef MF_GRID_ISO_AREA
+#define MF_GRID_ISO_AREA 1
+#endif
+
 // extinction at p along dir; 0 outside the region [lo_mult sigma, 3 sigma].
 // Also reports f and sigma (for the absorption rule).
 MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir, float lo_mult,
@@ -127,11 +131,19 @@ MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir,
   *s_out = sg;
   if (fs.v < lo_mult * sg || fs.v > 3.0f * sg) return 0.0f;
   float gn2 = dot3(fs.grad, fs.grad);
+  float ax = g.k_xy * sg, az = g.k_z * sg;
+#if MF_GRID_ISO_AREA
+  // alpha_x = alpha_y: sigma(w) depends on the local w.z = <n, dir> alone,
+  // so the local frame is not needed -- sigma at (sqrt(1 - c^2), 0, c)
+  float c = gn2 > 0.0f ? dot3(fs.grad, dir) * frsqrt(gn2) : dir.z;
+  c = fminf(fmaxf(c, -1.0f), 1.0f);
+  float area = proj_area_erf<true>(v3(fsqrt(fmaxf(1.0f - c * c, 0.0f)), 0.0f, c), ax, ax, az);
+#else
   V3 n = gn2 > 0.0f ? mul3(fs.grad, frsqrt(gn2)) : v3(0.0f, 0.0f, 1.0f);
   Frame fr = frame_about(n);
   V3 wl = to_local(fr, dir);
-  float ax = g.k_xy * sg, az = g.k_z * sg;
   float area = proj_area_erf<true>(wl, ax, ax, az);   // render walks: MUFU exp2
+#endif
   (void)base;
   return mills<true>(fs.v * frcp(sg)) * frcp(sg) * area;
 }
@@ -167,46 +179,29 @@ MF_HD bool grid_box(const GridDev& g, V3 o, V3 d, float* t0, float* t1) {
   return ta <= tb;
 }
 
-// Delta (ratio == false) or ratio tracking through the majorant grid.
+// Delta (ratio == false) or ratio tracking through the majorant grid, as a
+// resumable walker: dda() advances the 3D DDA over the majorant cells until
+// the next tentative collision (or the end of the walk), tentative()
+// evaluates the extinction there and takes the tracking decision.  The
+// per-lane arithmetic and random-number consumption are those of one
+// sequential loop, whichever driver runs the two halves.
 // Random draws: blocks (segment, call0 + k) of the path's Philox stream.
 template <typename RngBlock>
-MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_block,
-                         uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
-                         float rr_min = 0.0f) {
+struct GridWalker {
+  RngBlock rng_block;
   GridWalk w;
-  w.outcome = 0;
-  w.pos = pos;
-  w.weight = 1.0f;
-  w.steps = 0;
-  w.violations = 0;
-  float lo_mult = ratio ? -3.0f : -6.0f;
-  float t0, t1;
-  if (!grid_box(g, pos, dir, &t0, &t1)) return w;
-  t1 = fminf(t1, t_max);
-  float t = t0;
-  // DDA setup in majorant-cell coordinates
-  V3 gc = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
-  int n = g.n_maj;
-  int cx = clampi((int)gc.x, 0, n - 1), cy = clampi((int)gc.y, 0, n - 1),
-      cz = clampi((int)gc.z, 0, n - 1);
-  int sx = dir.x > 0.0f ? 1 : -1, sy = dir.y > 0.0f ? 1 : -1, sz = dir.z > 0.0f ? 1 : -1;
-  float idx = 1.0f / dir.x, idy = 1.0f / dir.y, idz = 1.0f / dir.z;
-  // parametric distance to the next cell wall on each axis
-  auto wall = [&](int c, int s, float bmin, float h, float o, float id) {
-    float x = bmin + h * (float)(c + (s > 0 ? 1 : 0));
-    float tw = (x - o) * id;
-    return isfinite(tw) ? tw : INFINITY;
-  };
-  float tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
-  float ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
-  float tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
-  float dtx = isfinite(idx) ? fabsf(g.h_maj.x * idx) : INFINITY;
-  float dty = isfinite(idy) ? fabsf(g.h_maj.y * idy) : INFINITY;
-  float dtz = isfinite(idz) ? fabsf(g.h_maj.z * idz) : INFINITY;
-  U4 bits = U4{0, 0, 0, 0};
-  int avail = 0;
-  uint32_t call = call0;
-  auto draw = [&]() {
+  V3 pos, dir;
+  float t, t1, tau, lo_mult, rr_min;
+  float tx, ty, tz, dtx, dty, dtz, idx, idy, idz, mu;
+  int cx, cy, cz, sx, sy, sz, iter;
+  bool ratio;
+  U4 bits;
+  int avail;
+  uint32_t call;
+
+  MF_HDM GridWalker(RngBlock rb) : rng_block(rb) {}
+
+  MF_HDM float draw() {
     if (avail == 0) {
       bits = rng_block(call++);
       avail = 4;
@@ -217,112 +212,191 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
     bits.z = bits.w;
     --avail;
     return u;
-  };
-  // optical depth left to the next tentative collision: sampled once per
-  // tentative and used up cell by cell (tau -= mu dt), instead of a fresh
-  // exponential (a uniform and a log) in every cell the ray crosses -- the
-  // same process (the majorant is piecewise constant along the ray), a
-  // fraction of the random numbers and logs
-  float tau = -flog(draw());
-  int iter = 0;
-  MF_GSTAT(3);
-  for (; iter < kGridIterCap; ++iter) {
+  }
+
+  // parametric distance to the next cell wall on one axis
+  MF_HDM static float wall(int c, int s, float bmin, float h, float o, float id) {
+    float x = bmin + h * (float)(c + (s > 0 ? 1 : 0));
+    float tw = (x - o) * id;
+    return isfinite(tw) ? tw : INFINITY;
+  }
+
+  MF_HDM void locate(const GridDev& g) {
+    V3 q = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
+    int n = g.n_maj;
+    cx = clampi((int)q.x, 0, n - 1);
+    cy = clampi((int)q.y, 0, n - 1);
+    cz = clampi((int)q.z, 0, n - 1);
+    tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
+    ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
+    tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
+  }
+
+  // false: the ray misses the grid (escaped at once)
+  MF_HDM bool begin(const GridDev& g, uint32_t call0, V3 p0, V3 d, bool ratio_walk, float t_max,
+                   float rr) {
+    w.outcome = 0;
+    w.pos = p0;
+    w.weight = 1.0f;
+    w.steps = 0;
+    w.violations = 0;
+    pos = p0;
+    dir = d;
+    ratio = ratio_walk;
+    rr_min = rr;
+    lo_mult = ratio ? -3.0f : -6.0f;
+    avail = 0;
+    call = call0;
+    bits = U4{0, 0, 0, 0};
+    iter = 0;
+    float t0;
+    if (!grid_box(g, pos, dir, &t0, &t1)) return false;
+    t1 = fminf(t1, t_max);
+    t = t0;
+    sx = dir.x > 0.0f ? 1 : -1;
+    sy = dir.y > 0.0f ? 1 : -1;
+    sz = dir.z > 0.0f ? 1 : -1;
+    idx = 1.0f / dir.x;
+    idy = 1.0f / dir.y;
+    idz = 1.0f / dir.z;
+    locate(g);
+    dtx = isfinite(idx) ? fabsf(g.h_maj.x * idx) : INFINITY;
+    dty = isfinite(idy) ? fabsf(g.h_maj.y * idy) : INFINITY;
+    dtz = isfinite(idz) ? fabsf(g.h_maj.z * idz) : INFINITY;
+    // optical depth left to the next tentative collision: sampled once per
+    // tentative and used up cell by cell (tau -= mu dt), instead of a fresh
+    // exponential (a uniform and a log) in every cell the ray crosses -- the
+    // same process (the majorant is piecewise constant along the ray), a
+    // fraction of the random numbers and logs
+    tau = -flog(draw());
+    MF_GSTAT(3);
+    return true;
+  }
+
+  MF_HDM void end_at(float te) { w.pos = fma3(dir, te, pos); }
+
+  // One loop iteration of the DDA.  Returns 1 when a tentative collision
+  // lies in the current cell (t is advanced to it; call tentative()), 2 when
+  // the walk has ended (w is final), 0 otherwise.
+  MF_HDM int dda(const GridDev& g) {
+    if (iter >= kGridIterCap) {
+      // iteration cap (transport.py:297 raises): a distinct result, counted
+      // by the callers as capped, never taken for an escape
+      end_at(t);
+      w.outcome = 1;
+      w.weight = 0.0f;
+      w.steps = -1;
+      return 2;
+    }
+    ++iter;
     MF_GSTAT(0);
+    int n = g.n_maj;
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
-    float mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
-#if defined(MF_GRID_DEBUG) && !defined(__CUDA_ARCH__)
-    printf("it %d t %g cell %d %d %d mu %g tx %g ty %g tz %g t1 %g\n", iter, t, cx, cy, cz, mu, tx, ty, tz, t1);
-#endif
+    mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
     if (mu > 0.0f) {
       float need = mu * (t_exit - t);
       if (tau < need) {
         t += tau / mu;
-        w.steps++;
-        MF_GSTAT(1);
-        V3 p = fma3(dir, t, pos);
-        float f, sg;
-        float st = grid_extinction(g, base, p, dir, lo_mult, &f, &sg);
-        if (st > mu * 1.00001f) w.violations++;
-        if (ratio) {
-          w.weight *= fmaxf(1.0f - st / mu, 0.0f);
-          if (w.weight < rr_min && w.weight > 0.0f) {
-            // Russian roulette on the weight (see walk() in mf_transport.cuh)
-            float ur = draw();
-            w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
-          }
-          if (!(w.weight > 0.0f)) {
-            w.pos = p;
-            return w;
-          }
-        } else {
-          if (f < -6.0f * sg) {
-            w.outcome = 1;   // absorbed below the depth cap
-            w.pos = p;
-            return w;
-          }
-          if (draw() * mu < st) {
-            w.outcome = 2;
-            w.pos = p;
-            return w;
-          }
-        }
-        tau = -flog(draw());
-        continue;
+        return 1;
       }
       tau -= need;
+      MF_GSTAT(4);
     }
     // leave the cell
     if (t_exit >= t1) {
-      w.pos = fma3(dir, t1, pos);
-      return w;   // escaped the grid (or reached the light)
+      end_at(t1);
+      return 2;   // escaped the grid (or reached the light)
     }
     if (mu <= -2.0f) {
       // empty space: jump (D - 1) cells in every axis, then restart the DDA
-      // (stepping the cheap DDA and the costly tentative collisions in
-      // separate re-converged loops was measured slower: 4.4 vs 3.2 ms)
       float tj = t + (-mu - 1.0f) * fminf(fminf(dtx, dty), dtz);
       if (tj >= t1) {
-        w.pos = fma3(dir, t1, pos);
-        return w;
+        end_at(t1);
+        return 2;
       }
       if (tj > t_exit) {
         MF_GSTAT(2);
         t = tj;
-        V3 q = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
-        cx = clampi((int)q.x, 0, n - 1);
-        cy = clampi((int)q.y, 0, n - 1);
-        cz = clampi((int)q.z, 0, n - 1);
-        tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
-        ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
-        tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
-        continue;
+        locate(g);
+        return 0;
       }
     }
     t = t_exit;
+    bool out;
     if (tx <= ty && tx <= tz) {
       cx += sx;
       tx += dtx;
-      if (cx < 0 || cx >= n) break;
+      out = cx < 0 || cx >= n;
     } else if (ty <= tz) {
       cy += sy;
       ty += dty;
-      if (cy < 0 || cy >= n) break;
+      out = cy < 0 || cy >= n;
     } else {
       cz += sz;
       tz += dtz;
-      if (cz < 0 || cz >= n) break;
+      out = cz < 0 || cz >= n;
     }
+    if (out) {
+      end_at(t);
+      return 2;
+    }
+    return 0;
   }
-  w.pos = fma3(dir, t, pos);
-  if (iter >= kGridIterCap) {
-    // iteration cap (transport.py:297 raises): a distinct result, counted
-    // by the callers as capped, never taken for an escape
-    w.outcome = 1;
-    w.weight = 0.0f;
-    w.steps = -1;
+
+  // The tentative collision at t (majorant mu): true when the walk ends.
+  MF_HDM bool tentative(const GridDev& g, const MediumK& base) {
+    w.steps++;
+    MF_GSTAT(1);
+    V3 p = fma3(dir, t, pos);
+    float f, sg;
+    float st = grid_extinction(g, base, p, dir, lo_mult, &f, &sg);
+    if (st > mu * 1.00001f) w.violations++;
+    if (ratio) {
+      w.weight *= fmaxf(1.0f - st / mu, 0.0f);
+      if (w.weight < rr_min && w.weight > 0.0f) {
+        // Russian roulette on the weight (see walk() in mf_transport.cuh)
+        float ur = draw();
+        w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
+      }
+      if (!(w.weight > 0.0f)) {
+        w.pos = p;
+        return true;
+      }
+    } else {
+      if (f < -6.0f * sg) {
+        w.outcome = 1;   // absorbed below the depth cap
+        w.pos = p;
+        return true;
+      }
+      if (draw() * mu < st) {
+        w.outcome = 2;
+        w.pos = p;
+        return true;
+      }
+    }
+    tau = -flog(draw());
+    return false;
   }
-  return w;
+};
+
+// The driver: one lane walks on its own.  (A warp-batched driver -- lanes
+// step their DDAs and evaluate the tentative collisions together once half
+// of the walking lanes have one pending -- gave bit-identical images but
+// was slower on config 5: 4.6 - 6.6 ms for batch fractions 0.3 - 1 against
+// 3.56 ms.)
+template <typename RngBlock>
+MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_block,
+                         uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
+                         float rr_min = 0.0f) {
+  GridWalker<RngBlock> W(rng_block);
+  if (!W.begin(g, call0, pos, dir, ratio, t_max, rr_min)) return W.w;
+  while (true) {
+    int r = W.dda(g);
+    if (r == 2 || (r == 1 && W.tentative(g, base))) break;
+  }
+  return W.w;
 }
+
 
 // ---------------------------------------------------------------------------
 // empty-space distances (second pass of mf_grid_majorant)

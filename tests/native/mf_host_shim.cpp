@@ -214,7 +214,7 @@ float mfh_u01(uint32_t bits) { return u01(bits); }
 #ifdef MF_GRID_STATS
 // walk statistics of the grid walker (tools/grid_walk_stats.py only)
 namespace mf {
-long long g_grid_stats[4];
+long long g_grid_stats[8];
 }
 extern "C" long long* mfh_grid_stats() { return mf::g_grid_stats; }
 #endif

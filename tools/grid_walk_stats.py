@@ -57,14 +57,15 @@ def walk(O, D, ratio, rr=0.0):
     pos = np.zeros((3, n), np.float32)
     w = np.zeros(n, np.float32)
     v = ctypes.c_int64()
-    for i in range(4):
+    for i in range(8):
         gs[i] = 0
     assert lib.mfh_walk(ctypes.byref(cs), O.ctypes.data_as(ctypes.c_void_p),
                         D.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(n), ctypes.c_uint64(4),
                         int(ratio), st.ctypes.data_as(ctypes.c_void_p),
                         pos.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p),
                         ctypes.c_float(1.0), ctypes.byref(v), ctypes.c_float(rr)) == 0
-    it, tent, skip, walks = (gs[i] for i in range(4))
+    it, tent, skip, walks, med = (gs[i] for i in range(5))
+    print(f"   medium-cell crossings/walk {med / max(walks, 1):.2f}")
     return st, pos, w, v.value, it / max(walks, 1), tent / max(walks, 1), skip / max(walks, 1), walks
 
 
@@ -76,5 +77,18 @@ sun = np.array([1.0, -1.0, 2.0]); sun /= np.linalg.norm(sun)
 P = np.ascontiguousarray(pos[:, hit], np.float32)
 S = np.ascontiguousarray(np.tile(sun, (P.shape[1], 1)).T, np.float32)
 _, _, w2, viol2, it2, tent2, skip2, nw2 = walk(P, S, True, 0.05)
-print(f"shadow walks {nw2}: mean Tr {w2.mean():.3f}  iters/walk {it2:.1f}  "
+print(f"shadow walks {nw2}: mean Tr {w2.astype(np.float64).mean():.9f}  iters/walk {it2:.1f}  "
       f"tentatives/walk {tent2:.2f}  skips/walk {skip2:.2f}  viol {viol2}")
+
+if os.environ.get("MF_GSTAT_HIST"):
+    h = 3.2 / n_maj
+    m = maj[maj > 0] * h
+    for q in (0.01, 0.03, 0.1, 0.3, 1.0, 3.0):
+        print(f"  cells with mu*h < {q}: {np.mean(m < q):.3f}")
+    M = maj.reshape(n_maj, n_maj, n_maj)
+    for b in (2, 4):
+        nb = n_maj // b
+        bm = np.clip(M, 0, None).reshape(nb, b, nb, b, nb, b).max(axis=(1, 3, 5))
+        bt = bm * h * b
+        print(f"  {b}^3 bricks: medium {np.mean(bm > 0):.3f}; thin (mu_max*size < 0.1) "
+              f"{np.mean((bt > 0) & (bt < 0.1)):.3f}, < 0.3 {np.mean((bt > 0) & (bt < 0.3)):.3f}")
