@@ -1522,11 +1522,43 @@ int slope_table(const float** out, cudaStream_t st) {
   return MF_OK;
 }
 
+// The render kernels' sigma(w) tables (area_q_build), one per distinct
+// roughness triple and device, uploaded once and kept for the process.
+int area_table(const MediumK& m, const float4** out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, float, float, float, int>, const float4*> cache;
+  int dev = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  auto key = std::make_tuple(m.kind, m.ax, m.ay, m.az, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::vector<float4> q(kAreaQN);
+    float4* d = nullptr;
+    if (area_q_build(m, q.data())) {
+      MF_CUDA(cudaMalloc((void**)&d, kAreaQN * sizeof(float4)));
+      MF_CUDA(cudaMemcpy(d, q.data(), kAreaQN * sizeof(float4), cudaMemcpyHostToDevice));
+    }
+    it = cache.emplace(key, d).first;
+  }
+  *out = it->second;
+  return MF_OK;
+}
+
 int attach_slope_table(SceneDev* sc, cudaStream_t st) {
   const float* tab = nullptr;
   int rc = slope_table(&tab, st);
   if (rc) return rc;
   for (int j = 0; j < kMaxPrims; ++j) sc->media[j].slope_tab = tab;
+  // sigma(w) tables for the render kernels (not for grid fields, whose
+  // roughness follows sigma(p))
+  const char* e = std::getenv("MF_AREA_TABLE");   // =0: the formula (A/B test hook)
+  if (!sc->has_grid && !(e && e[0] == '0')) {
+    for (int j = 0; j < sc->n_prims && j < kMaxPrims; ++j) {
+      rc = area_table(sc->media[j], &sc->media[j].area_q);
+      if (rc) return rc;
+    }
+  }
   return MF_OK;
 }
 

@@ -74,6 +74,81 @@ inline void direction_factors(const MediumK& m, float* sig_max, int* monotone) {
   *monotone = mono;
 }
 
+// sigma(w) (ndf.py:156-164) in float64 of an azimuthally symmetric erf-family
+// medium at w.z = z: sigma = s/2 e^{-a^2} ierfcx(|a|) (+ |z| for z < 0),
+// s^2 = ax^2 (1 - z^2) + az^2 z^2, a = z / s, ierfcx(x) = 1/sqrt(pi) -
+// x erfcx(x); erfcx from erfc in float64 (|a| <= 26 keeps e^{a^2} erfc(a)
+// finite; beyond, the asymptotic series)
+inline double proj_area_iso_f64(double z, double ax, double az) {
+  double s = std::sqrt(std::max(ax * ax * (1.0 - z * z) + az * az * z * z, 0.0));
+  if (!(s > 0.0)) return std::max(-z, 0.0);
+  double a = z / s, x = std::fabs(a);
+  double ex;
+  if (x < 26.0) {
+    ex = std::exp(x * x) * std::erfc(x);
+  } else {
+    double r = 1.0 / (2.0 * x * x);
+    ex = (1.0 - r * (1.0 - 3.0 * r * (1.0 - 5.0 * r))) / (x * 1.7724538509055160273);
+  }
+  double v = 0.5 * s * std::exp(-x * x) * (0.56418958354775628695 - x * ex);
+  return a >= 0.0 ? v : v - z;
+}
+
+// The render kernels' table of sigma(w) for an azimuthally symmetric
+// GENERALIZED medium (ax == ay, az > 0: sigma depends on z = w.z alone):
+// per piece i of kAreaQN over z in [-1, 1], the cubic through
+// R(z) = log2 sigma(z) + [z > 0] a(z)^2 log2(e) at t = 0, 1/3, 2/3, 1 of the
+// piece.  Dividing out the Gaussian factor e^{-a^2} of the upper
+// hemisphere (which area_q_eval puts back exactly) leaves a smooth R; the
+// table is kept only when area_q_eval reproduces the float64 sigma to
+// 1e-6 + 1.2e-7 (a^2 + |d ln sigma / dz|) relative -- the fp32 rounding of
+// the exponent (the formula's MUFU exp2 path has it as well) and of z
+// itself -- at eight further points per piece, else false (the kernels
+// use the formula).
+inline bool area_q_build(const MediumK& m, float4* q) {
+  if (m.kind != kGeneralized || m.ax != m.ay || !(m.az > 0.0f)) return false;
+  const double ax = m.ax, az = m.az;
+  auto a2 = [&](double z) {
+    double s2 = ax * ax * (1.0 - z * z) + az * az * z * z;
+    return z * z / s2;
+  };
+  auto R = [&](double z) {
+    double v = proj_area_iso_f64(z, ax, az);
+    return (v > 0.0 && std::isfinite(v)) ? std::log2(v) + (z > 0.0 ? a2(z) * 1.4426950408889634 : 0.0)
+                                         : NAN;
+  };
+  const double h = 2.0 / kAreaQN;
+  for (int i = 0; i < kAreaQN; ++i) {
+    double z0 = -1.0 + h * i;
+    double l[4];
+    for (int k = 0; k < 4; ++k) {
+      l[k] = R(k == 3 ? -1.0 + h * (i + 1) : z0 + h * k / 3.0);
+      if (!std::isfinite(l[k])) return false;
+    }
+    // monomial coefficients of the cubic through (0, l0) (1/3, l1) (2/3, l2) (1, l3)
+    double c0 = l[0];
+    double c1 = (-11.0 * l[0] + 18.0 * l[1] - 9.0 * l[2] + 2.0 * l[3]) / 2.0;
+    double c2 = (18.0 * l[0] - 45.0 * l[1] + 36.0 * l[2] - 9.0 * l[3]) / 2.0;
+    double c3 = (-9.0 * l[0] + 27.0 * l[1] - 27.0 * l[2] + 9.0 * l[3]) / 2.0;
+    q[i] = float4{(float)c0, (float)c1, (float)c2, (float)c3};
+  }
+  // check the device evaluation (host build of area_q_eval) at 8 points per piece
+  for (int i = 0; i < kAreaQN; ++i) {
+    for (int k = 1; k <= 8; ++k) {
+      float z = (float)(-1.0 + h * (i + (k - 0.5) / 8.0));
+      double ex = proj_area_iso_f64(z, ax, az);
+      double got = area_q_eval(q, z, m.ax, m.az);
+      // + the conditioning: sigma's response to a rounding of z itself
+      double dz = 1e-6;
+      double dl = std::fabs(std::log(proj_area_iso_f64(std::min(1.0, z + dz), ax, az) /
+                                     proj_area_iso_f64(std::max(-1.0, z - dz), ax, az))) / (2.0 * dz);
+      double tol = 1e-6 + 1.2e-7 * (z > 0.0f ? a2(z) : 0.0) + 1.2e-7 * dl;
+      if (!(std::fabs(got / ex - 1.0) <= tol)) return false;
+    }
+  }
+  return true;
+}
+
 inline int build_scene(const mf_scene& in, SceneDev* out, std::string* err) {
   if (in.n_prims < 0 || in.n_prims > MF_MAX_PRIMS)
     return (*err = std::string("n_prims out of range"), MF_ERR_PARAM);
