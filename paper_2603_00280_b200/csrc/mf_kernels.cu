@@ -1109,6 +1109,9 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
 #ifndef MF_SPHERE_POOL_MIN_BLOCKS
 #define MF_SPHERE_POOL_MIN_BLOCKS 7
 #endif
+#ifndef MF_GRID_POOL_MIN_BLOCKS
+#define MF_GRID_POOL_MIN_BLOCKS 6   // config 5: 3.60 -> 3.48 ms against 7
+#endif
 // The medium and local frame at a collision point: the sphere's medium and
 // the frame about its normal (kMode 3), or the grid field's medium from
 // sigma(p) and the frame about the trilinear SDF gradient (kMode 2) -- the
@@ -1140,7 +1143,8 @@ struct CollisionLocal<2> {
 };
 
 template <int kMode, bool kMono, int kSpec>
-__global__ void __launch_bounds__(kBlock, MF_SPHERE_POOL_MIN_BLOCKS) curved_pool_kernel(
+__global__ void __launch_bounds__(kBlock, kMode == 2 ? MF_GRID_POOL_MIN_BLOCKS
+                                                     : MF_SPHERE_POOL_MIN_BLOCKS) curved_pool_kernel(
     const __grid_constant__ SceneDev sc, const __grid_constant__ PassDev ps) {
   __shared__ PoolSlots<true, kMono> pools[kWarpsPerBlock];
   const unsigned full = 0xffffffffu;
@@ -1578,6 +1582,12 @@ void launch_pool(int grid, const SceneDev& sc, const PassDev& ps, cudaStream_t s
   pool_kernel<kPoint, kMono, kSpec><<<grid, kBlock, 0, st>>>(sc, ps);
 }
 
+// the curved pools' GENERALIZED + albedo build.  (With the NDF out of line
+// the kernel is 4 % smaller, but its time moves by +-5 % with where ptxas
+// places the callee -- the kernel sits at the instruction-cache limit --
+// so the inline build is kept.)
+constexpr int kCurvedSpec = kSpecGenAlbedo;
+
 template <int kMode, bool kMono, int kSpec>
 cudaError_t occ_curved(int* blocks) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks,
@@ -1598,8 +1608,10 @@ void launch_curved_pool(int mode, const SceneDev& sc, const PassDev& ps, const O
   using K = void (*)(SceneDev, PassDev);
   static const K ks[8] = {curved_pool_kernel<3, false, 0>, curved_pool_kernel<3, true, 0>,
                           curved_pool_kernel<2, false, 0>, curved_pool_kernel<2, true, 0>,
-                          curved_pool_kernel<3, false, 1>, curved_pool_kernel<3, true, 1>,
-                          curved_pool_kernel<2, false, 1>, curved_pool_kernel<2, true, 1>};
+                          curved_pool_kernel<3, false, kCurvedSpec>,
+                          curved_pool_kernel<3, true, kCurvedSpec>,
+                          curved_pool_kernel<2, false, kCurvedSpec>,
+                          curved_pool_kernel<2, true, kCurvedSpec>};
   ks[pk - 20]<<<grid, kBlock, 0, st>>>(sc, ps);
 }
 
@@ -1647,10 +1659,10 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_curved<3, true, 0>(&o.blocks[21])));
   MF_CUDA((occ_curved<2, false, 0>(&o.blocks[22])));
   MF_CUDA((occ_curved<2, true, 0>(&o.blocks[23])));
-  MF_CUDA((occ_curved<3, false, 1>(&o.blocks[24])));
-  MF_CUDA((occ_curved<3, true, 1>(&o.blocks[25])));
-  MF_CUDA((occ_curved<2, false, 1>(&o.blocks[26])));
-  MF_CUDA((occ_curved<2, true, 1>(&o.blocks[27])));
+  MF_CUDA((occ_curved<3, false, kCurvedSpec>(&o.blocks[24])));
+  MF_CUDA((occ_curved<3, true, kCurvedSpec>(&o.blocks[25])));
+  MF_CUDA((occ_curved<2, false, kCurvedSpec>(&o.blocks[26])));
+  MF_CUDA((occ_curved<2, true, kCurvedSpec>(&o.blocks[27])));
   MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
   MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
   MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));

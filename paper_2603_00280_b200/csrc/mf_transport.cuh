@@ -706,7 +706,7 @@ MF_HD float sphere_sigma_dir(const MediumK& m, float g) {
   // Sigma(cos theta): sigma(w) of a local direction with w.z = g
   if (kFast && m.area_q) return area_q_eval(m.area_q, g, m.ax, m.az);
   float sn = fsqrt(fmaxf(1.0f - g * g, 0.0f));
-  if (kFast && kSpec == kSpecGenAlbedo) return proj_area_erf_cold(v3(sn, 0.0f, g), m.ax, m.ay, m.az);
+  if (kFast && spec_gen(kSpec)) return proj_area_erf_cold(v3(sn, 0.0f, g), m.ax, m.ay, m.az);
   return kSpec == kSpecRuntime && m.kind == kGGX ? proj_area_ggx(v3(sn, 0.0f, g), m.ax, m.ay)
                         : proj_area_erf<kFast>(v3(sn, 0.0f, g), m.ax, m.ay, m.az);
 }
