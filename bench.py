@@ -378,8 +378,8 @@ def run_render(args, torch, dist, n, rank, local, dev):
     rl = roofline.from_ops(F, S, kms, pf, ps_, tot.get("paths", 1))
     kernel = {"config4": "pool_kernel (single-plane path pool, grey)",
               "config2": "pool_kernel (single-plane path pool, grey)",
-              "config3": "path_kernel<3> (single-sphere megakernel)",
-              "config5": "path_kernel<2> (grid-field megakernel)"}[args.workload]
+              "config3": "curved_pool_kernel<3> (single-sphere path pool, grey)",
+              "config5": "curved_pool_kernel<2> (grid-field path pool, grey)"}[args.workload]
     roof = {"bound": rl["bound"], "achieved": rl["achieved"], "peak": rl["peak"],
             "unit": rl["unit"], "frac": rl["frac"], "traffic": ncu_traffic(args.workload),
             "peak_source": "measured on this device by mf_measure_peaks (FFMA / MUFU.EX2 issue "
