@@ -350,6 +350,7 @@ struct PathState {
   float u_br, u_s2, u_rr;  // the segment's branch / slope / RR uniforms
   float lphi;            // single plane: log Phi(f / sigma) at pos, NaN when unknown
   int bounce;
+  bool pre;              // raygen drew segment 0's block: u_rr holds u_flight
   uint32_t pid;          // result slot: caller-ray index, or the local pixel (render)
   PathRng rng;
 };
@@ -509,11 +510,20 @@ template <int kMode, int kSpec = kSpecRuntime, int kNeedPos = -1, bool kPool = f
 __device__ __forceinline__ bool flight_stage(const SceneDev& sc, const PassDev& ps, PathState& st,
                                              Counters& cn) {
   cn.v[kStSegments]++;
-  U4 b = philox_rk(U4{st.rng.pixel, st.rng.sample, (uint32_t)st.bounce, 0u}, ps.rk);
-  float u_fl = u01(b.x);
-  st.u_br = u01(b.y);
-  st.u_s2 = u01(b.z);
-  st.u_rr = u01(b.w);
+  float u_fl;
+  if (st.pre) {
+    // segment 0 of a render path: its block was drawn at raygen (the camera
+    // jitter took its spare bits); the RR uniform of segment 0 is never read
+    // (Russian roulette starts after bounce 8)
+    u_fl = st.u_rr;
+    st.pre = false;
+  } else {
+    U4 b = philox_rk(U4{st.rng.pixel, st.rng.sample, (uint32_t)st.bounce, 0u}, ps.rk);
+    u_fl = u01(b.x);
+    st.u_br = u01(b.y);
+    st.u_s2 = u01(b.z);
+    st.u_rr = u01(b.w);
+  }
   st.ck = 0;
   st.csig = -1.0f;
   int outcome;
@@ -670,6 +680,7 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   st.L = v3(0.0f, 0.0f, 0.0f);
   st.lphi = NAN;
   st.bounce = 0;
+  st.pre = false;
   if (kCallerRays) {
     st.rng.pixel = ps.pix[my];
     st.rng.sample = ps.smp[my];
@@ -697,8 +708,16 @@ __device__ __forceinline__ bool start_path(const SceneDev& sc, const PassDev& ps
   if (pixel < 0) return false;   // tile padding
   st.rng.pixel = (uint32_t)pixel;
   st.rng.sample = ps.sample_begin + s;
-  U4 jb = philox_rk(U4{st.rng.pixel, st.rng.sample, kSegCamera, 0u}, ps.rk);
-  camera_ray(sc, px, py, u01(jb.x), u01(jb.y), &st.pos, &st.dir);
+  // one block serves the camera jitter and segment 0: (u_flight, u_branch,
+  // u_slope) from words x, y, z as in every segment, the jitter from word w
+  // and from the 23 low bits of x, y, z that u01 leaves unused
+  U4 b = philox_rk(U4{st.rng.pixel, st.rng.sample, 0u, 0u}, ps.rk);
+  uint32_t low = (b.x & 0x1FFu) | ((b.y & 0x1FFu) << 9) | ((b.z & 0x1Fu) << 18);
+  camera_ray(sc, px, py, u01(b.w), u01(low << 9), &st.pos, &st.dir);
+  st.u_rr = u01(b.x);   // u_flight of segment 0 (see flight_stage)
+  st.u_br = u01(b.y);
+  st.u_s2 = u01(b.z);
+  st.pre = true;
   return true;
 }
 
@@ -918,6 +937,7 @@ __device__ __forceinline__ void pool_load(const PoolSlots<kPoint, kMono>& P, int
   st.rng.pixel = P.u[1][s];
   st.rng.sample = P.u[2][s];
   st.bounce = (int)P.u[3][s];
+  st.pre = false;
 }
 
 // next-event estimation at a collision of the single plane (the stage-2
