@@ -855,6 +855,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) path_kernel(const __grid_c
 #ifndef MF_POOL
 #define MF_POOL 96
 #endif
+// render kernels: evaluate each upper slope-residual form only when some
+// lane of the warp needs it (rare with kSlopeUpperRender)
+#ifndef MF_RENDER_SLOPE_GUARD
+#define MF_RENDER_SLOPE_GUARD 1
+#endif
+constexpr bool kRenderSlopeGuard = MF_RENDER_SLOPE_GUARD;
 constexpr int kPool = MF_POOL;
 static_assert(kPool % 32 == 0 && kPool <= 128, "pool size: whole warps of slots");
 constexpr int kPoolWords = kPool / 32;
@@ -1044,7 +1050,7 @@ __global__ void __launch_bounds__(kBlock, kPoolMinBlocks) pool_kernel(const __gr
       float vm;
       if (stage == kStageBeck && sig_b > 1e-12f) {
         int iters = 0;
-        wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
+        wm = beckmann_visible_normal<kRenderSlopeGuard, true>(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
         cn.v[kStSlopeIters] += (uint32_t)iters;
       } else {
@@ -1232,7 +1238,7 @@ __global__ void __launch_bounds__(kBlock, kMode == 2 ? MF_GRID_POOL_MIN_BLOCKS
       float vm;
       if (stage == kStageBeck && sig_b > 1e-12f) {
         int iters = 0;
-        wm = beckmann_visible_normal<false, true>(m, v, uu, st.u_s2, &iters);
+        wm = beckmann_visible_normal<kRenderSlopeGuard, true>(m, v, uu, st.u_s2, &iters);
         vm = dot3(v, wm);
         cn.v[kStSlopeIters] += (uint32_t)iters;
       } else {
