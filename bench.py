@@ -292,17 +292,25 @@ def run_render(args, torch, dist, n, rank, local, dev):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     paths_per_step = P * cam.width * cam.height * spp
 
-    def step(stats_acc=None):
-        for i in range(P):
-            _, st = mf.render_device(scenes[i], spp, seed, max_bounces=depth, tile=32, rank=rank,
-                                     nranks=n, shard="tiles", out=out[i], stats=True, c_scene=cs[i])
-            if stats_acc is not None:
-                stats_acc[i].append(st)
+    def step():
+        # every panel queued on the stream (mf_render_async): no host
+        # synchronisation inside a step; the tickets are finished -- and
+        # validated -- while the next step runs
+        tickets = [mf.render_device(scenes[i], spp, seed, max_bounces=depth, tile=32, rank=rank,
+                                    nranks=n, shard="tiles", out=out[i], c_scene=cs[i],
+                                    wait=False) for i in range(P)]
         if n > 1:
             dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)   # the one collective of the step
+        return tickets
+
+    def finish(tickets, stats_acc=None):
+        for i, t in enumerate(tickets):
+            st = t.finish()
+            if stats_acc is not None:
+                stats_acc[i].append(st)
 
     for _ in range(max(args.warmup, 0)):
-        step()
+        finish(step())
     torch.cuda.synchronize()
     if n > 1:
         dist.barrier()
@@ -312,11 +320,16 @@ def run_render(args, torch, dist, n, rank, local, dev):
     l0 = lib.mf_launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        pending = None
         for i in range(args.steps):
             flush.fill_(float(i))          # evict L2 between steps (256 MiB > 126 MB L2)
             starts[i].record()
-            step(acc)
+            tickets = step()
             ends[i].record()
+            if pending is not None:
+                finish(pending, acc)
+            pending = tickets
+        finish(pending, acc)
         torch.cuda.synchronize()
         if n > 1:
             dist.barrier()

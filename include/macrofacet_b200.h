@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MF_ABI_VERSION 2
+#define MF_ABI_VERSION 3
 
 enum mf_status {
   MF_OK = 0,
@@ -215,6 +215,19 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
  */
 int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
               mf_stats* stats, void* stream);
+
+/* The same render in two halves, for callers that queue several renders
+ * (panels, steps) on one stream without a host synchronisation between
+ * them: mf_render_async validates the arguments, queues the whole render
+ * and its event-counter read-back on `stream` and returns a ticket;
+ * mf_render_finish waits for that ticket's work, fills stats (may be NULL)
+ * and returns the status mf_render would have returned (the same
+ * validation).  Every ticket must be finished exactly once; tickets of one
+ * stream may be finished in any order.  mf_render == async + finish. */
+typedef struct mf_render_ticket mf_render_ticket;
+int mf_render_async(const mf_scene* scene, const mf_render_params* params, float* d_accum,
+                    mf_render_ticket** ticket, void* stream);
+int mf_render_finish(mf_render_ticket* ticket, mf_stats* stats);
 
 /* trace_paths(origins, directions, scene, max_bounces, brng) (render.py:32-108)
  * for caller-given rays: d_org / d_dir are SoA float32 [3][n], path i is

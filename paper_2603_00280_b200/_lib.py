@@ -29,7 +29,7 @@ COMM_ID_BYTES = 128
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
 SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID, SHAPE_BOX = 0, 1, 2, 3
 WALK_COLLISION, WALK_RATIO, WALK_TENTATIVE = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 SHARD_TILES, SHARD_SAMPLES = 0, 1
 
 _d3 = ctypes.c_double * 3
@@ -111,6 +111,9 @@ SIGNATURES = {
                                       ctypes.c_int64, _vp]),
     "mf_render": (ctypes.c_int, [ctypes.POINTER(MfScene), ctypes.POINTER(MfRenderParams), _vp,
                                  ctypes.POINTER(MfStats), _vp]),
+    "mf_render_async": (ctypes.c_int, [ctypes.POINTER(MfScene), ctypes.POINTER(MfRenderParams),
+                                       _vp, ctypes.POINTER(_vp), _vp]),
+    "mf_render_finish": (ctypes.c_int, [_vp, ctypes.POINTER(MfStats)]),
     "mf_trace_paths": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp,
                                       ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, _vp,
                                       ctypes.POINTER(MfStats), _vp]),

@@ -342,6 +342,20 @@ __device__ __forceinline__ int local_to_pixel(const SceneDev& sc, const PassDev&
   return (int)(y * (uint32_t)sc.width + x);
 }
 
+// inverse of local_to_pixel: this rank's local index of an image pixel, or
+// -1 when another rank owns its tile
+__device__ __forceinline__ int64_t pixel_to_local(const SceneDev& sc, const PassDev& ps,
+                                                  uint32_t pixel) {
+  if (ps.shard == MF_SHARD_SAMPLES) return pixel;
+  uint32_t y = fdiv(pixel, ps.div_width), x = pixel - y * (uint32_t)sc.width;
+  uint32_t ty = fdiv(y, ps.div_tile), tx = fdiv(x, ps.div_tile);
+  uint32_t t = ty * (uint32_t)ps.tiles_x + tx;
+  uint32_t k = t / (uint32_t)ps.nranks;
+  if (t - k * (uint32_t)ps.nranks != (uint32_t)ps.rank) return -1;
+  uint32_t jy = y - ty * (uint32_t)ps.tile, jx = x - tx * (uint32_t)ps.tile;
+  return (int64_t)k * ps.div_t2.d + jy * (uint32_t)ps.tile + jx;
+}
+
 struct PathState {
   V3 pos, dir, T, L;
   V3 cpos;               // pending collision (flight -> scatter stage)
@@ -1310,12 +1324,16 @@ __global__ void __launch_bounds__(kBlock, kMode == 2 ? MF_GRID_POOL_MIN_BLOCKS
 // written into) accum[pixel][c]
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ SceneDev sc,
                                                         const __grid_constant__ PassDev ps,
-                                                        uint32_t n_local, double inv_scale_spp,
+                                                        uint32_t n_pix, double inv_scale_spp,
                                                         int add, float* accum) {
-  uint32_t lp = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lp >= n_local) return;
-  int pixel = local_to_pixel(sc, ps, lp);
-  if (pixel < 0) return;
+  uint32_t pixel = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pixel >= n_pix) return;
+  float* a = accum + (size_t)pixel * 3;
+  int64_t lp = pixel_to_local(sc, ps, pixel);
+  if (lp < 0) {                     // another rank's tile
+    if (!add) a[0] = a[1] = a[2] = 0.0f;
+    return;
+  }
   float t[3];
   if (ps.mono) {
     t[0] = t[1] = t[2] = (float)((double)ps.fx[lp] * inv_scale_spp);
@@ -1323,7 +1341,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
 #pragma unroll
     for (int c = 0; c < 3; ++c) t[c] = (float)((double)ps.fx[(size_t)lp * 3 + c] * inv_scale_spp);
   }
-  float* a = accum + (size_t)pixel * 3;
   float v0 = t[0], v1 = t[1], v2 = t[2];
   if (add) {
     v0 += a[0];
@@ -1755,22 +1772,23 @@ int retain_pool_memory() {
   return MF_OK;
 }
 
+// one stream-ordered block, zeroed with one memset: stats (kStCount u64,
+// padded to 256 B), the work counters (64 u32) and the pixel sums
 int scratch_alloc(Scratch* s, size_t n_fx, cudaStream_t st) {
   int rc = retain_pool_memory();
   if (rc) return rc;
-  if (n_fx) {
-    MF_CUDA(cudaMallocAsync((void**)&s->fx, n_fx * sizeof(unsigned long long), st));
-    MF_CUDA(cudaMemsetAsync(s->fx, 0, n_fx * sizeof(unsigned long long), st));
-  }
-  MF_CUDA(cudaMallocAsync((void**)&s->counter, 64 * sizeof(unsigned int), st));
-  MF_CUDA(cudaMallocAsync((void**)&s->stats, kStCount * sizeof(unsigned long long), st));
-  MF_CUDA(cudaMemsetAsync(s->stats, 0, kStCount * sizeof(unsigned long long), st));
+  static_assert(kStCount * sizeof(unsigned long long) <= 256, "stats block");
+  size_t bytes = 512 + n_fx * sizeof(unsigned long long);
+  char* base = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&base, bytes, st));
+  MF_CUDA(cudaMemsetAsync(base, 0, bytes, st));
+  s->stats = (unsigned long long*)base;
+  s->counter = (unsigned int*)(base + 256);
+  s->fx = n_fx ? (unsigned long long*)(base + 512) : nullptr;
   return MF_OK;
 }
 
 int scratch_free(Scratch* s, cudaStream_t st) {
-  if (s->fx) MF_CUDA(cudaFreeAsync(s->fx, st));
-  if (s->counter) MF_CUDA(cudaFreeAsync(s->counter, st));
   if (s->stats) MF_CUDA(cudaFreeAsync(s->stats, st));
   *s = Scratch();
   return MF_OK;
@@ -1879,6 +1897,41 @@ double scene_emax(const SceneDev& sc) {
   return e;
 }
 
+}  // namespace
+
+// A queued render (mf_render_async): its read-back block of event
+// counters (pinned host memory, recycled), the completion event and the
+// path-kernel timing events.
+struct mf_render_ticket {
+  bool empty = true;
+  unsigned long long* h_stats = nullptr;
+  cudaEvent_t done = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+
+namespace {
+std::mutex g_pinned_mu;
+std::vector<unsigned long long*> g_pinned_free;
+
+unsigned long long* pinned_stats_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      unsigned long long* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, 32 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+    return nullptr;
+  return (unsigned long long*)p;
+}
+
+void pinned_stats_put(unsigned long long* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
 }  // namespace
 
 extern "C" {
@@ -2062,8 +2115,10 @@ int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d
   return MF_OK;
 }
 
-int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
-              mf_stats* stats, void* stream) {
+int mf_render_async(const mf_scene* scene, const mf_render_params* params, float* d_accum,
+                    mf_render_ticket** ticket, void* stream) {
+  if (!ticket) return fail(MF_ERR_PARAM, "null ticket");
+  *ticket = nullptr;
   if (!scene || !params || !d_accum) return fail(MF_ERR_PARAM, "null argument");
   const mf_render_params& p = *params;
   if (p.spp < 1) return fail(MF_ERR_PARAM, "spp must be >= 1, got " + std::to_string(p.spp));
@@ -2083,7 +2138,6 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   size_t npix = (size_t)sc.width * sc.height;
-  if (!p.accumulate) MF_CUDA(cudaMemsetAsync(d_accum, 0, npix * 3 * sizeof(float), st));
 
   PassDev ps;
   std::memset(&ps, 0, sizeof(ps));
@@ -2115,7 +2169,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     s_count = (uint32_t)(b - a);
   }
   if (n_local == 0 || s_count == 0) {
-    if (stats) std::memset(stats, 0, sizeof(*stats));
+    *ticket = new mf_render_ticket();   // nothing to render: an empty ticket
     return MF_OK;
   }
   size_t max_pass = kMaxPassPaths;
@@ -2168,7 +2222,7 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     ps.n_local = (uint32_t)n_local;
     ps.div_local = make_fastdiv((uint32_t)n_local);
     ps.div_S = make_fastdiv(S);
-    MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
+    if (s0 > 0) MF_CUDA(cudaMemsetAsync(scr.counter, 0, sizeof(unsigned int), st));
     ev.resize(ev.size() + 2, nullptr);
     MF_CUDA(cudaEventCreate(&ev[ev.size() - 2]));
     MF_CUDA(cudaEventCreate(&ev[ev.size() - 1]));
@@ -2182,29 +2236,70 @@ int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_ac
     }
   }
   ps.n_local = (uint32_t)n_local;
-  finalize_kernel<<<(uint32_t)((n_local + 255) / 256), 256, 0, st>>>(
-      sc, ps, (uint32_t)n_local, std::ldexp(1.0, -k) / (double)p.spp, p.accumulate ? 1 : 0, d_accum);
+  // over every image pixel: owned ones get sum / spp, the others +0.0 in
+  // overwrite mode (no separate clearing of the caller's buffer)
+  finalize_kernel<<<(uint32_t)((npix + 255) / 256), 256, 0, st>>>(
+      sc, ps, (uint32_t)npix, std::ldexp(1.0, -k) / (double)p.spp, p.accumulate ? 1 : 0, d_accum);
   g_launches++;
   MF_CUDA(cudaGetLastError());
-  // the event counters always come back: majorant violations, iteration caps
-  // and invalid radiance raise, as the reference's render() always
-  // validates (transport.py:264-268,297; image.py:38-42)
-  unsigned long long h[kStCount];
-  MF_CUDA(cudaMemcpyAsync(h, scr.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
-  MF_CUDA(cudaStreamSynchronize(st));
+  // the event counters always come back (mf_render_finish validates them:
+  // majorant violations, iteration caps and invalid radiance raise, as the
+  // reference's render() always validates -- transport.py:264-268,297;
+  // image.py:38-42)
+  mf_render_ticket* t = new mf_render_ticket();
+  t->h_stats = pinned_stats_get();
+  if (!t->h_stats) {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    scratch_free(&scr, st);
+    delete t;
+    return fail(MF_ERR_CUDA, "cannot allocate pinned host memory");
+  }
+  MF_CUDA(cudaMemcpyAsync(t->h_stats, scr.stats, kStCount * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  MF_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  MF_CUDA(cudaEventRecord(t->done, st));
+  t->ev.swap(ev);
+  t->empty = false;
+  *ticket = t;
+  return scratch_free(&scr, st);   // stream-ordered: after the read-back
+}
+
+int mf_render_finish(mf_render_ticket* t, mf_stats* stats) {
+  if (!t) return fail(MF_ERR_PARAM, "null ticket");
+  if (t->empty) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    delete t;
+    return MF_OK;
+  }
+  cudaError_t e = cudaEventSynchronize(t->done);
   mf_stats local;
   mf_stats& out_st = stats ? *stats : local;
-  fill_stats(h, &out_st);
-  for (size_t i = 0; i + 1 < ev.size(); i += 2) {
-    float ms = 0.0f;
-    MF_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-    kernel_ms += ms;
+  int out = MF_OK;
+  if (e != cudaSuccess) {
+    out = fail(MF_ERR_CUDA, std::string("render: ") + cudaGetErrorString(e));
+  } else {
+    fill_stats(t->h_stats, &out_st);
+    double kernel_ms = 0.0;
+    for (size_t i = 0; i + 1 < t->ev.size(); i += 2) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, t->ev[i], t->ev[i + 1]) == cudaSuccess) kernel_ms += ms;
+    }
+    out_st.path_kernel_ms = kernel_ms;
+    out = check_stats(out_st);
   }
-  for (cudaEvent_t e : ev) cudaEventDestroy(e);
-  out_st.path_kernel_ms = kernel_ms;
-  int out = check_stats(out_st);
-  rc = scratch_free(&scr, st);
-  return out ? out : rc;
+  for (cudaEvent_t ev : t->ev) cudaEventDestroy(ev);
+  cudaEventDestroy(t->done);
+  pinned_stats_put(t->h_stats);
+  delete t;
+  return out;
+}
+
+int mf_render(const mf_scene* scene, const mf_render_params* params, float* d_accum,
+              mf_stats* stats, void* stream) {
+  mf_render_ticket* t = nullptr;
+  int rc = mf_render_async(scene, params, d_accum, &t, stream);
+  if (rc) return rc;
+  return mf_render_finish(t, stats);
 }
 
 int mf_trace_paths(const mf_scene* scene, const float* d_org, const float* d_dir,

@@ -60,10 +60,40 @@ def _c_scene(scene: ShellScene, device):
     return cs
 
 
+class RenderTicket:
+    """A render queued on its stream (render_device(wait=False), C ABI
+    mf_render_async): `finish()` waits for it, validates it exactly like a
+    synchronous render (majorant violations, walker caps and invalid
+    radiance raise) and returns the stats dict.  Finish every ticket once;
+    tickets of one stream may be finished in any order."""
+
+    def __init__(self, handle, out, keep):
+        self._h, self.out, self._keep = handle, out, keep
+
+    def finish(self):
+        if self._h is None:
+            raise ParameterDomainError("render ticket already finished")
+        st = _lib.MfStats()
+        h, self._h = self._h, None
+        _lib.check(_lib.load().mf_render_finish(h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None:   # never finished: release it
+            try:
+                _lib.load().mf_render_finish(self._h, None)
+            except Exception:
+                pass
+
+
 def render_device(scene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
-                  shard="tiles", out=None, stats=False, stream=None, c_scene=None):
+                  shard="tiles", out=None, stats=False, stream=None, c_scene=None, wait=True):
     """Render into a (H, W, 3) float32 CUDA tensor holding radiance / spp for
-    this rank's share.  Returns (tensor, stats dict or None)."""
+    this rank's share.  Returns (tensor, stats dict or None); with
+    wait=False the render is only queued on the stream and a RenderTicket
+    comes back instead (ticket.out is the tensor; ticket.finish() validates
+    and returns the stats), so several renders run back to back without a
+    host synchronisation between them."""
     prm = _params(spp, seed, max_bounces, tile, shard, rank, nranks)
     torch = _lib.require_cuda()
     lib = _lib.load()
@@ -74,8 +104,13 @@ def render_device(scene, spp, seed, max_bounces=64, tile=32, rank=0, nranks=1,
             tuple(out.shape) != (cam.height, cam.width, 3):
         raise ParameterDomainError("out must be a contiguous (H, W, 3) float32 CUDA tensor")
     cs = c_scene if c_scene is not None else _c_scene(scene, out.device.index)
-    st = _lib.MfStats() if stats else None
     s = stream if stream is not None else _lib.stream_handle(torch, out.device)
+    if not wait:
+        h = ctypes.c_void_p()
+        _lib.check(lib.mf_render_async(ctypes.byref(cs), ctypes.byref(prm),
+                                       ctypes.c_void_p(out.data_ptr()), ctypes.byref(h), s))
+        return RenderTicket(h, out, (cs, prm))
+    st = _lib.MfStats() if stats else None
     _lib.check(lib.mf_render(ctypes.byref(cs), ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
                              ctypes.byref(st) if st is not None else None, s))
     return out, (st.as_dict() if st is not None else None)

@@ -44,7 +44,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_error_string(lib):
     lib.mf_abi_version.restype = ctypes.c_int
-    assert lib.mf_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.mf_abi_version() == _lib.ABI_VERSION == 3
     lib.mf_last_error.restype = ctypes.c_char_p
     assert isinstance(lib.mf_last_error(), bytes)
 
@@ -94,3 +94,20 @@ def test_sm100a_code_in_library():
     out = subprocess.run(["cuobjdump", "--list-elf", build.OUT], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
 STRUCTS["mf_grid_field"] = _lib.MfGridField
+
+
+def test_async_render_parameter_errors_without_gpu(lib):
+    """mf_render_async validates before any CUDA call and hands out no
+    ticket on an error; mf_render_finish rejects a null ticket."""
+    lib.mf_render_async.restype = ctypes.c_int
+    lib.mf_render_finish.restype = ctypes.c_int
+    scene = _lib.MfScene()
+    params = _lib.MfRenderParams()
+    params.spp = 1
+    params.max_bounces = 0
+    params.nranks = 1
+    h = ctypes.c_void_p(123)
+    rc = lib.mf_render_async(ctypes.byref(scene), ctypes.byref(params), ctypes.c_void_p(1),
+                             ctypes.byref(h), None)
+    assert rc == 1 and not h.value
+    assert lib.mf_render_finish(None, None) == 1
