@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 python tools/timeline.py > gpurun_out/timeline.txt 2>&1
+timeout 1500 python tools/time_variants.py variants/noguard.so variants/guard.so variants/noguard.so variants/guard.so > gpurun_out/variants.txt 2>&1

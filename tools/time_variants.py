@@ -25,6 +25,10 @@ c2 = configs.config2_scene(); c3 = configs.config3_scene(256, 256)
 t2, m2 = tm(c2, 64, 1, 16); t3, m3 = tm(c3, 64, 2, 32, reps=5)
 c5 = configs.config5_scene(256, 256)
 t5, m5 = tm(c5, 16, 4, 64, reps=5)
+c4 = configs.config4_scene(0.05, 0.1, 512, 512)
+t4, m4 = tm(c4, 64, 3, 64, reps=5)
+c4b = configs.config4_scene(0.2, 0.02, 512, 512)
+t4b, m4b = tm(c4b, 64, 3, 64, reps=5)
 _, st = mf.render_device(c2, 64, 1, max_bounces=16, stats=True)
 p, wo, wi, u = configs.config1_inputs(1 << 20)
 d = torch.device("cuda", 0)
@@ -40,7 +44,7 @@ qt = []
 for _ in range(5):
     s.record(); mf.query_batch(med, P, WO, WI, U1, U2); e.record(); torch.cuda.synchronize(); qt.append(s.elapsed_time(e))
 qms = min(qt)
-print(json.dumps({"c2_ms": t2, "c2_Mpaths_s": 256*256*64/t2/1e3, "c2_mean": m2, "c3_ms": t3, "c3_Mpaths_s": 256*256*64/t3/1e3, "c3_mean": m3, "c5_ms": t5, "c5_mean": m5, "hashes": tm.hashes, "slope_iters_per_path": st["slope_iters"]/st["paths"], "query_2^24_ms": qms, "Mq_s": (1<<24)/qms/1e3}))
+print(json.dumps({"c4_ms": t4, "c4b_ms": t4b, "c2_ms": t2, "c2_Mpaths_s": 256*256*64/t2/1e3, "c2_mean": m2, "c3_ms": t3, "c3_Mpaths_s": 256*256*64/t3/1e3, "c3_mean": m3, "c5_ms": t5, "c5_mean": m5, "hashes": tm.hashes, "slope_iters_per_path": st["slope_iters"]/st["paths"], "query_2^24_ms": qms, "Mq_s": (1<<24)/qms/1e3}))
 ''' % here
 for so in sys.argv[1:]:
     env = dict(os.environ, MF_LIB_PATH=os.path.abspath(so))
