@@ -278,6 +278,24 @@ def ncu_traffic(workload):
         return None
 
 
+def ncu_memory(workload):
+    """Memory-system figures of the dominant kernel from the committed ncu
+    summary of this workload (profiles/r02_<workload>_ncu_full.json): DRAM
+    and L2 GB/s of that capture -- for config 5, the grid lookups (the SDF
+    and sigma grids are L2-resident) -- or None."""
+    prof = os.path.join(ROOT, "profiles", f"r02_{workload}_ncu_full.json")
+    if not os.path.exists(prof):
+        return None
+    try:
+        with open(prof) as fh:
+            d = json.load(fh)
+        return {"dram_GB_s": d.get("dram_GB_s"), "l2_GB_s": d.get("l2_GB_s"),
+                "l2_hit_pct": d.get("l2_hit_pct"), "capture": d.get("source"),
+                "units_per_launch": d.get("units_per_launch")}
+    except Exception:
+        return None
+
+
 def run_render(args, torch, dist, n, rank, local, dev):
     import paper_2603_00280_b200 as mf
     from paper_2603_00280_b200 import _lib, roofline
@@ -404,6 +422,7 @@ def run_render(args, torch, dist, n, rank, local, dev):
                                     for a in acc],
             "kernel_share_of_step": kms / max(ms, 1e-9),
             "kernel": kernel,
+            "memory": ncu_memory(args.workload),
             "work": "algorithmic FP32 / MUFU lane ops from the frozen per-event counts "
                     "(paper_2603_00280_b200/roofline.py) x the device event counters of the "
                     "timed launches"}

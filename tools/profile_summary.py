@@ -32,6 +32,8 @@ METRICS = {
     "dram__bytes_read.sum": "dram_read_bytes",
     "dram__bytes_write.sum": "dram_write_bytes",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "lts__t_sectors.sum": "l2_sectors",
+    "lts__t_sectors.sum.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
     "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
 }
 UNITS = {"ms": 1.0, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "nsecond": 1e-6,
@@ -58,7 +60,7 @@ def main():
         if k in h:
             x = num(v[h.index(k)])
             unit = u[h.index(k)]
-            if x is not None and unit in UNITS and name.endswith(("ms", "bytes")):
+            if x is not None and unit in UNITS and (name.endswith("ms") or "bytes" in name):
                 x *= UNITS[unit]
             out[name] = x
     stalls = {}
@@ -71,6 +73,11 @@ def main():
     out["stall_share"] = {k: round(x / tot, 4) for k, x in
                           sorted(stalls.items(), key=lambda kv: -kv[1])[:10]}
     out["dram_bytes_per_launch"] = (out.get("dram_read_bytes") or 0) + (out.get("dram_write_bytes") or 0)
+    t = out.get("time_ms")
+    if t:
+        out["dram_GB_s"] = round(out["dram_bytes_per_launch"] / (t * 1e-3) / 1e9, 2)
+        if out.get("l2_sectors") is not None:   # 32-byte sectors through the L2 slices
+            out["l2_GB_s"] = round(out["l2_sectors"] * 32 / (t * 1e-3) / 1e9, 1)
     # executed-instruction mix per unit (sass_mix's classes)
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                           "sass"], capture_output=True, text=True).stdout
