@@ -332,6 +332,48 @@ int mf_abi_version(void);
 /* number of kernel launches this thread has issued through the library */
 uint64_t mf_launch_count(void);
 
+/* ---------------------------------------------------------------------
+ * Gaussian-random-field oracle (reference gp.py):
+ * periodic field realisations and their first zero crossings, float64.
+ * The FFT filtering of the white noise (gp.py:131-141) is the caller's
+ * (cuFFT through torch.fft, batched); these entry points draw the noise,
+ * evaluate the trilinear interpolant and march rays through it.  A batch
+ * holds n_real realisations of n^3 values each; ray / point i belongs to
+ * realisation d_real[i] (NULL: all to realisation 0).  Arrays of 3-vectors
+ * are SoA [3][count] float64. */
+typedef struct mf_gp_grid {
+  const double* d_grid; /* realisation r at d_grid + r n^3, index (ix n + iy) n + iz */
+  int32_t n;
+  double spacing;
+  double origin;        /* lower corner on every axis (-extent / 2) */
+  int32_t planar;       /* 1: mean mu(p) = p_z; 0: zero mean */
+} mf_gp_grid;
+
+/* RandomStream(seed, stream).normal(n) (rng.py:87-97) of the streams whose
+ * SplitMix64 base states are d_bases[0..n_streams) (counters start at
+ * counter0): d_out[s * n + i].  mf_gp_uniform: RandomStream.uniform(n). */
+int mf_gp_noise(const uint64_t* d_bases, int32_t n_streams, uint64_t counter0, int64_t n,
+                double* d_out, void* stream);
+int mf_gp_uniform(const uint64_t* d_bases, int32_t n_streams, uint64_t counter0, int64_t n,
+                  double* d_out, void* stream);
+/* GpRealization.field_at / gradient_at (gp.py:80-127); d_f / d_grad may be NULL */
+int mf_gp_eval(const mf_gp_grid* grid, const double* d_p, const int32_t* d_real, int64_t n,
+               double* d_f, double* d_grad, void* stream);
+/* first_hit (gp.py:148-197): march step `step`, range t_max (or
+ * d_tmax_real[realisation] when not NULL) */
+int mf_gp_first_hit(const mf_gp_grid* grid, const double* d_org, const double* d_dir,
+                    const int32_t* d_real, int64_t n, double step, const double* d_tmax_real,
+                    double t_max, uint8_t* d_hit, double* d_pos, double* d_normal,
+                    double* d_travel, void* stream);
+/* the specular bounce loop of ensemble_radiance (gp.py:361-397) for n paths
+ * in place: origins d_o, directions d_d, throughput d_thr, radiance d_rad
+ * (SoA [3][n]); eta / k: conductor Fresnel per channel (host arrays of 3),
+ * NULL for F = 1 */
+int mf_gp_reflect_paths(const mf_gp_grid* grid, double* d_o, double* d_d, double* d_thr,
+                        double* d_rad, const int32_t* d_real, int64_t n, int32_t n_real,
+                        double sigma, double env, double eps, double step, int32_t max_bounces,
+                        const double* eta, const double* k, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

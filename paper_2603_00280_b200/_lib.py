@@ -94,6 +94,11 @@ class MfStats(ctypes.Structure):
 _vp = ctypes.c_void_p
 
 
+class MfGpGrid(ctypes.Structure):
+    _fields_ = [("d_grid", ctypes.c_void_p), ("n", ctypes.c_int32), ("spacing", ctypes.c_double),
+                ("origin", ctypes.c_double), ("planar", ctypes.c_int32)]
+
+
 class MfQueryIn(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("px", "py", "pz", "wox", "woy", "woz", "wix", "wiy", "wiz",
                                    "u1", "u2", "f", "frame")]
@@ -114,6 +119,18 @@ SIGNATURES = {
     "mf_render_async": (ctypes.c_int, [ctypes.POINTER(MfScene), ctypes.POINTER(MfRenderParams),
                                        _vp, ctypes.POINTER(_vp), _vp]),
     "mf_render_finish": (ctypes.c_int, [_vp, ctypes.POINTER(MfStats)]),
+    "mf_gp_noise": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int64, _vp, _vp]),
+    "mf_gp_uniform": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int64, _vp,
+                                     _vp]),
+    "mf_gp_eval": (ctypes.c_int, [ctypes.POINTER(MfGpGrid), _vp, _vp, ctypes.c_int64, _vp, _vp,
+                                  _vp]),
+    "mf_gp_first_hit": (ctypes.c_int, [ctypes.POINTER(MfGpGrid), _vp, _vp, _vp, ctypes.c_int64,
+                                       ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp, _vp,
+                                       _vp]),
+    "mf_gp_reflect_paths": (ctypes.c_int, [ctypes.POINTER(MfGpGrid), _vp, _vp, _vp, _vp, _vp,
+                                           ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int32, _vp, _vp, _vp]),
     "mf_trace_paths": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp,
                                       ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, _vp,
                                       ctypes.POINTER(MfStats), _vp]),

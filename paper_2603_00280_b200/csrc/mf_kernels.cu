@@ -28,6 +28,7 @@
 #include "mf_prepare.h"
 #include "mf_scene_build.h"
 #include "mf_transport.cuh"
+#include "mf_gp.cuh"
 
 using namespace mf;
 
@@ -2459,6 +2460,124 @@ int mf_transmittance(const mf_scene* scene, const double origin[3], const double
   for (float v : hw) ss += ((double)v - m) * ((double)v - m);
   *mean = m;
   *se = n > 1 ? std::sqrt(ss / (double)(n - 1)) / std::sqrt((double)n) : 0.0;
+  return MF_OK;
+}
+
+
+// --- Gaussian-random-field oracle (mf_gp.cuh) ---------------------------
+
+static mf::gp::Grid gp_grid(const mf_gp_grid& g) {
+  mf::gp::Grid G;
+  G.g = g.d_grid;
+  G.n = g.n;
+  G.h = g.spacing;
+  G.origin = g.origin;
+  G.planar = g.planar;
+  return G;
+}
+
+static int gp_check(const mf_gp_grid* g) {
+  if (!g || !g->d_grid || g->n < 2 || !(g->spacing > 0.0))
+    return fail(MF_ERR_PARAM, "gp grid: null array, n < 2 or spacing <= 0");
+  return MF_OK;
+}
+
+static unsigned gp_blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+int mf_gp_noise(const uint64_t* d_bases, int32_t n_streams, uint64_t counter0, int64_t n,
+                double* d_out, void* stream) {
+  if (!d_bases || !d_out || n_streams < 0 || n < 0) return fail(MF_ERR_PARAM, "bad gp_noise arguments");
+  if (!n || !n_streams) return MF_OK;
+  mf::gp::noise_kernel<<<gp_blocks(n * n_streams), 256, 0, (cudaStream_t)stream>>>(
+      d_bases, n_streams, counter0, n, d_out);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_gp_uniform(const uint64_t* d_bases, int32_t n_streams, uint64_t counter0, int64_t n,
+                  double* d_out, void* stream) {
+  if (!d_bases || !d_out || n_streams < 0 || n < 0)
+    return fail(MF_ERR_PARAM, "bad gp_uniform arguments");
+  if (!n || !n_streams) return MF_OK;
+  mf::gp::uniform_kernel<<<gp_blocks(n * n_streams), 256, 0, (cudaStream_t)stream>>>(
+      d_bases, n_streams, counter0, n, d_out);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_gp_eval(const mf_gp_grid* grid, const double* d_p, const int32_t* d_real, int64_t n,
+               double* d_f, double* d_grad, void* stream) {
+  int rc = gp_check(grid);
+  if (rc) return rc;
+  if (!d_p || n < 0) return fail(MF_ERR_PARAM, "bad gp_eval arguments");
+  if (!n || (!d_f && !d_grad)) return MF_OK;
+  mf::gp::eval_kernel<<<gp_blocks(n), 256, 0, (cudaStream_t)stream>>>(gp_grid(*grid), n, d_p,
+                                                                       d_real, d_f, d_grad);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_gp_first_hit(const mf_gp_grid* grid, const double* d_org, const double* d_dir,
+                    const int32_t* d_real, int64_t n, double step, const double* d_tmax_real,
+                    double t_max, uint8_t* d_hit, double* d_pos, double* d_normal,
+                    double* d_travel, void* stream) {
+  int rc = gp_check(grid);
+  if (rc) return rc;
+  if (!d_org || !d_dir || !d_hit || !d_pos || !d_normal || !d_travel || n < 0 || !(step > 0.0))
+    return fail(MF_ERR_PARAM, "bad gp_first_hit arguments");
+  if (!n) return MF_OK;
+  mf::gp::first_hit_kernel<<<gp_blocks(n), 256, 0, (cudaStream_t)stream>>>(
+      gp_grid(*grid), n, d_org, d_dir, d_real, step, d_tmax_real, t_max, d_hit, d_pos, d_normal,
+      d_travel);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_gp_reflect_paths(const mf_gp_grid* grid, double* d_o, double* d_d, double* d_thr,
+                        double* d_rad, const int32_t* d_real, int64_t n, int32_t n_real,
+                        double sigma, double env, double eps, double step, int32_t max_bounces,
+                        const double* eta, const double* k, void* stream) {
+  int rc = gp_check(grid);
+  if (rc) return rc;
+  if (!d_o || !d_d || !d_thr || !d_rad || !d_real || n < 0 || n_real < 1 || !(step > 0.0))
+    return fail(MF_ERR_PARAM, "bad gp_reflect_paths arguments");
+  if (!n || max_bounces < 1) return MF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  mf::gp::Paths P;
+  P.o = d_o; P.d = d_d; P.thr = d_thr; P.rad = d_rad; P.real = d_real; P.n = n;
+  P.sigma = sigma; P.env = env; P.eps = eps; P.step = step;
+  P.fresnel = (eta && k) ? 1 : 0;
+  for (int c = 0; c < 3; ++c) {
+    P.eta[c] = P.fresnel ? eta[c] : 0.0;
+    P.k[c] = P.fresnel ? k[c] : 0.0;
+  }
+  // scratch: alive flags, per-realisation march length, live count
+  size_t bytes = (size_t)n + 8 * (size_t)n_real + 64;
+  char* base = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&base, bytes, st));
+  P.tcap = (unsigned long long*)base;
+  P.live = (unsigned int*)(base + 8 * (size_t)n_real);
+  P.alive = (uint8_t*)(base + 8 * (size_t)n_real + 64);
+  MF_CUDA(cudaMemsetAsync(P.alive, 1, (size_t)n, st));
+  mf::gp::Grid G = gp_grid(*grid);
+  unsigned live = 0;
+  for (int b = 0; b < max_bounces; ++b) {
+    MF_CUDA(cudaMemsetAsync(base, 0, 8 * (size_t)n_real + 64, st));
+    mf::gp::escape_kernel<<<gp_blocks(n), 256, 0, st>>>(G, P);
+    g_launches++;
+    MF_CUDA(cudaGetLastError());
+    MF_CUDA(cudaMemcpyAsync(&live, P.live, sizeof(live), cudaMemcpyDeviceToHost, st));
+    MF_CUDA(cudaStreamSynchronize(st));
+    if (!live) break;
+    mf::gp::reflect_kernel<<<gp_blocks(n), 256, 0, st>>>(G, P);
+    g_launches++;
+    MF_CUDA(cudaGetLastError());
+  }
+  MF_CUDA(cudaFreeAsync(base, st));
   return MF_OK;
 }
 

@@ -48,6 +48,17 @@ class RandomStream:
         u = (raw >> _U(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
         return float(u[0]) if shape is None else u.reshape(shape)
 
+    def normal(self, shape=None):
+        """Box-Muller over two uniforms per pair (rng.py:87-97)."""
+        n = 1 if shape is None else int(np.prod(shape))
+        m = (n + 1) // 2
+        u1 = self.uniform((m,))
+        u2 = self.uniform((m,))
+        r = np.sqrt(-2.0 * np.log1p(-u1))
+        z = np.concatenate([r * np.cos(6.283185307179586 * u2),
+                            r * np.sin(6.283185307179586 * u2)])[:n]
+        return float(z[0]) if shape is None else z.reshape(shape)
+
     def derive(self, index):
         with np.errstate(over="ignore"):
             child = int(_mix(np.asarray(self.stream, dtype=np.uint64) * _PHI

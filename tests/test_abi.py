@@ -94,6 +94,7 @@ def test_sm100a_code_in_library():
     out = subprocess.run(["cuobjdump", "--list-elf", build.OUT], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
 STRUCTS["mf_grid_field"] = _lib.MfGridField
+STRUCTS["mf_gp_grid"] = _lib.MfGpGrid
 
 
 def test_async_render_parameter_errors_without_gpu(lib):
