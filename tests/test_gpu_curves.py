@@ -121,7 +121,7 @@ def test_curve_errors(cuda):
 def test_validate_suites_pass(cuda):
     lines = []
     assert validate.run_suites(list(validate.SUITES), out=lines.append), "\n".join(lines)
-    assert len(lines) == 13
+    assert len(lines) == 15   # 13 + the two multiplicativity checks
 
 
 def test_cli_curves_and_validate(cuda, tmp_path, capsys):

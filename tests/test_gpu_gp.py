@@ -95,3 +95,32 @@ def test_desk_scale_limits(cuda, kernel):
         gp.empirical_transmittance(kernel, 0.1, 0.5, 0.0, [0.1], 10, RandomStream(1))
     with pytest.raises(ParameterDomainError):
         gp.realize_gp(kernel, "sphere", None, RandomStream(1))
+
+
+def test_cli_oracle(cuda, tmp_path):
+    """`oracle` subcommand (cli.py:193-265) on the device: CSV / PFM outputs
+    and the reference's caps."""
+    from paper_2603_00280_b200 import cli
+    from paper_2603_00280_b200.image import read_pfm
+
+    out = tmp_path / "tr.csv"
+    assert cli.main(["oracle", "gp-transmittance", "--realizations", "64", "--steps", "5",
+                     "--t-max", "0.5", "--z0", "0.05", "--out", str(out)]) == 0
+    rows = [l for l in out.read_text().splitlines() if l and not l.startswith("#")]
+    assert rows[0].startswith("t_world") and len(rows) == 6
+    vals = np.array([[float(x) for x in r.split(",")] for r in rows[1:]])
+    assert vals[0, 1] == 1.0 and np.all(np.diff(vals[:, 1]) <= 0)
+    pfm = tmp_path / "ens.pfm"
+    assert cli.main(["oracle", "gp-ensemble", "--realizations", "4", "--spp", "2", "--width",
+                     "8", "--height", "8", "--out", str(pfm)]) == 0
+    img = read_pfm(pfm)
+    assert img.pixels.shape == (8, 8, 3) and np.all(np.isfinite(img.pixels))
+    assert cli.main(["oracle", "gp-vndf", "--realizations", "5000", "--out",
+                     str(tmp_path / "v.csv")]) == 1
+
+
+def test_validate_multiplicativity(cuda):
+    from paper_2603_00280_b200 import validate
+
+    lines = []
+    assert validate.run_suites(["multiplicativity"], out=lines.append), lines
