@@ -21,6 +21,8 @@ roofline records in profiles/):
   config2  planar render 256^2 x 64 spp, depth 16, seed 1
   config3  sphere + point light 512^2 x 256 spp, depth 32, seed 2
   config5  heterogeneous grid field 2048^2 x 4096 spp, depth 64, seed 4
+  gp       the GP-realisation oracle: ensemble_radiance,
+           64^2 pixels x 64 realisations
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
                     [--workload config4|config1|config2|config3|config5]
@@ -230,6 +232,23 @@ def run_reference(args):
     if args.workload == "config5":
         print(json.dumps({"impl": "reference", "unavailable": "config 5 (grid SDF, per-voxel "
                           "sigma) has no reference implementation (SURVEY.md 8(c))"}))
+        return 0
+    if args.workload == "gp":
+        prof = os.path.join(ROOT, "profiles", "r02_gp_reference_cpu.json")
+        ref = json.load(open(prof))
+        v = ref["paths_per_s"] / 1e6
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": METRIC, "n_gpus": ws,
+            "steps": 1, "warmup": 0, "ms_per_step": ref["seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "gp (reference gp.ensemble_radiance)",
+                                            "sample": ref["sample"]},
+            "cpu_baseline": {"value": v, "unit": METRIC, "cores": 1, "kind": "reference",
+                             "sample": ref["sample"] + " -- recorded in the build container "
+                             "(profiles/r02_gp_reference_cpu.json): the reference package "
+                             "cannot travel to the GPU box"},
+            "e2e": {"value": v, "unit": METRIC, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
         return 0
     if args.workload == "config1":
         v, workers, sample = cpu_queries(args.ref_seconds)
@@ -566,6 +585,98 @@ def run_queries(args, torch, n, rank, local, dev):
     }
 
 
+# ---------------------------------------------------------------------------
+# our arm: the GP-realisation oracle
+
+GP_W = GP_H = 64          # the reference's desk-scale maximum
+GP_ROUNDS = 64            # realisations (sample rounds) per step
+
+
+def gp_workload():
+    from paper_2603_00280_b200.ndf import KernelParams
+    from paper_2603_00280_b200.scene import Camera
+
+    sigma = ell = 0.05
+    k = KernelParams(sigma, ell, ell, ell)
+    cam = Camera(position=(0, 0, 8 * sigma + 2), look_at=(1.0, 0, 0), fov_deg=35, width=GP_W,
+                 height=GP_H)
+    return k, cam
+
+
+def run_gp(args, torch, n, rank, local, dev):
+    """ensemble_radiance (gp.py:334-398) of GP_ROUNDS realisations at the
+    reference's 64 x 64 desk-scale limit, kernel sigma 0.05, l 0.05, the CLI
+    gp-ensemble camera, F = 1, depth 64.  value: paths of the step over the
+    device time of its realisation + bounce-loop work (CUDA events);
+    e2e: the public ensemble_radiance() call (host camera rays, uniforms
+    read-back, image download)."""
+    from paper_2603_00280_b200 import _lib, gp
+    from paper_2603_00280_b200.rng import RandomStream
+
+    k, cam = gp_workload()
+    lib = _lib.load()
+    paths = GP_W * GP_H * GP_ROUNDS
+    for _ in range(max(args.warmup, 1)):
+        gp.ensemble_radiance(k, cam, GP_ROUNDS, GP_ROUNDS, RandomStream(0, 0))
+    torch.cuda.synchronize()
+    work = {}
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = lib.mf_launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            starts[i].record()
+            gp.ensemble_radiance(k, cam, GP_ROUNDS, GP_ROUNDS, RandomStream(i, 0), work=work)
+            ends[i].record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+    launches = lib.mf_launch_count() - l0
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    if rank != 0:
+        return None
+    peak = _lib.ctypes.c_double()
+    _lib.check(lib.mf_measure_peak_fp64(_lib.ctypes.byref(peak), _lib.stream_handle(torch, dev)))
+    # algorithmic work: 45 float64 operations per evaluation of the trilinear
+    # interpolant (3 sub + 3 div + 3 sub + 3 one-minus + 8 x (2 mul weight +
+    # mul + add) + the planar mean) and 6 per ray point of the march
+    # (csrc/mf_gp.cuh); FMA-free by construction (numpy's rounding)
+    evals = work.get("evals", 0) / args.steps
+    ops = evals * 51.0
+    achieved = ops / (ms * 1e-3) / 1e9
+    ref = None
+    prof = os.path.join(ROOT, "profiles", "r02_gp_reference_cpu.json")
+    if os.path.exists(prof):
+        ref = json.load(open(prof))
+    cpu = {"value": ref["paths_per_s"] / 1e6, "unit": METRIC, "cores": 1, "kind": "reference",
+           "sample": ref["sample"] + "; " + ref["what"] + " (timed in the build container: "
+           "the reference cannot travel to the GPU box)"} if ref else None
+    return {
+        "metric": METRIC, "value": paths / (ms * 1e-3) / 1e6, "unit": METRIC, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"gp: GP-realisation oracle ensemble_radiance, {GP_W}x{GP_H} "
+                               f"pixels x {GP_ROUNDS} realisations, sigma 0.05, l 0.05, depth 64 "
+                               "(SURVEY.md 8(f) rank 4, reference gp.py:334-398)",
+                   "paths_per_step": paths, "evaluations_per_step": evals,
+                   "timing": "CUDA events around each public call (host work inside)"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
+                     "unit": "Ginst/s", "frac": achieved / peak.value, "traffic": None,
+                     "peak_source": "measured on this device by mf_measure_peak_fp64 (DFMA "
+                                    "issue microbenchmark, all SMs)",
+                     "kernel": "gp::reflect_kernel (march + bisection + bounce)",
+                     "work": "51 float64 ops per interpolant evaluation x the device's "
+                             "evaluation counter"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": paths / wall / 1e6, "unit": METRIC, "h2d_bytes_per_step": paths * 48,
+                "d2h_bytes_per_step": paths * 24,
+                "api": "paper_2603_00280_b200.gp.ensemble_radiance()"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -592,6 +703,8 @@ def run_ours(args):
                   file=sys.stderr)
     if args.workload == "config1":
         result = run_queries(args, torch, n, rank, local, dev)
+    elif args.workload == "gp":
+        result = run_gp(args, torch, n, rank, local, dev)
     else:
         result = run_render(args, torch, dist, n, rank, local, dev)
     if result is not None:
@@ -612,7 +725,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="config4",
-                    choices=("config4", "config1", "config2", "config3", "config5"))
+                    choices=("config4", "config1", "config2", "config3", "config5", "gp"))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")

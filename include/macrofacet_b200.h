@@ -324,6 +324,8 @@ int mf_reduce(void* comm, float* d_buf, size_t count, int root, int mode, void* 
 /* Issue-rate peaks of this device measured by microbenchmark kernels
  * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane
  * instructions per second: the FP32 / SFU roofline denominators. */
+/* DFMA issue-rate microbenchmark: the FP64 roofline of the mf_gp_* kernels */
+int mf_measure_peak_fp64(double* dfma_ginst_s, void* stream);
 int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream);
 
 /* diagnostics */
@@ -368,11 +370,12 @@ int mf_gp_first_hit(const mf_gp_grid* grid, const double* d_org, const double* d
 /* the specular bounce loop of ensemble_radiance (gp.py:361-397) for n paths
  * in place: origins d_o, directions d_d, throughput d_thr, radiance d_rad
  * (SoA [3][n]); eta / k: conductor Fresnel per channel (host arrays of 3),
- * NULL for F = 1 */
+ * NULL for F = 1; d_evals (may be NULL) accumulates the interpolant
+ * evaluations (the oracle's work unit) */
 int mf_gp_reflect_paths(const mf_gp_grid* grid, double* d_o, double* d_d, double* d_thr,
                         double* d_rad, const int32_t* d_real, int64_t n, int32_t n_real,
                         double sigma, double env, double eps, double step, int32_t max_bounces,
-                        const double* eta, const double* k, void* stream);
+                        const double* eta, const double* k, uint64_t* d_evals, void* stream);
 
 #ifdef __cplusplus
 }

@@ -130,7 +130,8 @@ SIGNATURES = {
     "mf_gp_reflect_paths": (ctypes.c_int, [ctypes.POINTER(MfGpGrid), _vp, _vp, _vp, _vp, _vp,
                                            ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                           ctypes.c_int32, _vp, _vp, _vp]),
+                                           ctypes.c_int32, _vp, _vp, _vp, _vp]),
+    "mf_measure_peak_fp64": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _vp]),
     "mf_trace_paths": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp,
                                       ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, _vp,
                                       ctypes.POINTER(MfStats), _vp]),

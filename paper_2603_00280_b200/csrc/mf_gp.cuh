@@ -90,9 +90,11 @@ __device__ __forceinline__ void gradient_at(const Grid& G, int r, double px, dou
 struct Hit {
   bool hit;
   double px, py, pz, nx, ny, nz, travel;
+  int evals;   // interpolant evaluations (march + bisection + gradient)
 };
 
 constexpr int kHitBisections = 30;
+
 
 // first_hit (gp.py:148-197) of one ray in realisation r: the march visits
 // t = step, 2 step (by repeated addition, as the reference's shared loop
@@ -103,9 +105,11 @@ __device__ __forceinline__ Hit first_hit(const Grid& G, int r, double ox, double
   double f_prev = field_at(G, r, ox, oy, oz);
   double t_prev = 0.0, lo = 0.0, hi = 0.0;
   bool found = false;
+  int evals = 1;
   const double t_end = da(t_max, step);
   for (double t = step; t <= t_end; t = da(t, step)) {
     double f = field_at(G, r, da(ox, dm(t, dx)), da(oy, dm(t, dy)), da(oz, dm(t, dz)));
+    ++evals;
     if (signbit(f) != signbit(f_prev)) {
       lo = t_prev;
       hi = t;
@@ -131,6 +135,7 @@ __device__ __forceinline__ Hit first_hit(const Grid& G, int r, double ox, double
       }
     }
     h.travel = dm(0.5, da(lo, hi));
+    evals += 1 + kHitBisections;
   } else {
     h.travel = INFINITY;
   }
@@ -145,6 +150,7 @@ __device__ __forceinline__ Hit first_hit(const Grid& G, int r, double ox, double
   h.nx = dd(gx, den);
   h.ny = dd(gy, den);
   h.nz = dd(gz, den);
+  h.evals = evals + 6;
   return h;
 }
 
@@ -237,6 +243,7 @@ struct Paths {
   double eta[3], k[3];
   unsigned long long* tcap;    // per realisation: max march length (ordered bits)
   unsigned int* live;          // live rays after the escape test
+  unsigned long long* evals;   // interpolant evaluations (work counter), or null
 };
 
 // escape upward above the shell (gp.py:366-372), then the march length of
@@ -269,6 +276,7 @@ __global__ void reflect_kernel(const __grid_constant__ Grid G, const __grid_cons
   double t_max = __longlong_as_double((long long)P.tcap[r]);
   double dx = P.d[i], dy = P.d[n + i], dz = P.d[2 * n + i];
   Hit h = first_hit(G, r, P.o[i], P.o[n + i], P.o[2 * n + i], dx, dy, dz, P.step, t_max);
+  if (P.evals) atomicAdd(P.evals, (unsigned long long)h.evals);
   if (!h.hit) {
     for (int c = 0; c < 3; ++c) P.rad[c * n + i] = da(P.rad[c * n + i], dm(P.thr[c * n + i], P.env));
     P.alive[i] = 0;
@@ -289,6 +297,22 @@ __global__ void reflect_kernel(const __grid_constant__ Grid G, const __grid_cons
     P.d[c * n + i] = nd[c];
     P.o[c * n + i] = da(p[c], dm(P.eps, nd[c]));
   }
+}
+
+// DFMA issue-rate microbenchmark (the FP64 roofline of these kernels)
+__global__ void __launch_bounds__(256) peak_dfma_kernel(double* out, int iters, double a,
+                                                        double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 123.456) out[threadIdx.x] = s;
 }
 
 }  // namespace gp

@@ -1973,6 +1973,38 @@ int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* str
   return MF_OK;
 }
 
+int mf_measure_peak_fp64(double* dfma_ginst_s, void* stream) {
+  if (!dfma_ginst_s) return fail(MF_ERR_PARAM, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  MF_CUDA(cudaGetDevice(&dev));
+  MF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* dummy = nullptr;
+  MF_CUDA(cudaMallocAsync((void**)&dummy, 256 * sizeof(double), st));
+  cudaEvent_t e0, e1;
+  MF_CUDA(cudaEventCreate(&e0));
+  MF_CUDA(cudaEventCreate(&e1));
+  const int blocks = sms * 8, threads = 256, it = 2048;
+  double best = 0.0;
+  for (int rep = 0; rep < 3; ++rep) {
+    MF_CUDA(cudaEventRecord(e0, st));
+    mf::gp::peak_dfma_kernel<<<blocks, threads, 0, st>>>(dummy, it, 0.9999, 1e-4);
+    MF_CUDA(cudaEventRecord(e1, st));
+    MF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    MF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    double nops = (double)blocks * threads * it * 8;
+    if (rep) best = std::max(best, nops / (ms * 1e-3) / 1e9);
+    g_launches++;
+  }
+  MF_CUDA(cudaGetLastError());
+  MF_CUDA(cudaFreeAsync(dummy, st));
+  MF_CUDA(cudaEventDestroy(e0));
+  MF_CUDA(cudaEventDestroy(e1));
+  *dfma_ginst_s = best;
+  return MF_OK;
+}
+
 int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream) {
   if (!fp32_ginst_s || !sfu_ginst_s) return fail(MF_ERR_PARAM, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
@@ -2540,7 +2572,7 @@ int mf_gp_first_hit(const mf_gp_grid* grid, const double* d_org, const double* d
 int mf_gp_reflect_paths(const mf_gp_grid* grid, double* d_o, double* d_d, double* d_thr,
                         double* d_rad, const int32_t* d_real, int64_t n, int32_t n_real,
                         double sigma, double env, double eps, double step, int32_t max_bounces,
-                        const double* eta, const double* k, void* stream) {
+                        const double* eta, const double* k, uint64_t* d_evals, void* stream) {
   int rc = gp_check(grid);
   if (rc) return rc;
   if (!d_o || !d_d || !d_thr || !d_rad || !d_real || n < 0 || n_real < 1 || !(step > 0.0))
@@ -2551,6 +2583,7 @@ int mf_gp_reflect_paths(const mf_gp_grid* grid, double* d_o, double* d_d, double
   P.o = d_o; P.d = d_d; P.thr = d_thr; P.rad = d_rad; P.real = d_real; P.n = n;
   P.sigma = sigma; P.env = env; P.eps = eps; P.step = step;
   P.fresnel = (eta && k) ? 1 : 0;
+  P.evals = (unsigned long long*)d_evals;
   for (int c = 0; c < 3; ++c) {
     P.eta[c] = P.fresnel ? eta[c] : 0.0;
     P.k[c] = P.fresnel ? k[c] : 0.0;

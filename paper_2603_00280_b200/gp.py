@@ -458,12 +458,13 @@ def camera_rays(camera, px, py, jitter_x, jitter_y):
 
 
 def ensemble_radiance(kernel, camera, spp, m_realizations, rng, env_radiance=1.0, fresnel=None,
-                      max_bounces=64, spec=None):
+                      max_bounces=64, spec=None, work=None):
     """Ensemble-averaged radiance of a planar statistical surface patch:
     per sample round one fresh realisation shared by all pixels; paths
     reflect specularly off first-hit normals until they escape upward and
     gather the constant environment (gp.py:334-398).  All rounds run in one
-    batch on the device."""
+    batch on the device.  `work` (a dict, optional) receives the number of
+    interpolant evaluations and paths."""
     w, h = camera.width, camera.height
     if w * h > 64 * 64:
         raise ConfigError("ensemble radiance is desk-scale only (<= 64x64 pixels)")
@@ -508,6 +509,7 @@ def ensemble_radiance(kernel, camera, spp, m_realizations, rng, env_radiance=1.0
         T = torch.ones((3, m), dtype=torch.float64, device=dev)
         L = torch.zeros((3, m), dtype=torch.float64, device=dev)
         R = torch.arange(B, dtype=torch.int32, device=dev).repeat_interleave(h * w)
+        ev = torch.zeros(1, dtype=torch.int64, device=dev) if work is not None else None
         cg = batch.c_grid()
         _lib.check(lib.mf_gp_reflect_paths(
             ctypes.byref(cg), ctypes.c_void_p(O.data_ptr()), ctypes.c_void_p(D.data_ptr()),
@@ -515,7 +517,11 @@ def ensemble_radiance(kernel, camera, spp, m_realizations, rng, env_radiance=1.0
             ctypes.c_void_p(R.data_ptr()), m, B, float(kernel.sigma), float(env_radiance),
             float(eps), float(step), int(max_bounces),
             eta_k[0] if eta_k else None, eta_k[1] if eta_k else None,
+            ctypes.c_void_p(ev.data_ptr()) if ev is not None else None,
             _lib.stream_handle(torch, dev)))
+        if work is not None:
+            work["evals"] = work.get("evals", 0) + int(ev.item())
+            work["paths"] = work.get("paths", 0) + m
         rad = L.cpu().numpy().T.reshape(B, h, w, 3)
         for j in range(B):       # the reference's round-by-round sum
             img += rad[j]
