@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-for v in u1 u4 u8; do
-MF_LIB_PATH=variants/$v.so timeout 900 python bench.py --workload gp --steps 3 --warmup 1 > gpurun_out/bench_gp_$v.json 2>&1
-done
-timeout 900 python -m pytest tests/test_gpu_gp.py -q -p no:cacheprovider --tb=short > gpurun_out/gp_tests.log 2>&1
-echo "rc=$?" >> gpurun_out/gp_tests.log
+( python tools/ab_env.py MF_GRID_TEXTURE config5 256 16; python tools/ab_env.py MF_GRID_TEXTURE config5 512 16 ) > gpurun_out/ab.txt 2>&1
+timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -k "grid" > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log

@@ -17,7 +17,7 @@ cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True,
                      text=True).stdout.splitlines()
 
-FDEF = re.compile(r"^\s*(?:template\s*<[^>]*>\s*)?(?:__device__|__global__|inline|static|__forceinline__|MF_HD|MF_DEV)[^;(]*?\b(\w+)\s*\(")
+FDEF = re.compile(r"^\s*(?:template\s*<[^>]*>\s*)?(?:__device__|__global__|inline|static|__forceinline__|MF_\w+)[^;(]*?\b(\w+)\s*\(")
 fcache = {}
 
 
