@@ -108,6 +108,25 @@ def _plane_field():
     return p
 
 
+_PLANE_FIELD = _plane_field()
+
+
+_C_MEDIA = {}
+
+
+def _c_medium_cached(medium):
+    """to_c_medium, memoised by value for hashable (frozen) media."""
+    try:
+        c = _C_MEDIA.get(medium)
+    except TypeError:          # unhashable (a duck-typed medium): no cache
+        return to_c_medium(medium)
+    if c is None:
+        if len(_C_MEDIA) > 256:
+            _C_MEDIA.clear()
+        c = _C_MEDIA[medium] = to_c_medium(medium)
+    return c
+
+
 _QUERY_OUTS = ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx", "wsy", "wsz", "pdf_s",
                "w_r", "w_g", "w_b", "flags")
 
@@ -128,10 +147,19 @@ def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None,
     for t in (p, wo, wi, u1, u2):
         if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
             raise ParameterDomainError("query_batch expects contiguous float32 CUDA tensors")
+    for t in (p, wo, wi):
+        if t.dim() != 2 or t.shape[0] != 3 or t.shape[1] != n:
+            raise ParameterDomainError("p / wo / wi must be (3, n) tensors")
+    # SoA rows by pointer arithmetic (no per-row tensor views: the host path
+    # of a 2^20 batch must stay shorter than its ~50 us kernel)
     qi = _lib.MfQueryIn()
-    qi.px, qi.py, qi.pz = (p[k].data_ptr() for k in range(3))
-    qi.wox, qi.woy, qi.woz = (wo[k].data_ptr() for k in range(3))
-    qi.wix, qi.wiy, qi.wiz = (wi[k].data_ptr() for k in range(3))
+    row = 4 * n
+    a = p.data_ptr()
+    qi.px, qi.py, qi.pz = a, a + row, a + 2 * row
+    a = wo.data_ptr()
+    qi.wox, qi.woy, qi.woz = a, a + row, a + 2 * row
+    a = wi.data_ptr()
+    qi.wix, qi.wiy, qi.wiz = a, a + row, a + 2 * row
     qi.u1, qi.u2 = u1.data_ptr(), u2.data_ptr()
     qi.f = f.data_ptr() if f is not None else None
     qi.frame = frame.data_ptr() if frame is not None else None
@@ -149,8 +177,8 @@ def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None,
             raise ParameterDomainError(f"output {name!r} must be a contiguous ({n},) "
                                        f"{want} CUDA tensor")
         setattr(qo, name, t.data_ptr())
-    fld = field if field is not None else _plane_field()
-    cm = to_c_medium(medium)
+    fld = field if field is not None else _PLANE_FIELD
+    cm = _c_medium_cached(medium)
     s = stream if stream is not None else _lib.stream_handle(torch, dev)
     _lib.check(lib.mf_query_batch(ctypes.byref(cm), ctypes.byref(fld), ctypes.byref(qi),
                                   ctypes.byref(qo), n, s))
