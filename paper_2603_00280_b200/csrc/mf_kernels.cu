@@ -2246,7 +2246,6 @@ int mf_render_async(const mf_scene* scene, const mf_render_params* params, float
   fx_scale(emax, s_count, &ps.fx_scale, &ps.fx_limit, &k);
   // path-kernel timing: one event pair per launch, read after the final sync
   std::vector<cudaEvent_t> ev;
-  double kernel_ms = 0.0;
   for (uint32_t s0 = 0; s0 < s_count; s0 += S_pass) {
     uint32_t S = std::min(S_pass, s_count - s0);
     ps.S = S;
