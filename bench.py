@@ -495,7 +495,7 @@ def run_queries(args, torch, n, rank, local, dev):
              ("u2", u[a:b, 1]))}
     d = {k: v.to(dev) for k, v in host.items()}
     outs = {k: torch.empty(b - a, dtype=torch.int32 if k == "flags" else torch.float32,
-                           device=dev) for k in mf.medium._QUERY_OUTS}
+                           device=dev) for k in mf.medium._QUERY_DEFAULT}
     host_out = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in outs.items()}
 
     def call(dd, oo):

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MF_ABI_VERSION 3
+#define MF_ABI_VERSION 4
 
 enum mf_status {
   MF_OK = 0,
@@ -194,6 +194,8 @@ typedef struct mf_query_out {
   float* pdf_s;
   float *w_r, *w_g, *w_b;
   int32_t* flags; /* bit0 degenerate view (sigma(wo) < 1e-12) */
+  float *wmx, *wmy, *wmz; /* the sampled visible normal (vndf_sample, ndf.py:409-427) */
+  float* pdf_m;           /* its mixture density (ndf.py:397-405) */
 } mf_query_out;
 
 int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_query_in* d_in,
@@ -280,7 +282,12 @@ enum mf_curve_kind {
   MF_CURVE_PROJECTED_AREA = 1,
   MF_CURVE_NDF = 2,
   MF_CURVE_VNDF = 3,
-  MF_CURVE_TRANSMITTANCE = 4
+  MF_CURVE_TRANSMITTANCE = 4,
+  MF_CURVE_DENSITY = 5,    /* rho(f) = phi(f/s) / (s Phi(f/s)), f = d_x[i]   density, medium.py:70-88 */
+  MF_CURVE_FRESNEL = 6,    /* conductor F(cos_i = d_x[i]) of channel 0 (eta[0], k[0]),
+                              fresnel_conductor, medium.py:127-147 */
+  MF_CURVE_GDF = 7         /* gradient density at g = (d_x, d_y, d_z), gdf_pdf, ndf.py:232-239
+                              (GENERALIZED media only) */
 };
 int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d_y,
              const float* d_z, int64_t n, const double params[4], float* d_out, void* stream);
@@ -324,6 +331,10 @@ int mf_reduce(void* comm, float* d_buf, size_t count, int root, int mode, void* 
 /* Issue-rate peaks of this device measured by microbenchmark kernels
  * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane
  * instructions per second: the FP32 / SFU roofline denominators. */
+/* float64 special functions on the device (the reference's core.py:29-98
+ * erf / erfc / the Gaussian pieces): which 0 erf, 1 erfc, 2 exp(-x) */
+int mf_special_f64(int which, const double* d_x, int64_t n, double* d_out, void* stream);
+
 /* DFMA issue-rate microbenchmark: the FP64 roofline of the mf_gp_* kernels */
 int mf_measure_peak_fp64(double* dfma_ginst_s, void* stream);
 int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream);

@@ -7,10 +7,16 @@ kernels behind the C ABI in include/macrofacet_b200.h.  No CPU fallback."""
 
 __version__ = "0.1.0"
 
-from .core import Frame, build_frame, dot, normalize
-from .curves import (generalized_lambda, generalized_lambda_dir, generalized_ndf,
-                     generalized_ndf_dir, planar_transmittance, projected_area,
-                     projected_area_dir, vndf_eval)
+from . import gp
+from .core import (Frame, build_frame, direction_to_spherical, dot, erf, erfc, gauss_cdf,
+                   gauss_pdf, normalize, reflect, spherical_to_direction)
+from .curves import (beckmann_ndf, density, fresnel_conductor, gdf_pdf, generalized_lambda,
+                     generalized_lambda_dir, generalized_ndf, generalized_ndf_dir, ggx_ndf,
+                     planar_transmittance, projected_area, projected_area_dir, sample_gdf,
+                     vndf_eval, vndf_sample)
+from .gp import (FirstHit, GpRealization, GridSpec, default_grid, empirical_transmittance,
+                 empirical_vndf, ensemble_radiance, first_hit, multiplicativity_probe,
+                 realize_gp)
 from .errors import (ConfigError, DegenerateVisibilityError, GrazingSingularityError,
                      InternalConsistencyError, IoError, MacrofacetError, NumericFailureError,
                      ParameterDomainError, UnsupportedGeometryError)

@@ -24,12 +24,13 @@ MF_MAX_MEDIA = 8
 
 KIND = {"beckmann": 0, "ggx": 1, "generalized": 2}
 REDUCE_NCCL, REDUCE_ORDERED = 0, 1
-CURVE = {"lambda": 0, "projected-area": 1, "ndf": 2, "vndf": 3, "transmittance": 4}
+CURVE = {"lambda": 0, "projected-area": 1, "ndf": 2, "vndf": 3, "transmittance": 4, "density": 5,
+         "fresnel": 6, "gdf": 7}
 COMM_ID_BYTES = 128
 FRESNEL_CONDUCTOR, FRESNEL_ONE, FRESNEL_ALBEDO = 0, 1, 2
 SHAPE_PLANE, SHAPE_SPHERE, SHAPE_GRID, SHAPE_BOX = 0, 1, 2, 3
 WALK_COLLISION, WALK_RATIO, WALK_TENTATIVE = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 SHARD_TILES, SHARD_SAMPLES = 0, 1
 
 _d3 = ctypes.c_double * 3
@@ -106,7 +107,8 @@ class MfQueryIn(ctypes.Structure):
 
 class MfQueryOut(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx",
-                                   "wsy", "wsz", "pdf_s", "w_r", "w_g", "w_b", "flags")]
+                                   "wsy", "wsz", "pdf_s", "w_r", "w_g", "w_b", "flags", "wmx",
+                                   "wmy", "wmz", "pdf_m")]
 
 
 # exported symbols and their signatures (must match include/macrofacet_b200.h)
@@ -132,6 +134,7 @@ SIGNATURES = {
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "mf_measure_peak_fp64": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _vp]),
+    "mf_special_f64": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int64, _vp, _vp]),
     "mf_trace_paths": (ctypes.c_int, [ctypes.POINTER(MfScene), _vp, _vp, _vp, _vp,
                                       ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, _vp,
                                       ctypes.POINTER(MfStats), _vp]),

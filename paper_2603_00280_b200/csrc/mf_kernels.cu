@@ -101,6 +101,15 @@ __global__ void __launch_bounds__(256) curve_kernel(const __grid_constant__ Curv
       float h1 = __ldg(a.x + i);
       float dl = log_ndtr(h1 * a.m.inv_sigma) - log_ndtr(a.z0 * a.m.inv_sigma);
       r = expf(-a.sig_wo * dl);
+    } else if (a.kind == MF_CURVE_DENSITY) {
+      r = mills(__ldg(a.x + i) * a.m.inv_sigma) * a.m.inv_sigma;
+    } else if (a.kind == MF_CURVE_FRESNEL) {
+      r = fresnel_conductor(__ldg(a.x + i), a.m.eta[0], a.m.k[0]);
+    } else if (a.kind == MF_CURVE_GDF) {
+      // Gaussian gradient density conditioned on a crossing (ndf.py:232-239)
+      float gx = __ldg(a.x + i) * a.m.inv_ax, gy = __ldg(a.y + i) * a.m.inv_ay;
+      float gz = (__ldg(a.z + i) - 1.0f) * (1.0f / a.m.az);
+      r = expf(-fmaf(gx, gx, fmaf(gy, gy, gz * gz))) * a.m.d_norm;
     } else {
       V3 w = v3(__ldg(a.x + i), __ldg(a.y + i), __ldg(a.z + i));
       if (a.kind == MF_CURVE_LAMBDA) r = proj_area(a.m, w) / w.z;
@@ -155,7 +164,22 @@ __device__ __forceinline__ void query_write_sample(const mf_query_out& o, int64_
   if (o.w_b) o.w_b[i] = w.z;
 }
 
+// the visible normal of the sample and its mixture density (vndf_sample);
+// out of the config-1 path unless requested (uniform test on the pointer)
+template <bool kNormal>
+__device__ __forceinline__ void query_write_normal(const mf_query_out& o, int64_t i,
+                                                   const Frame& fr, const PhaseSample& smp) {
+  if (kNormal) {
+    V3 wm = to_world(fr, smp.wm);
+    if (o.wmx) o.wmx[i] = wm.x;
+    if (o.wmy) o.wmy[i] = wm.y;
+    if (o.wmz) o.wmz[i] = wm.z;
+    if (o.pdf_m) o.pdf_m[i] = smp.pdf_m;
+  }
+}
+
 // Beckmann branch and tail of ring entry k
+template <bool kNormal>
 __device__ __forceinline__ void query_beckmann(const QueryArgs& a, const QueryRing& R, int k) {
   const MediumK& m = a.m;
   int64_t j = (int64_t)(((uint64_t)R.idx_hi[k] << 32) | R.idx_lo[k]);
@@ -169,8 +193,12 @@ __device__ __forceinline__ void query_beckmann(const QueryArgs& a, const QueryRi
   V3 wm = beckmann_visible_normal<true>(m, v, R.uu[k], R.u2[k], &iters);
   PhaseSample smp = phase_sample_tail(m, v, wm, dot3(v, wm), R.sig_o[k], R.sig_b[k], true);
   query_write_sample(a.out, j, to_world(fr, smp.wi), smp.pdf, smp.weight);
+  query_write_normal<kNormal>(a.out, j, fr, smp);
 }
 
+// kNormal: the caller asked for the sampled visible normal / its density
+// (vndf_sample); the config-1 build carries neither
+template <bool kNormal>
 __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ QueryArgs a) {
   __shared__ QueryRing rings[kQBlock / 32];
   const unsigned full = 0xffffffffu;
@@ -230,6 +258,12 @@ __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ 
       if (o.flags) o.flags[i] = degenerate ? 1 : 0;
       if (degenerate) {
         query_write_sample(o, i, wo, 0.0f, v3(0.0f, 0.0f, 0.0f));
+        if (kNormal) {
+          if (o.wmx) o.wmx[i] = 0.0f;
+          if (o.wmy) o.wmy[i] = 0.0f;
+          if (o.wmz) o.wmz[i] = 0.0f;
+          if (o.pdf_m) o.pdf_m[i] = 0.0f;
+        }
       } else if (guided && u1 < m.mix) {
         queue = true;
       } else {
@@ -238,6 +272,7 @@ __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ 
         V3 wm = hemisphere_about(v, uu, u2);
         PhaseSample smp = phase_sample_tail(m, v, wm, uu, sig_safe, sig_b, guided);
         query_write_sample(o, i, to_world(fr, smp.wi), smp.pdf, smp.weight);
+        query_write_normal<kNormal>(o, i, fr, smp);
       }
     }
     // enqueue the Beckmann-branch queries of this chunk
@@ -255,14 +290,14 @@ __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ 
     tail += (unsigned)__popc(qm);
     __syncwarp();
     if (tail - head >= 32) {
-      query_beckmann(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
+      query_beckmann<kNormal>(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
       head += 32;
       __syncwarp();
     }
   }
   // drain
   int left = (int)(tail - head);
-  if (lane < left) query_beckmann(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
+  if (lane < left) query_beckmann<kNormal>(a, R, (int)((head + (unsigned)lane) & (kQRing - 1)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1517,6 +1552,16 @@ __global__ void __launch_bounds__(128) grid_skip_kernel(float* maj, int n) {
 // ---------------------------------------------------------------------------
 // roofline microbenchmarks: 8 independent FFMA chains / 4 MUFU.EX2 chains
 
+// erf / erfc / exp(-x) in float64 (CUDA's correctly-rounded-to-a-few-ulp
+// double functions; erf(-x) = -erf(x) exactly as the reference's)
+__global__ void __launch_bounds__(256) special_f64_kernel(int which, const double* x, int64_t n,
+                                                          double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = x[i];
+  out[i] = which == 0 ? copysign(erf(fabs(v)), v) : (which == 1 ? erfc(v) : exp(-v));
+}
+
 __global__ void __launch_bounds__(256) peak_ffma_kernel(float* out, int iters, float a, float b) {
   float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
   float x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
@@ -1973,6 +2018,17 @@ int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* str
   return MF_OK;
 }
 
+int mf_special_f64(int which, const double* d_x, int64_t n, double* d_out, void* stream) {
+  if (which < 0 || which > 2) return fail(MF_ERR_PARAM, "unknown special function");
+  if (n < 0 || (n > 0 && (!d_x || !d_out))) return fail(MF_ERR_PARAM, "bad special_f64 arguments");
+  if (!n) return MF_OK;
+  special_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(which, d_x, n,
+                                                                                   d_out);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
 int mf_measure_peak_fp64(double* dfma_ginst_s, void* stream) {
   if (!dfma_ginst_s) return fail(MF_ERR_PARAM, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
@@ -2087,10 +2143,13 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
   // two resident waves: every warp loops over many 32-query chunks, so its
   // Beckmann ring fills to full warps
   int per_sm = 1;
-  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_kernel, kQBlock, 0));
+  bool normal = a.out.wmx || a.out.wmy || a.out.wmz || a.out.pdf_m;
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, normal ? query_kernel<true> : query_kernel<false>, kQBlock, 0));
   int64_t blocks = (n + kQBlock - 1) / kQBlock;
   int grid = (int)std::min<int64_t>(blocks, (int64_t)sms * std::max(per_sm, 1) * 2);
-  query_kernel<<<grid, kQBlock, 0, (cudaStream_t)stream>>>(a);
+  if (normal) query_kernel<true><<<grid, kQBlock, 0, (cudaStream_t)stream>>>(a);
+  else query_kernel<false><<<grid, kQBlock, 0, (cudaStream_t)stream>>>(a);
   g_launches++;
   MF_CUDA(cudaGetLastError());
   return MF_OK;
@@ -2099,9 +2158,10 @@ int mf_query_batch(const mf_medium* medium, const mf_primitive* field, const mf_
 int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d_y,
              const float* d_z, int64_t n, const double params[4], float* d_out, void* stream) {
   if (!medium || !params || (n > 0 && (!d_x || !d_out))) return fail(MF_ERR_PARAM, "null argument");
-  if (kind < MF_CURVE_LAMBDA || kind > MF_CURVE_TRANSMITTANCE)
+  if (kind < MF_CURVE_LAMBDA || kind > MF_CURVE_GDF)
     return fail(MF_ERR_PARAM, "unknown curve kind " + std::to_string(kind));
-  if (kind != MF_CURVE_TRANSMITTANCE && n > 0 && (!d_y || !d_z))
+  bool scalar = kind == MF_CURVE_TRANSMITTANCE || kind == MF_CURVE_DENSITY || kind == MF_CURVE_FRESNEL;
+  if (!scalar && n > 0 && (!d_y || !d_z))
     return fail(MF_ERR_PARAM, "direction arrays are null");
   if (n < 0) return fail(MF_ERR_PARAM, "n must be >= 0");
   CurveArgs a;
@@ -2130,6 +2190,8 @@ int mf_curve(const mf_medium* medium, int kind, const float* d_x, const float* d
     if (!(a.sig_wo >= 1e-12f))
       return fail(MF_ERR_DEGENERATE, "sigma(wo) < 1e-12: visible normals undefined");
   }
+  if (kind == MF_CURVE_GDF && medium->kind != MF_KIND_GENERALIZED)
+    return fail(MF_ERR_PARAM, "gdf_pdf requires az > 0");
   if (kind == MF_CURVE_TRANSMITTANCE) {
     if (std::fabs(wz) < 1e-12)
       return fail(MF_ERR_UNSUPPORTED, "planar transmittance is undefined at cos(theta) = 0");

@@ -146,3 +146,100 @@ def planar_transmittance(h0, h1, theta, phi, medium: MacrofacetMedium):
         raise UnsupportedGeometryError("closed-form transmittance covers the erf-family lambda only")
     wo = tuple(_sph_dir(theta, float(phi)))
     return _curve_host(medium, "transmittance", t=h1, wo=wo, z0=float(h0))
+
+
+# ---------------------------------------------------------------------------
+# the reference's remaining public helpers of the path, on the device
+
+def _scalar_curve(medium, kind, x):
+    x = np.asarray(x, dtype=np.float64)
+    return _curve_host(medium, kind, t=x)
+
+
+def density(f, sigma):
+    """Microflake density rho(f) = phi(f/s) / (s Phi(f/s)) (medium.py:70-88),
+    fp32 on the device (erfcx form: no underflow deep below the surface)."""
+    sigma = float(sigma)
+    if not sigma > 0.0:
+        raise ParameterDomainError(f"sigma must be > 0, got {sigma}")
+    med = MacrofacetMedium(kind=NdfKind.GENERALIZED, a3=RoughnessTriple(1.0, 1.0, 1.0),
+                           sigma=sigma, fresnel_one=True)
+    return _scalar_curve(med, "density", f)
+
+
+def fresnel_conductor(cos_i, eta, k):
+    """Unpolarised conductor reflectance (medium.py:127-147); eta / k scalars
+    or per-channel arrays broadcast against cos_i (device, fp32)."""
+    cos_i = np.asarray(cos_i, dtype=np.float64)
+    eta = np.asarray(eta, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    c, e, kk = np.broadcast_arrays(cos_i, eta, k)
+    out = np.empty(c.shape)
+    pairs = {}
+    for idx in np.ndindex(c.shape) if c.shape else [()]:
+        pairs.setdefault((float(e[idx]), float(kk[idx])), []).append(idx)
+    for (ev, kv), idxs in pairs.items():
+        med = MacrofacetMedium(kind=NdfKind.GENERALIZED, a3=RoughnessTriple(1.0, 1.0, 1.0),
+                               sigma=1.0, fresnel_eta=(ev, ev, ev), fresnel_k=(kv, kv, kv))
+        vals = np.atleast_1d(_scalar_curve(med, "fresnel", np.array([c[i] for i in idxs])))
+        for i, v in zip(idxs, vals):
+            out[i] = v
+    return out[()]
+
+
+def beckmann_ndf(wm, ax, ay):
+    """Height-field Beckmann D(wm) (ndf.py:85-94), device."""
+    return ndf_dir(wm, NdfKind.BECKMANN, RoughnessTriple(float(ax), float(ay), 0.0))
+
+
+def ggx_ndf(wm, ax, ay):
+    """GGX D(wm) (ndf.py:97-103), device."""
+    return ndf_dir(wm, NdfKind.GGX, RoughnessTriple(float(ax), float(ay), 0.0))
+
+
+def gdf_pdf(g, a3: RoughnessTriple):
+    """Gradient density conditioned on a zero crossing: Gaussian with mean
+    (0, 0, 1) and variances alpha_i^2 / 2 (ndf.py:232-239), device."""
+    if a3.az <= 0.0:
+        raise ParameterDomainError("gdf_pdf requires az > 0")
+    med = MacrofacetMedium(kind=NdfKind.GENERALIZED, a3=a3, sigma=1.0, fresnel_one=True)
+    return _curve_host(med, "gdf", w=g)
+
+
+def sample_gdf(a3: RoughnessTriple, rng, n: int):
+    """n gradients from the conditioned gradient distribution (ndf.py:242-246):
+    the stream's normals scaled by alpha / sqrt2 about (0, 0, 1)."""
+    z = rng.normal((n, 3))
+    return z * (np.array([a3.ax, a3.ay, a3.az]) / np.sqrt(2.0)) + np.array([0.0, 0.0, 1.0])
+
+
+def vndf_sample(wo, kind: NdfKind, a3: RoughnessTriple, mix_ratio, rng, n=None):
+    """Visible normals for propagation direction wo and their exact mixture
+    pdf (ndf.py:383-427): the device's phase sampler (query_kernel) returns
+    the normal it drew and its density.  Three uniforms per sample are
+    taken from rng as the reference does; the device's two-uniform
+    convention uses the first and the third."""
+    from .core import Frame
+    from .errors import DegenerateVisibilityError
+    from .medium import _host_query
+
+    if not (0.0 <= mix_ratio <= 1.0):
+        raise ParameterDomainError(f"mix_ratio must lie in [0, 1], got {mix_ratio}")
+    wo = np.asarray(wo, dtype=np.float64)
+    if np.any(np.asarray(projected_area_dir(wo, kind, a3)) <= 0.0):
+        raise DegenerateVisibilityError("projected area is zero toward wo")
+    shape = wo.shape[:-1] if n is None else (n,)
+    u = rng.uniform(shape + (3,))
+    if n is not None and wo.ndim == 1:
+        wo = np.broadcast_to(wo, (n, 3))
+    a = a3 if kind is NdfKind.GENERALIZED else RoughnessTriple(a3.ax, a3.ay, 0.0)
+    med = MacrofacetMedium(kind=kind, a3=a, sigma=1.0, fresnel_one=True, mix_ratio=mix_ratio)
+    ident = Frame(tangent=np.array([1.0, 0.0, 0.0]), bitangent=np.array([0.0, 1.0, 0.0]),
+                  normal=np.array([0.0, 0.0, 1.0]))
+    r, _ = _host_query(med, wo, None, None, ident, np.stack([u[..., 0], u[..., 2]], axis=-1),
+                       ("wmx", "wmy", "wmz", "pdf_m", "flags"))
+    if np.any(r["flags"] & 1):
+        raise DegenerateVisibilityError("projected area is zero toward wo")
+    wm = np.stack([r["wmx"], r["wmy"], r["wmz"]], axis=-1).astype(np.float64)
+    pdf = r["pdf_m"].astype(np.float64)
+    return wm, pdf[()]

@@ -127,12 +127,15 @@ def _c_medium_cached(medium):
     return c
 
 
-_QUERY_OUTS = ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx", "wsy", "wsz", "pdf_s",
-               "w_r", "w_g", "w_b", "flags")
+# the config-1 outputs (query_batch's default) and the optional visible
+# normal of the sample and its mixture density (vndf_sample)
+_QUERY_DEFAULT = ("sigma_t", "phase_r", "phase_g", "phase_b", "pdf", "wsx", "wsy", "wsz", "pdf_s",
+                  "w_r", "w_g", "w_b", "flags")
+_QUERY_OUTS = _QUERY_DEFAULT + ("wmx", "wmy", "wmz", "pdf_m")
 
 
 def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None, frame=None,
-                outputs=_QUERY_OUTS, stream=None, out=None):
+                outputs=_QUERY_DEFAULT, stream=None, out=None):
     """Fused coefficient query (BASELINE config 1) on device tensors.
 
     p, wo, wi: (3, n) float32 CUDA tensors (SoA rows); u1, u2: (n,).

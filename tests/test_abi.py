@@ -44,7 +44,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_error_string(lib):
     lib.mf_abi_version.restype = ctypes.c_int
-    assert lib.mf_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.mf_abi_version() == _lib.ABI_VERSION == 4
     lib.mf_last_error.restype = ctypes.c_char_p
     assert isinstance(lib.mf_last_error(), bytes)
 

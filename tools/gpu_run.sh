@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python tools/time_variants.py variants/base.so variants/constm.so variants/base.so variants/constm.so > gpurun_out/variants.txt 2>&1
+timeout 900 python bench.py --workload config1 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_config1.json 2> gpurun_out/bench_config1.err
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -k "query or helpers" > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log
