@@ -335,6 +335,14 @@ int mf_reduce(void* comm, float* d_buf, size_t count, int root, int mode, void* 
  * erf / erfc / the Gaussian pieces): which 0 erf, 1 erfc, 2 exp(-x) */
 int mf_special_f64(int which, const double* d_x, int64_t n, double* d_out, void* stream);
 
+/* Radial Gauss-Legendre quadrature of the gradient distribution along wm
+ * (ndf_from_gdf_quadrature, ndf.py:254-293): the sum over n_sub equal
+ * pieces of [0, t_max] x 32 nodes (host arrays nodes / weights) of
+ * t^3 exp(-(a t^2 - 2 b t + c) - shift), times the piece half-width, in
+ * float64; *total receives it (host). */
+int mf_gdf_radial(double a, double b, double c, double shift, double t_max, int32_t n_sub,
+                  const double nodes[32], const double weights[32], double* total, void* stream);
+
 /* DFMA issue-rate microbenchmark: the FP64 roofline of the mf_gp_* kernels */
 int mf_measure_peak_fp64(double* dfma_ginst_s, void* stream);
 int mf_measure_peaks(double* fp32_ginst_s, double* sfu_ginst_s, void* stream);

@@ -12,6 +12,7 @@ from .core import (Frame, build_frame, direction_to_spherical, dot, erf, erfc, g
                    gauss_pdf, normalize, reflect, spherical_to_direction)
 from .curves import (beckmann_ndf, density, fresnel_conductor, gdf_pdf, generalized_lambda,
                      generalized_lambda_dir, generalized_ndf, generalized_ndf_dir, ggx_ndf,
+                     ndf_from_gdf_quadrature,
                      planar_transmittance, projected_area, projected_area_dir, sample_gdf,
                      vndf_eval, vndf_sample)
 from .gp import (FirstHit, GpRealization, GridSpec, default_grid, empirical_transmittance,

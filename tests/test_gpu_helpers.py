@@ -79,3 +79,18 @@ def test_vndf_sample(cuda):
     # the unbiased weight vndf / pdf integrates to one
     w = om.vndf(wm, np.broadcast_to(wo, wm.shape), "generalized", 0.6, 0.6, 0.4) / pdf
     assert abs(w.mean() - 1.0) < 4 * w.std() / np.sqrt(len(w))
+
+
+def test_ndf_from_gdf_quadrature(cuda):
+    """The radial quadrature (ndf.py:254-293) on the device in float64: the
+    reference suite's pinned value at the pole for alpha = 1 (test_ndf.py:
+    170-177) and agreement with the closed-form generalized NDF."""
+    iso1 = mf.RoughnessTriple(1.0, 1.0, 1.0)
+    assert abs(mf.ndf_from_gdf_quadrature(0.0, 0.0, iso1) - 0.7992537597222495) < 1e-10
+    a3 = mf.RoughnessTriple(0.8, 0.5, 0.3)
+    for th, ph in ((0.3, 0.2), (1.2, 2.0), (2.5, 4.0)):
+        q = mf.ndf_from_gdf_quadrature(th, ph, a3)
+        d = float(mf.generalized_ndf(th, ph, a3))
+        assert abs(d / q - 1.0) < 2e-5, (th, ph, q, d)
+    with pytest.raises(mf.ParameterDomainError):
+        mf.ndf_from_gdf_quadrature(0.1, 0.0, mf.RoughnessTriple(1.0, 1.0, 0.0))
