@@ -11,7 +11,7 @@ echo "pytest rc=$?" >> gpurun_out/gpu_tests_full.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
 echo "bench config4 rc=$?"
-for wl in ${WORKLOADS:-config1 config2 config3 config5}; do
+for wl in ${WORKLOADS:-config1 config2 config3 config5 gp}; do
   st=3; [ "$wl" = config5 ] && st=1
   timeout 900 python bench.py --workload $wl --steps $st --warmup 3 --no-cpu \
       > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err
