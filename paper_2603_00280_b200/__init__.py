@@ -23,7 +23,7 @@ from .errors import (ConfigError, DegenerateVisibilityError, GrazingSingularityE
                      ParameterDomainError, UnsupportedGeometryError)
 from .image import RadianceImage, read_pfm, write_image, write_pfm, write_ppm
 from .medium import (MacrofacetMedium, extinction, phase_eval, phase_pdf, phase_sample,
-                     query_batch)
+                     query_batch, query_batch_host)
 from .ndf import KernelParams, NdfKind, RoughnessTriple, roughness_from_kernel
 from .render import PathKeys, render, render_device, render_sharded, trace_path, trace_paths
 from .rng import BatchRng, RandomStream, derive_bases, stream_base

@@ -188,6 +188,54 @@ def query_batch(medium: MacrofacetMedium, p, wo, wi, u1, u2, field=None, f=None,
     return out
 
 
+_STREAMS = {}   # the pipeline's three streams per device, created once
+
+
+def query_batch_host(medium: MacrofacetMedium, p, wo, wi, u1, u2, out=None,
+                     outputs=_QUERY_DEFAULT, chunk=1 << 19, device=None):
+    """The fused coefficient query from HOST tensors to host tensors
+    (BASELINE config 1 end to end): chunks of `chunk` queries flow through
+    three CUDA streams -- copy in, query_kernel, copy out -- so the PCIe
+    transfers of one chunk overlap the kernel and the transfers of the
+    others.  p / wo / wi: (3, n) float32 CPU tensors (pinned for the copies
+    to run asynchronously), u1 / u2: (n,).  `out`: {name: (n,) CPU tensor}
+    (pinned) to write into; returns it."""
+    torch = _lib.require_cuda()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = int(u1.numel())
+    if out is None:
+        out = {name: torch.empty(n, dtype=torch.int32 if name == "flags" else torch.float32,
+                                 pin_memory=True) for name in outputs}
+    cur = torch.cuda.current_stream(dev)
+    streams = _STREAMS.get(dev)
+    if streams is None:
+        streams = _STREAMS[dev] = [torch.cuda.Stream(dev) for _ in range(3)]
+    for st in streams:
+        st.wait_stream(cur)
+    for c, a in enumerate(range(0, n, chunk)):
+        b = min(n, a + chunk)
+        st = streams[c % 3]
+        with torch.cuda.stream(st):
+            d = []
+            for t in (p, wo, wi):        # (3, m) device buffers from the contiguous host rows
+                x = torch.empty((3, b - a), dtype=torch.float32, device=dev)
+                for k in range(3):
+                    x[k].copy_(t[k, a:b], non_blocking=True)
+                d.append(x)
+            d1 = u1[a:b].to(dev, non_blocking=True)
+            d2 = u2[a:b].to(dev, non_blocking=True)
+            r = query_batch(medium, d[0], d[1], d[2], d1, d2, outputs=tuple(out),
+                            stream=_lib.stream_handle(torch, dev))
+            for name, t in r.items():
+                out[name][a:b].copy_(t, non_blocking=True)
+            for t in (*d, d1, d2, *r.values()):   # keep the chunk's buffers until done
+                t.record_stream(st)
+    for st in streams:
+        cur.wait_stream(st)
+    cur.synchronize()
+    return out
+
+
 def _frame_rows(local_frame: Frame, shape):
     rows = []
     for v in (local_frame.tangent, local_frame.bitangent, local_frame.normal):

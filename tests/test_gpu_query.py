@@ -284,3 +284,18 @@ def test_throughput_smoke(cuda):
     a = mf.query_batch(med, P, WO, WI, t(u[:, 0], 16), t(u[:, 1], 16), outputs=("sigma_t",))
     b = mf.query_batch(med, P, WO, WI, t(u[:, 0], 16), t(u[:, 1], 16), outputs=("sigma_t",))
     assert torch.equal(a["sigma_t"], b["sigma_t"])
+
+
+def test_query_batch_host_pipelined(cuda):
+    """query_batch_host (host tensors in and out, chunks pipelined over
+    three streams) returns exactly the device query's outputs."""
+    torch = cuda
+    p, wo, wi, u = configs.config1_inputs(n=(1 << 16) + 123)
+    med = configs.config1_medium()
+    host = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    got = mf.query_batch_host(med, host(p.T), host(wo.T), host(wi.T), host(u[:, 0]),
+                              host(u[:, 1]), chunk=1 << 14)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    ref = mf.query_batch(med, dev(p.T), dev(wo.T), dev(wi.T), dev(u[:, 0]), dev(u[:, 1]))
+    for k, v in ref.items():
+        assert torch.equal(got[k], v.cpu()), k
