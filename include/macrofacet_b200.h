@@ -368,6 +368,8 @@ typedef struct mf_gp_grid {
   double spacing;
   double origin;        /* lower corner on every axis (-extent / 2) */
   int32_t planar;       /* 1: mean mu(p) = p_z; 0: zero mean */
+  const double* d_bound; /* per realisation max |stationary value| (planar mean: lets a march
+                            stop once no later point can change sign), or NULL */
 } mf_gp_grid;
 
 /* RandomStream(seed, stream).normal(n) (rng.py:87-97) of the streams whose

@@ -97,7 +97,8 @@ _vp = ctypes.c_void_p
 
 class MfGpGrid(ctypes.Structure):
     _fields_ = [("d_grid", ctypes.c_void_p), ("n", ctypes.c_int32), ("spacing", ctypes.c_double),
-                ("origin", ctypes.c_double), ("planar", ctypes.c_int32)]
+                ("origin", ctypes.c_double), ("planar", ctypes.c_int32),
+                ("d_bound", ctypes.c_void_p)]
 
 
 class MfQueryIn(ctypes.Structure):

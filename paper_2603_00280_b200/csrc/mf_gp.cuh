@@ -38,6 +38,7 @@ struct Grid {
   double h;           // spacing
   double origin;      // -extent / 2 on every axis
   int planar;         // mean mu = z (else zero)
+  const double* bound;  // per realisation max |stationary value|, or null
 };
 
 // SplitMix64 output of the Weyl sequence from base (rng.py raw_u64)
@@ -107,8 +108,15 @@ __device__ __forceinline__ Hit first_hit(const Grid& G, int r, double ox, double
   bool found = false;
   int evals = 1;
   const double t_end = da(t_max, step);
+  // planar mean: f = z + g with |g| <= B, so once the ray's height is past
+  // +-B on the side it is heading to and the last value has that sign, no
+  // later march point can change sign -- stop (the same "no hit" the full
+  // march reaches, bit for bit)
+  const double B = (G.planar && G.bound) ? G.bound[r] : INFINITY;
   for (double t = step; t <= t_end; t = da(t, step)) {
-    double f = field_at(G, r, da(ox, dm(t, dx)), da(oy, dm(t, dy)), da(oz, dm(t, dz)));
+    double zt = da(oz, dm(t, dz));
+    if ((dz >= 0.0 && zt > B && f_prev > 0.0) || (dz <= 0.0 && zt < -B && f_prev < 0.0)) break;
+    double f = field_at(G, r, da(ox, dm(t, dx)), da(oy, dm(t, dy)), zt);
     ++evals;
     if (signbit(f) != signbit(f_prev)) {
       lo = t_prev;

@@ -2612,6 +2612,7 @@ static mf::gp::Grid gp_grid(const mf_gp_grid& g) {
   G.h = g.spacing;
   G.origin = g.origin;
   G.planar = g.planar;
+  G.bound = g.d_bound;
   return G;
 }
 

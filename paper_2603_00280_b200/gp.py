@@ -124,6 +124,7 @@ class GpBatch:
     spec: GridSpec
     kernel: KernelParams
     mean: str
+    bound: object = None     # (B,) max |value| per realisation (march early exit)
 
     def c_grid(self):
         g = _lib.MfGpGrid()
@@ -132,6 +133,7 @@ class GpBatch:
         g.spacing = self.spec.spacing
         g.origin = self.spec.origin
         g.planar = 1 if self.mean == "planar" else 0
+        g.d_bound = self.bound.data_ptr() if self.bound is not None else None
         return g
 
 
@@ -150,7 +152,8 @@ def _realize(kernel, mean, spec, bases, counter0=0):
                                ctypes.c_void_p(white.data_ptr()), _lib.stream_handle(torch, dev)))
     spec_f = torch.fft.fftn(white, dim=(1, 2, 3)) * _filter_sqrt(kernel, spec, torch, dev)
     grid = torch.fft.ifftn(spec_f, dim=(1, 2, 3)).real.contiguous()
-    return GpBatch(grid=grid, spec=spec, kernel=kernel, mean=mean)
+    bound = grid.abs().amax(dim=(1, 2, 3)).contiguous()
+    return GpBatch(grid=grid, spec=spec, kernel=kernel, mean=mean, bound=bound)
 
 
 def _noise_draws(n_cells):

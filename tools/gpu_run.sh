@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --workload config1 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_config1.json 2> gpurun_out/bench_config1.err
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -k "query" > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -k "gp" > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log
+timeout 900 python bench.py --workload gp --steps 3 --warmup 1 > gpurun_out/bench_gp.json 2> gpurun_out/bench_gp.err
