@@ -28,6 +28,6 @@ from .ndf import KernelParams, NdfKind, RoughnessTriple, roughness_from_kernel
 from .render import PathKeys, render, render_device, render_sharded, trace_path, trace_paths
 from .rng import BatchRng, RandomStream, derive_bases, stream_base
 from .scene import (Camera, DirectionalLight, Environment, PointLight, ShellPrimitive,
-                    ShellScene)
+                    ShellScene, shell_intersect)
 from .sdf import Box, Plane, Sphere
 from .transport import EventKind, MediumEvent, sample_collision, transmittance_estimate, walk

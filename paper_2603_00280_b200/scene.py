@@ -205,3 +205,72 @@ def to_c_scene(scene) -> _lib.MfScene:
         c.point_pos[:] = _vec3(point.position, "point light position")
         c.point_intensity[:] = _vec3(point.intensity, "point light intensity")
     return c
+
+
+def shell_intersect(origin, direction, scene, t_max=1e6):
+    """Ordered disjoint ray intervals inside the primitives' 3-sigma shells
+    and whether the ray reaches below a shell (scene.py:132-200): sphere
+    tracing of min_k |f_k| - w_k with the 1-Lipschitz step, every boundary
+    bisected 60 times, the march ended once the ray is outside every shell
+    and receding from every (convex-exterior) primitive.  Host float64
+    geometry query on the callers' SDF objects; the device walkers use
+    their own exact level-set distances.  Returns ([(t_in, t_out, k)],
+    deep)."""
+    from .errors import NumericFailureError
+
+    o = np.asarray(origin, dtype=np.float64)
+    d = np.asarray(direction, dtype=np.float64)
+    prims = scene.primitives
+    if not prims:
+        return [], False
+    w = np.array([pr.medium.shell_half_width for pr in prims])
+
+    def fields(t):
+        p = o + t * d
+        return np.array([float(pr.sdf.sdf(p)) for pr in prims])
+
+    def gap(t):                         # signed distance to the nearest shell, its index
+        f = fields(t)
+        g = np.abs(f) - w
+        k = int(np.argmin(g))
+        return f, float(g[k]), k
+
+    def crossing(lo, hi, k):            # the boundary of shell k on [lo, hi]
+        pr, wk = prims[k], w[k]
+        g = lambda t: abs(float(pr.sdf.sdf(o + t * d))) - wk  # noqa: E731
+        out_lo = g(lo) > 0.0
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            if (g(mid) > 0.0) == out_lo:
+                lo = mid
+            else:
+                hi = mid
+        return 0.5 * (lo + hi)
+
+    eps = 1e-7 * max(1.0, float(np.linalg.norm(o)))
+    f, g, k = gap(0.0)
+    deep = bool(np.any(f < -w))
+    cur = k if g <= 0.0 else None        # the shell the ray is in, if any
+    spans = [[0.0, None, cur]] if cur is not None else []
+    t_prev, t = 0.0, max(abs(g), eps)
+    for _ in range(1_000_000):
+        if t >= t_max:
+            break
+        f, g, k = gap(t)
+        deep = deep or bool(np.any(f < -w))
+        if cur is None and g <= 0.0:
+            spans.append([crossing(t_prev, t, k), None, k])
+            cur = k
+        elif cur is not None and g > 0.0:
+            spans[-1][1] = crossing(t_prev, t, cur)
+            cur = None
+        if cur is None and g > 0.0:
+            p = o + t * d
+            if all(float(np.dot(pr.sdf.gradient(p), d)) >= 0.0 for pr in prims):
+                break                    # receding from every convex exterior
+        t_prev, t = t, t + max(abs(g), eps)
+    else:
+        raise NumericFailureError("shell_intersect exceeded its iteration cap")
+    if spans and spans[-1][1] is None:
+        spans[-1][1] = min(t, t_max)
+    return [tuple(s) for s in spans], deep

@@ -25,6 +25,16 @@ class Plane:
 
     z0: float = 0.0
 
+    # host evaluation of the field for callers (sdf.py:25-33); the walkers
+    # evaluate it on the device
+    def sdf(self, p):
+        return np.asarray(p, dtype=np.float64)[..., 2] - self.z0
+
+    def gradient(self, p):
+        g = np.zeros(np.shape(p))
+        g[..., 2] = 1.0
+        return g
+
 
 @dataclass(frozen=True)
 class Sphere:
@@ -35,6 +45,16 @@ class Sphere:
         if not self.radius > 0:
             raise ParameterDomainError(f"sphere radius must be > 0, got {self.radius}")
         object.__setattr__(self, "center", tuple(float(c) for c in self.center))
+
+    def sdf(self, p):
+        """|p - c| - r (sdf.py:45-47)."""
+        return np.linalg.norm(np.asarray(p, dtype=np.float64) - self.center, axis=-1) - self.radius
+
+    def gradient(self, p):
+        """Outward unit radial direction (the +z axis at the centre)."""
+        d = np.asarray(p, dtype=np.float64) - self.center
+        r = np.linalg.norm(d, axis=-1, keepdims=True)
+        return np.where(r > 0.0, d / np.where(r > 0.0, r, 1.0), np.array([0.0, 0.0, 1.0]))
 
 
 @dataclass(frozen=True)
@@ -49,6 +69,23 @@ class Box:
             raise ParameterDomainError("box half extents must be > 0")
         object.__setattr__(self, "center", tuple(float(c) for c in self.center))
         object.__setattr__(self, "half_extents", tuple(float(h) for h in self.half_extents))
+
+    def sdf(self, p):
+        """Exact signed distance (sdf.py:66-72): the length of the positive
+        part of q = |p - c| - h plus the (non-positive) largest component."""
+        q = np.abs(np.asarray(p, dtype=np.float64) - self.center) - np.asarray(self.half_extents)
+        return np.linalg.norm(np.maximum(q, 0.0), axis=-1) + np.minimum(q.max(axis=-1), 0.0)
+
+    def gradient(self, p):
+        """Gradient a.e. (sdf.py:74-84): outside, along the positive part of
+        q with the octant's signs; inside, the normal of the nearest face."""
+        d = np.asarray(p, dtype=np.float64) - self.center
+        q = np.abs(d) - np.asarray(self.half_extents)
+        sgn = np.where(d >= 0.0, 1.0, -1.0)
+        pos = np.maximum(q, 0.0)
+        n = np.linalg.norm(pos, axis=-1, keepdims=True)
+        inside = np.eye(3)[np.argmax(q, axis=-1)] * sgn
+        return np.where(n > 0.0, sgn * pos / np.where(n > 0.0, n, 1.0), inside)
 
 
 def shape_name(sdf) -> str:
