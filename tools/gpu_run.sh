@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short -k "gp" > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log
-timeout 900 python bench.py --workload gp --steps 3 --warmup 1 > gpurun_out/bench_gp.json 2> gpurun_out/bench_gp.err
+timeout 1500 python tools/time_variants.py variants/nopf.so variants/pf.so variants/nopf.so variants/pf.so > gpurun_out/variants.txt 2>&1
