@@ -3,15 +3,15 @@
 // realisations and first zero crossings of their trilinear interpolant, in
 // float64 like the reference.
 //
-//   gp_noise_kernel      the white noise of RandomStream.normal (rng.py:46-97:
+//   gp::noise_kernel     the white noise of RandomStream.normal (rng.py:46-97:
 //                        SplitMix64 over a Weyl sequence, Box-Muller over
 //                        the two halves of the counter range), bit for bit
-//   gp_eval_kernel       field_at / gradient_at (gp.py:80-131)
-//   gp_first_hit_kernel  first_hit (gp.py:148-197): the fixed-step march
+//   gp::eval_kernel      field_at / gradient_at (gp.py:80-131)
+//   gp::first_hit_kernel first_hit (gp.py:148-197): the fixed-step march
 //                        (min(l)/8) to the first sign change, 30 bisections,
 //                        the normalised central-difference gradient
-//   gp_escape_kernel,    the bounce loop of ensemble_radiance (gp.py:340-398):
-//   gp_reflect_kernel    escape test + per-realisation march length, then
+//   gp::escape_kernel,   the bounce loop of ensemble_radiance (gp.py:340-398):
+//   gp::reflect_kernel   escape test + per-realisation march length, then
 //                        the march and the specular bounce
 //
 // One thread per ray; rays carry the index of their realisation, so a launch

@@ -12,7 +12,16 @@
 //   finalize_kernel   per-pixel 64-bit fixed-point sums (accumulated by the
 //                     render kernels themselves, accumulate_fx) -> the
 //                     caller's fp32 buffer (render.py:150,165-166)
+//   pool_kernel       shared-memory path pool for single-plane scenes (configs
+//                     2, 4): R / B / H visits over per-warp slot rings, every
+//                     visit at full warp width
+//   curved_pool_kernel the same pool for one sphere or a grid field (configs 3, 5)
 //   ratio_kernel      ratio-tracking transmittance samples (transport.py:300-313)
+//   walk_kernel       walk / sample_collision of caller rays (transport.py:144-416)
+//   curve_kernel      closed-form curves of one medium (cli.py:132-175)
+//   slope_table_kernel, grid_majorant_kernel, grid_skip_kernel, env_max_kernel
+//                     per-device / per-grid / per-render set-up
+//   gp::*             the GP-realisation oracle (mf_gp.cuh)
 #include <cuda_runtime.h>
 
 #include <algorithm>

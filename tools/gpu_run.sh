@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-timeout 1500 python tools/time_variants.py variants/nopf.so variants/pf.so variants/nopf.so variants/pf.so > gpurun_out/variants.txt 2>&1
+for r in 1 2; do
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=line > gpurun_out/gpu_tests_rep$r.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/gpu_tests_rep$r.log
+done
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
