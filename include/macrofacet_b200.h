@@ -331,6 +331,20 @@ int mf_reduce(void* comm, float* d_buf, size_t count, int root, int mode, void* 
 /* Issue-rate peaks of this device measured by microbenchmark kernels
  * (independent FFMA chains / MUFU.EX2 chains, all SMs), in 1e9 lane
  * instructions per second: the FP32 / SFU roofline denominators. */
+/* Camera rays of ensemble_radiance's rounds (scene.py:30-51 with each
+ * round's jitter uniforms, gp.py:352-357) into SoA [3][rounds h w] d_o / d_d:
+ * pos / fwd / right / up / half_w / half_h are the camera basis computed as
+ * Camera.rays does; d_bases[r] the SplitMix64 base of round r's stream.
+ * mf_gp_round_sum: d_img (h w 3, row-major) = the rounds' radiance (SoA
+ * [3][rounds h w]) summed in round order, continuing d_img's values when
+ * accumulate != 0. */
+int mf_gp_camera_rays(const double pos[3], const double fwd[3], const double right[3],
+                      const double up[3], double half_w, double half_h, int32_t width,
+                      int32_t height, const uint64_t* d_bases, int32_t rounds, double* d_o,
+                      double* d_d, void* stream);
+int mf_gp_round_sum(const double* d_rad, int32_t width, int32_t height, int32_t rounds,
+                    int32_t accumulate, double* d_img, void* stream);
+
 /* float64 special functions on the device (the reference's core.py:29-98
  * erf / erfc / the Gaussian pieces): which 0 erf, 1 erfc, 2 exp(-x) */
 int mf_special_f64(int which, const double* d_x, int64_t n, double* d_out, void* stream);

@@ -136,6 +136,11 @@ SIGNATURES = {
                                            ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "mf_measure_peak_fp64": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), _vp]),
     "mf_special_f64": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int64, _vp, _vp]),
+    "mf_gp_camera_rays": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, _vp,
+                                         _vp, _vp]),
+    "mf_gp_round_sum": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, _vp, _vp]),
     "mf_gdf_radial": (ctypes.c_int, [ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_int32, _vp, _vp,
                                      ctypes.POINTER(ctypes.c_double), _vp]),

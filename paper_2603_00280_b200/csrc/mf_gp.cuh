@@ -307,6 +307,52 @@ __global__ void reflect_kernel(const __grid_constant__ Grid G, const __grid_cons
   }
 }
 
+// Camera rays of ensemble_radiance's rounds (scene.py:30-51 on the round's
+// jitter uniforms, gp.py:352-357), float64 in numpy's operation order:
+// round r, pixel (py, px): jitter x = uniform(bases[r], py w + px), jitter y
+// = uniform(bases[r], h w + py w + px); origins at the camera
+struct CamRays {
+  double pos[3], fwd[3], right[3], up[3];
+  double half_w, half_h;
+  int w, h;
+};
+
+__global__ void camera_kernel(const __grid_constant__ CamRays c, const uint64_t* bases, int rounds,
+                              double* o, double* d) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t hw = (int64_t)c.w * c.h, n = hw * rounds;
+  if (i >= n) return;
+  int r = (int)(i / hw);
+  int64_t q = i - (int64_t)r * hw;
+  int py = (int)(q / c.w), px = (int)(q - (int64_t)py * c.w);
+  double jx = uniform_from(bases[r], (uint64_t)q), jy = uniform_from(bases[r], (uint64_t)(hw + q));
+  double nx = ds(dm(dd(da((double)px, jx), (double)c.w), 2.0), 1.0);
+  double ny = ds(1.0, dm(dd(da((double)py, jy), (double)c.h), 2.0));
+  double ax = dm(nx, c.half_w), ay = dm(ny, c.half_h);
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = da(da(c.fwd[k], dm(ax, c.right[k])), dm(ay, c.up[k]));
+  double nrm = __dsqrt_rn(da(da(dm(v[0], v[0]), dm(v[1], v[1])), dm(v[2], v[2])));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    d[k * n + i] = dd(v[k], nrm);
+    o[k * n + i] = c.pos[k];
+  }
+}
+
+// the ensemble image: per pixel and channel the rounds' radiance summed in
+// round order (the reference's img += rad per round), divided by the count
+__global__ void round_sum_kernel(const double* rad, int64_t hw, int rounds, int add, double* img) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hw * 3) return;
+  int c = (int)(i / hw);
+  int64_t q = i - (int64_t)c * hw;
+  const int64_t n = hw * rounds;
+  double s = add ? img[q * 3 + c] : 0.0;   // continue an earlier batch's sum
+  for (int r = 0; r < rounds; ++r) s = da(s, rad[c * n + (int64_t)r * hw + q]);
+  img[q * 3 + c] = s;
+}
+
 // DFMA issue-rate microbenchmark (the FP64 roofline of these kernels)
 __global__ void __launch_bounds__(256) peak_dfma_kernel(double* out, int iters, double a,
                                                         double b) {

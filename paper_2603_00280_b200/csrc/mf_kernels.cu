@@ -2045,6 +2045,45 @@ int mf_grid_majorant(const mf_grid_field* grid, float* d_majorant_out, void* str
   return MF_OK;
 }
 
+int mf_gp_camera_rays(const double pos[3], const double fwd[3], const double right[3],
+                      const double up[3], double half_w, double half_h, int32_t width,
+                      int32_t height, const uint64_t* d_bases, int32_t rounds, double* d_o,
+                      double* d_d, void* stream) {
+  if (!pos || !fwd || !right || !up || !d_bases || !d_o || !d_d || width < 1 || height < 1 ||
+      rounds < 0)
+    return fail(MF_ERR_PARAM, "bad gp_camera_rays arguments");
+  mf::gp::CamRays c;
+  for (int k = 0; k < 3; ++k) {
+    c.pos[k] = pos[k];
+    c.fwd[k] = fwd[k];
+    c.right[k] = right[k];
+    c.up[k] = up[k];
+  }
+  c.half_w = half_w;
+  c.half_h = half_h;
+  c.w = width;
+  c.h = height;
+  int64_t n = (int64_t)width * height * rounds;
+  if (!n) return MF_OK;
+  mf::gp::camera_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      c, d_bases, rounds, d_o, d_d);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
+int mf_gp_round_sum(const double* d_rad, int32_t width, int32_t height, int32_t rounds,
+                    int32_t accumulate, double* d_img, void* stream) {
+  if (!d_rad || !d_img || width < 1 || height < 1 || rounds < 1)
+    return fail(MF_ERR_PARAM, "bad gp_round_sum arguments");
+  int64_t hw = (int64_t)width * height;
+  mf::gp::round_sum_kernel<<<(unsigned)((hw * 3 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      d_rad, hw, rounds, accumulate ? 1 : 0, d_img);
+  g_launches++;
+  MF_CUDA(cudaGetLastError());
+  return MF_OK;
+}
+
 int mf_special_f64(int which, const double* d_x, int64_t n, double* d_out, void* stream) {
   if (which < 0 || which > 2) return fail(MF_ERR_PARAM, "unknown special function");
   if (n < 0 || (n > 0 && (!d_x || !d_out))) return fail(MF_ERR_PARAM, "bad special_f64 arguments");

@@ -479,36 +479,44 @@ def ensemble_radiance(kernel, camera, spp, m_realizations, rng, env_radiance=1.0
     torch, dev = _dev()
     lib = _lib.load()
     n_rounds = max(int(spp), 1)
-    img = np.zeros((h, w, 3))
-    rounds = np.arange(n_rounds)
     # round s: r = rng.derive(s); the realisation from r.derive(1); the
     # jitter from r's own first 2 h w uniforms
+    rounds = np.arange(n_rounds)
     r_bases = derive_bases(int(rng.seed), int(rng.stream), rounds)
     r_streams = _child_streams(int(rng.stream), rounds)
     real_bases = np.array([derive_bases(int(rng.seed), int(s), [1])[0] for s in r_streams],
                           dtype=np.uint64)
-    yy, xx = np.mgrid[0:h, 0:w]
+    # the camera basis exactly as Camera.rays computes it (scene.py:30-51)
+    pos = np.asarray(camera.position, dtype=np.float64)
+    fwd = np.asarray(camera.look_at, dtype=np.float64) - pos
+    fwd = fwd / np.linalg.norm(fwd, axis=-1, keepdims=True)
+    up = np.array([0.0, 0.0, 1.0])
+    if abs(fwd @ up) > 0.999:
+        up = np.array([0.0, 1.0, 0.0])
+    right = np.cross(fwd, up)
+    right = right / np.linalg.norm(right, axis=-1, keepdims=True)
+    true_up = np.cross(right, fwd)
+    half_h = float(np.tan(0.5 * np.deg2rad(camera.fov_deg)))
+    half_w = half_h * camera.width / camera.height
+    vec = lambda a: (ctypes.c_double * 3)(*[float(x) for x in a])  # noqa: E731
     eps = spec.spacing * 0.25
     step = min(kernel.lx, kernel.ly, kernel.lz) / 8.0
     eta_k = None
     if fresnel is not None:
-        eta_k = ((ctypes.c_double * 3)(*[float(v) for v in np.asarray(fresnel[0])]),
-                 (ctypes.c_double * 3)(*[float(v) for v in np.asarray(fresnel[1])]))
+        eta_k = (vec(np.asarray(fresnel[0])), vec(np.asarray(fresnel[1])))
+    s = _lib.stream_handle(torch, dev)
+    img = torch.zeros((h, w, 3), dtype=torch.float64, device=dev)
     for a, b in _batches(n_rounds):
         B = b - a
+        m = B * h * w
         batch = _realize(kernel, "planar", spec, real_bases[a:b])
-        jit = _uniforms(r_bases[a:b], 0, 2 * h * w)
-        o_all, d_all = [], []
-        for j in range(B):
-            o, d = camera_rays(camera, xx, yy, jit[j, :h * w].reshape(h, w),
-                               jit[j, h * w:].reshape(h, w))
-            o_all.append(o.reshape(-1, 3))
-            d_all.append(d.reshape(-1, 3))
-        o = np.concatenate(o_all)
-        d = np.concatenate(d_all)
-        m = o.shape[0]
-        O = torch.from_numpy(np.ascontiguousarray(o.T)).to(dev)
-        D = torch.from_numpy(np.ascontiguousarray(d.T)).to(dev)
+        rb = torch.from_numpy(np.ascontiguousarray(r_bases[a:b]).view(np.int64)).to(dev)
+        O = torch.empty((3, m), dtype=torch.float64, device=dev)
+        D = torch.empty((3, m), dtype=torch.float64, device=dev)
+        _lib.check(lib.mf_gp_camera_rays(vec(pos), vec(fwd), vec(right), vec(true_up), half_w,
+                                         half_h, w, h, ctypes.c_void_p(rb.data_ptr()), B,
+                                         ctypes.c_void_p(O.data_ptr()),
+                                         ctypes.c_void_p(D.data_ptr()), s))
         T = torch.ones((3, m), dtype=torch.float64, device=dev)
         L = torch.zeros((3, m), dtype=torch.float64, device=dev)
         R = torch.arange(B, dtype=torch.int32, device=dev).repeat_interleave(h * w)
@@ -520,15 +528,15 @@ def ensemble_radiance(kernel, camera, spp, m_realizations, rng, env_radiance=1.0
             ctypes.c_void_p(R.data_ptr()), m, B, float(kernel.sigma), float(env_radiance),
             float(eps), float(step), int(max_bounces),
             eta_k[0] if eta_k else None, eta_k[1] if eta_k else None,
-            ctypes.c_void_p(ev.data_ptr()) if ev is not None else None,
-            _lib.stream_handle(torch, dev)))
+            ctypes.c_void_p(ev.data_ptr()) if ev is not None else None, s))
         if work is not None:
             work["evals"] = work.get("evals", 0) + int(ev.item())
             work["paths"] = work.get("paths", 0) + m
-        rad = L.cpu().numpy().T.reshape(B, h, w, 3)
-        for j in range(B):       # the reference's round-by-round sum
-            img += rad[j]
-    return img / n_rounds
+        # the reference's round-by-round sum, continued across batches
+        _lib.check(lib.mf_gp_round_sum(ctypes.c_void_p(L.data_ptr()), w, h, B, 1 if a else 0,
+                                       ctypes.c_void_p(img.data_ptr()), s))
+    return img.cpu().numpy() / n_rounds
+
 
 
 def _child_streams(stream, indices):

@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-for r in 1 2; do
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=line > gpurun_out/gpu_tests_rep$r.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/gpu_tests_rep$r.log
-done
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+timeout 900 python -m pytest tests/test_gpu_gp.py -q -p no:cacheprovider --tb=short > gpurun_out/gpu_tests_sel.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_sel.log
+timeout 900 python bench.py --workload gp --steps 3 --warmup 1 > gpurun_out/bench_gp.json 2> gpurun_out/bench_gp.err
+timeout 600 python tools/gp_profile.py > gpurun_out/gp_profile.txt 2>&1
