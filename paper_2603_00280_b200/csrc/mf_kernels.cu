@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kQBlock) query_kernel(const __grid_constant__ 
       sig_safe = degenerate ? 1.0f : sig_o;
       V3 phase = phase_eval(m, wol, wil, sig_safe);
       float pdf = phase_pdf(m, wol, wil, sig_b);
-      uu = remap_branch_uniform(u1, m.mix);
+      uu = remap_branch_uniform(u1, m);
       bool guided = sig_b > 1e-12f;
       if (degenerate) {
         phase = v3(0.0f, 0.0f, 0.0f);

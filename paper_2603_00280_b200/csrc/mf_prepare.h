@@ -62,6 +62,15 @@ inline int prepare_medium(const mf_medium& in, MediumK* out, std::string* err) {
   m.mix = (float)in.mix_ratio;
   m.inv_mix = in.mix_ratio > 0.0 ? (float)(1.0 / in.mix_ratio) : 0.0f;
   m.inv_1m_mix = in.mix_ratio < 1.0 ? (float)(1.0 / (1.0 - in.mix_ratio)) : 0.0f;
+  {
+    auto pow2 = [](double x) {   // x > 0 an exact power of two in float32
+      int e;
+      float f = (float)x;
+      return x > 0.0 && (double)f == x && std::frexp(f, &e) == 0.5f;
+    };
+    m.remap_exact = (pow2(in.mix_ratio) || in.mix_ratio == 0.0) &&
+                    (pow2(1.0 - in.mix_ratio) || in.mix_ratio == 1.0);
+  }
   m.inv_ax = (float)(1.0 / in.ax);
   m.inv_ay = (float)(1.0 / in.ay);
   const double pi = 3.14159265358979323846;

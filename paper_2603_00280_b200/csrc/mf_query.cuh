@@ -49,16 +49,19 @@ MF_HD float div_rn(float a, float b) {
 #endif
 }
 
-// u1' of the two-uniform convention, correctly rounded so the host test can
-// reproduce it bit-for-bit in numpy float32
-MF_HD float remap_branch_uniform(float u1, float mix) {
-  return u1 < mix ? div_rn(u1, mix) : div_rn(u1 - mix, 1.0f - mix);
-}
-
-// the same remap on the render path, by the reciprocals prepared on the host
-// (identical to remap_branch_uniform when R is a power of two, e.g. R = 1/2)
+// the remap on the render path, by the reciprocals prepared on the host
+// (identical to the correctly rounded quotients when R and 1 - R are powers
+// of two, e.g. R = 1/2)
 MF_HD float remap_branch_uniform_render(float u1, const MediumK& m) {
   return u1 < m.mix ? u1 * m.inv_mix : (u1 - m.mix) * m.inv_1m_mix;
+}
+
+// u1' of the two-uniform convention, correctly rounded so the host test can
+// reproduce it bit-for-bit in numpy float32: the reciprocal products when
+// they are exact (m.remap_exact), else IEEE divisions
+MF_HD float remap_branch_uniform(float u1, const MediumK& m) {
+  if (m.remap_exact) return remap_branch_uniform_render(u1, m);
+  return u1 < m.mix ? div_rn(u1, m.mix) : div_rn(u1 - m.mix, 1.0f - m.mix);
 }
 
 struct QueryResult {
@@ -103,7 +106,7 @@ MF_HD QueryResult query_local(const MediumK& m, float f, const Frame& fr, V3 wo,
   float sig_safe = degenerate ? 1.0f : sig_o;
   q.phase = phase_eval(m, wol, wil, sig_safe);
   q.pdf = phase_pdf(m, wol, wil, sig_b);
-  float uu = remap_branch_uniform(u1, m.mix);
+  float uu = remap_branch_uniform(u1, m);
   PhaseSample s = phase_sample<true>(m, wol, sig_safe, sig_b, u1, uu, u2, mask);
   q.ws = to_world(fr, s.wi);
   q.pdf_s = s.pdf;
