@@ -184,41 +184,50 @@ MF_HD bool grid_box(const GridDev& g, V3 o, V3 d, float* t0, float* t1) {
 // the next tentative collision (or the end of the walk), tentative()
 // evaluates the extinction there and takes the tracking decision.  The
 // per-lane arithmetic and random-number consumption are those of one
-// sequential loop, whichever driver runs the two halves.
-// Random draws: blocks (segment, call0 + k) of the path's Philox stream.
+// sequential loop, whichever driver runs the two halves, and the walk can
+// be parked between any two calls: (t, tau, weight, cell, steps) is its
+// whole state (park() / resume()); everything else is a function of the
+// ray.  The wall distances are therefore computed from the cell index
+// (c * wa + wb per axis), never accumulated.
+// Random draws: block (segment, call0) of the path's Philox stream gives the
+// first optical depth; block (segment, call0 + k) serves the k-th tentative
+// collision (x: acceptance / roulette uniform, y: the next optical depth).
+struct GridPark {
+  float t, tau, weight;
+  uint32_t cell;   // cx | cy << 10 | cz << 20 (n_maj <= 1024)
+  int steps;
+};
+
 template <typename RngBlock>
 struct GridWalker {
   RngBlock rng_block;
   GridWalk w;
   V3 pos, dir;
   float t, t1, tau, lo_mult, rr_min;
-  float tx, ty, tz, dtx, dty, dtz, idx, idy, idz, mu;
-  int cx, cy, cz, sx, sy, sz, iter;
+  float tx, ty, tz, wax, way, waz, wbx, wby, wbz, dt_min, mu;
+  int cx, cy, cz, sx, sy, sz;
   bool ratio;
-  U4 bits;
-  int avail;
-  uint32_t call;
+  uint32_t call0;
 
   MF_HDM GridWalker(RngBlock rb) : rng_block(rb) {}
 
-  MF_HDM float draw() {
-    if (avail == 0) {
-      bits = rng_block(call++);
-      avail = 4;
+  // wall distance of cell c on one axis is c * wa + wb (INFINITY for a ray
+  // parallel to the walls)
+  MF_HDM static void wall_coef(int s, float bmin, float h, float o, float d, float* wa, float* wb) {
+    if (!(fabsf(d) > 1e-30f)) {
+      *wa = 0.0f;
+      *wb = INFINITY;
+    } else {
+      float id = 1.0f / d;
+      *wa = h * id;
+      *wb = (bmin + (s > 0 ? h : 0.0f) - o) * id;
     }
-    float u = u01(bits.x);
-    bits.x = bits.y;
-    bits.y = bits.z;
-    bits.z = bits.w;
-    --avail;
-    return u;
   }
 
-  // parametric distance to the next cell wall on one axis
-  MF_HDM static float wall(int c, int s, float bmin, float h, float o, float id) {
-    float x = bmin + h * (float)(c + (s > 0 ? 1 : 0));
-    float tw = (x - o) * id;
-    return isfinite(tw) ? tw : INFINITY;
+  MF_HDM void walls() {
+    tx = fmaf((float)cx, wax, wbx);
+    ty = fmaf((float)cy, way, wby);
+    tz = fmaf((float)cz, waz, wbz);
   }
 
   MF_HDM void locate(const GridDev& g) {
@@ -227,14 +236,12 @@ struct GridWalker {
     cx = clampi((int)q.x, 0, n - 1);
     cy = clampi((int)q.y, 0, n - 1);
     cz = clampi((int)q.z, 0, n - 1);
-    tx = wall(cx, sx, g.bmin.x, g.h_maj.x, pos.x, idx);
-    ty = wall(cy, sy, g.bmin.y, g.h_maj.y, pos.y, idy);
-    tz = wall(cz, sz, g.bmin.z, g.h_maj.z, pos.z, idz);
+    walls();
   }
 
-  // false: the ray misses the grid (escaped at once)
-  MF_HDM bool begin(const GridDev& g, uint32_t call0, V3 p0, V3 d, bool ratio_walk, float t_max,
-                   float rr) {
+  // the ray's constants; false: the ray misses the grid.  t0 = entry distance
+  MF_HDM bool setup(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                   float rr, float* t0) {
     w.outcome = 0;
     w.pos = p0;
     w.weight = 1.0f;
@@ -245,32 +252,56 @@ struct GridWalker {
     ratio = ratio_walk;
     rr_min = rr;
     lo_mult = ratio ? -3.0f : -6.0f;
-    avail = 0;
-    call = call0;
-    bits = U4{0, 0, 0, 0};
-    iter = 0;
-    float t0;
-    if (!grid_box(g, pos, dir, &t0, &t1)) return false;
+    call0 = call0_;
+    if (!grid_box(g, pos, dir, t0, &t1)) return false;
     t1 = fminf(t1, t_max);
-    t = t0;
     sx = dir.x > 0.0f ? 1 : -1;
     sy = dir.y > 0.0f ? 1 : -1;
     sz = dir.z > 0.0f ? 1 : -1;
-    idx = 1.0f / dir.x;
-    idy = 1.0f / dir.y;
-    idz = 1.0f / dir.z;
+    wall_coef(sx, g.bmin.x, g.h_maj.x, pos.x, dir.x, &wax, &wbx);
+    wall_coef(sy, g.bmin.y, g.h_maj.y, pos.y, dir.y, &way, &wby);
+    wall_coef(sz, g.bmin.z, g.h_maj.z, pos.z, dir.z, &waz, &wbz);
+    // parametric length of one cell on the axis the ray crosses fastest
+    dt_min = fminf(fminf(wax != 0.0f ? fabsf(wax) : INFINITY, way != 0.0f ? fabsf(way) : INFINITY),
+                   waz != 0.0f ? fabsf(waz) : INFINITY);
+    return true;
+  }
+
+  // false: the ray misses the grid (escaped at once)
+  MF_HDM bool begin(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                   float rr) {
+    float t0;
+    if (!setup(g, call0_, p0, d, ratio_walk, t_max, rr, &t0)) return false;
+    t = t0;
     locate(g);
-    dtx = isfinite(idx) ? fabsf(g.h_maj.x * idx) : INFINITY;
-    dty = isfinite(idy) ? fabsf(g.h_maj.y * idy) : INFINITY;
-    dtz = isfinite(idz) ? fabsf(g.h_maj.z * idz) : INFINITY;
     // optical depth left to the next tentative collision: sampled once per
     // tentative and used up cell by cell (tau -= mu dt), instead of a fresh
     // exponential (a uniform and a log) in every cell the ray crosses -- the
     // same process (the majorant is piecewise constant along the ray), a
     // fraction of the random numbers and logs
-    tau = -flog(draw());
+    tau = -flog(u01(rng_block(call0).x));
     MF_GSTAT(3);
     return true;
+  }
+
+  MF_HDM GridPark park() const {
+    return GridPark{t, tau, w.weight, (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20),
+                    w.steps};
+  }
+
+  // continue a parked walk of the same ray (same arguments as begin())
+  MF_HDM void resume(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                    float rr, const GridPark& k) {
+    float t0;
+    setup(g, call0_, p0, d, ratio_walk, t_max, rr, &t0);
+    t = k.t;
+    tau = k.tau;
+    w.weight = k.weight;
+    w.steps = k.steps;
+    cx = (int)(k.cell & 1023u);
+    cy = (int)((k.cell >> 10) & 1023u);
+    cz = (int)(k.cell >> 20);
+    walls();
   }
 
   MF_HDM void end_at(float te) { w.pos = fma3(dir, te, pos); }
@@ -279,16 +310,6 @@ struct GridWalker {
   // lies in the current cell (t is advanced to it; call tentative()), 2 when
   // the walk has ended (w is final), 0 otherwise.
   MF_HDM int dda(const GridDev& g) {
-    if (iter >= kGridIterCap) {
-      // iteration cap (transport.py:297 raises): a distinct result, counted
-      // by the callers as capped, never taken for an escape
-      end_at(t);
-      w.outcome = 1;
-      w.weight = 0.0f;
-      w.steps = -1;
-      return 2;
-    }
-    ++iter;
     MF_GSTAT(0);
     int n = g.n_maj;
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
@@ -309,7 +330,7 @@ struct GridWalker {
     }
     if (mu <= -2.0f) {
       // empty space: jump (D - 1) cells in every axis, then restart the DDA
-      float tj = t + (-mu - 1.0f) * fminf(fminf(dtx, dty), dtz);
+      float tj = t + (-mu - 1.0f) * dt_min;
       if (tj >= t1) {
         end_at(t1);
         return 2;
@@ -322,21 +343,17 @@ struct GridWalker {
       }
     }
     t = t_exit;
-    bool out;
     if (tx <= ty && tx <= tz) {
       cx += sx;
-      tx += dtx;
-      out = cx < 0 || cx >= n;
+      tx = fmaf((float)cx, wax, wbx);
     } else if (ty <= tz) {
       cy += sy;
-      ty += dty;
-      out = cy < 0 || cy >= n;
+      ty = fmaf((float)cy, way, wby);
     } else {
       cz += sz;
-      tz += dtz;
-      out = cz < 0 || cz >= n;
+      tz = fmaf((float)cz, waz, wbz);
     }
-    if (out) {
+    if ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n || (unsigned)cz >= (unsigned)n) {
       end_at(t);
       return 2;
     }
@@ -345,18 +362,27 @@ struct GridWalker {
 
   // The tentative collision at t (majorant mu): true when the walk ends.
   MF_HDM bool tentative(const GridDev& g, const MediumK& base) {
+    V3 p = fma3(dir, t, pos);
+    if (w.steps >= kGridIterCap) {
+      // iteration cap (transport.py:297 raises): a distinct result, counted
+      // by the callers as capped, never taken for an escape
+      w.pos = p;
+      w.outcome = 1;
+      w.weight = 0.0f;
+      w.steps = -1;
+      return true;
+    }
     w.steps++;
     MF_GSTAT(1);
-    V3 p = fma3(dir, t, pos);
     float f, sg;
     float st = grid_extinction(g, base, p, dir, lo_mult, &f, &sg);
+    U4 b = rng_block(call0 + (uint32_t)w.steps);
     if (st > mu * 1.00001f) w.violations++;
     if (ratio) {
       w.weight *= fmaxf(1.0f - st / mu, 0.0f);
       if (w.weight < rr_min && w.weight > 0.0f) {
         // Russian roulette on the weight (see walk() in mf_transport.cuh)
-        float ur = draw();
-        w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
+        w.weight = u01(b.x) * rr_min < w.weight ? rr_min : 0.0f;
       }
       if (!(w.weight > 0.0f)) {
         w.pos = p;
@@ -368,13 +394,13 @@ struct GridWalker {
         w.pos = p;
         return true;
       }
-      if (draw() * mu < st) {
+      if (u01(b.x) * mu < st) {
         w.outcome = 2;
         w.pos = p;
         return true;
       }
     }
-    tau = -flog(draw());
+    tau = -flog(u01(b.y));
     return false;
   }
 };

@@ -1364,6 +1364,382 @@ __global__ void __launch_bounds__(kBlock, kMode == 2 ? MF_GRID_POOL_MIN_BLOCKS
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grid-field path pool with pooled walks (config 5; sun / environment
+// lighting).  In curved_pool_kernel<2> a lane runs a whole flight or shadow
+// walk inside its visit: ncu showed the tentative collisions (two trilinear
+// fetches, Mills ratio, projected area: 2/3 of the issue slots) at 4 active
+// lanes and the DDA at 8, because the lanes of a warp reach their tentative
+// collisions at different cells and finish their walks at different
+// lengths.  Here a walk is a pool citizen of its own: a fourth ring (W)
+// holds slots whose path waits on a walk -- the shadow ray of its last
+// collision, then the flight of its next segment -- and a W visit advances
+// up to 32 of them together, alternating two re-converged phases: DDA
+// steps for the lanes that have no tentative collision pending, until most
+// have one; then the tentative collisions of all pending lanes at once.
+// When fewer than a fraction of the visit's walks remain, the unfinished
+// ones are parked (GridPark: t, tau, weight, cell, steps -- five words; the
+// walker recomputes everything else from the ray) and rejoin the ring, so
+// the next W visit starts full again.  B / H visits do the collision's
+// local medium / frame, sigma(wo), the NEE phase value, the normal and the
+// phase sample, depth cap / RR and the next segment's uniforms, and queue
+// the shadow walk; the walk's end adds contribution x transmittance and
+// queues the flight.  Per path the arithmetic and the random stream are
+// those of path_kernel<2> / curved_pool_kernel<2> (same GridWalker calls on
+// the same Philox blocks), so images agree to float rounding
+// (test_grid_walk_pool_matches_curved_pool).
+#ifndef MF_GRID_WALK_POOL_MIN_BLOCKS
+#define MF_GRID_WALK_POOL_MIN_BLOCKS 6
+#endif
+// leave the DDA phase when stepping lanes * kGwNum <= pending lanes * kGwDen
+#ifndef MF_GW_NUM
+#define MF_GW_NUM 1
+#endif
+#ifndef MF_GW_DEN
+#define MF_GW_DEN 1
+#endif
+// park the visit's unfinished walks when fewer than kGwExit / 8 of them remain
+#ifndef MF_GW_EXIT
+#define MF_GW_EXIT 4
+#endif
+constexpr int kStageWalk = 3;
+constexpr uint8_t kTagWalk = 3;
+constexpr uint32_t kGwShadow = 1u << 16, kGwDone = 1u << 17, kGwFresh = 1u << 18;
+
+template <bool kMono>
+struct GridPoolF {
+  static constexpr int kC = kMono ? 1 : 3;
+  static constexpr int kDir = 0, kPos = 3, kT = 6, kL = 6 + kC, kNee = 6 + 2 * kC,
+                       kUrr = 6 + 3 * kC, kUbr = kUrr + 1, kUs2 = kUrr + 2, kWt = kUrr + 3,
+                       kWtau = kUrr + 4, kWw = kUrr + 5, kCount = kUrr + 6;
+};
+template <bool kMono>
+struct GridPoolSlots {
+  float f[GridPoolF<kMono>::kCount][kPool];
+  uint32_t u[6][kPool];   // pid pixel sample bounce|flags cell steps
+  uint8_t ring[4][kRing];
+};
+
+template <bool kMono, int kSpec>
+__global__ void __launch_bounds__(kBlock, MF_GRID_WALK_POOL_MIN_BLOCKS) grid_pool_kernel(
+    const __grid_constant__ SceneDev sc, const __grid_constant__ PassDev ps) {
+  using F = GridPoolF<kMono>;
+  __shared__ GridPoolSlots<kMono> pools[kWarpsPerBlock];
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  GridPoolSlots<kMono>& P = pools[threadIdx.x >> 5];
+  Counters cn;
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) cn.v[i] = 0;
+  auto load3 = [&](int f0, int s) { return v3(P.f[f0][s], P.f[f0 + 1][s], P.f[f0 + 2][s]); };
+  auto store3 = [&](int f0, int s, V3 v) {
+    P.f[f0][s] = v.x; P.f[f0 + 1][s] = v.y; P.f[f0 + 2][s] = v.z;
+  };
+  auto loadc = [&](int f0, int s) {
+    if constexpr (kMono) {
+      float t = P.f[f0][s];
+      return v3(t, t, t);
+    } else {
+      return load3(f0, s);
+    }
+  };
+  auto storec = [&](int f0, int s, V3 v) {
+    P.f[f0][s] = v.x;
+    if constexpr (!kMono) { P.f[f0 + 1][s] = v.y; P.f[f0 + 2][s] = v.z; }
+  };
+  auto finish = [&](uint32_t pid, V3 L) {
+    if constexpr (kMono) {
+      accumulate_fx(ps, pid, L.x, cn);
+    } else {
+      accumulate_fx(ps, pid * 3u, L.x, cn);
+      accumulate_fx(ps, pid * 3u + 1u, L.y, cn);
+      accumulate_fx(ps, pid * 3u + 2u, L.z, cn);
+    }
+  };
+#pragma unroll
+  for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
+  __syncwarp();
+  unsigned head[4] = {0, 0, 0, 0}, tail[4] = {kPool, 0, 0, 0};
+  bool exhausted = false;
+  while (true) {
+    int ne = exhausted ? 0 : (int)(tail[0] - head[0]);
+    int nb = (int)(tail[1] - head[1]), nh = (int)(tail[2] - head[2]), nw = (int)(tail[3] - head[3]);
+    int stage;
+    if (nw >= 32) stage = kStageWalk;
+    else if (nb >= 32) stage = kStageBeck;
+    else if (nh >= 32) stage = kStageHemi;
+    else if (ne >= 32) stage = kStageRaygen;
+    else {
+      int best = nw;
+      stage = kStageWalk;
+      if (nb > best) { best = nb; stage = kStageBeck; }
+      if (nh > best) { best = nh; stage = kStageHemi; }
+      if (ne > best) { best = ne; stage = kStageRaygen; }
+      if (best == 0) break;
+    }
+    int cnt = stage == kStageWalk ? nw : (stage == kStageBeck ? nb : (stage == kStageHemi ? nh : ne));
+    unsigned hd = stage == kStageWalk ? head[3]
+                                      : (stage == kStageBeck ? head[1]
+                                                             : (stage == kStageHemi ? head[2] : head[0]));
+    int n = cnt < 32 ? cnt : 32;
+    int slot = lane < n ? (int)P.ring[stage][(hd + (unsigned)lane) & (kRing - 1)] : -1;
+    if (stage == kStageWalk) head[3] += (unsigned)n;
+    else if (stage == kStageBeck) head[1] += (unsigned)n;
+    else if (stage == kStageHemi) head[2] += (unsigned)n;
+    else head[0] += (unsigned)n;
+
+    uint8_t tag = kTagEmpty;
+    if (stage == kStageRaygen) {
+      unsigned need = __ballot_sync(full, slot >= 0);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(ps.counter, (unsigned)__popc(need));
+      base = __shfl_sync(full, base, 0);
+      if (base + (unsigned)__popc(need) >= ps.n_paths) exhausted = true;
+      uint32_t my = base + (uint32_t)lane;
+      PathState st;
+      if (slot >= 0 && my < ps.n_paths && start_path<false>(sc, ps, st, my)) {
+        cn.v[kStPaths]++;
+        cn.v[kStSegments]++;
+        store3(F::kDir, slot, st.dir);
+        store3(F::kPos, slot, st.pos);
+        storec(F::kT, slot, st.T);
+        storec(F::kL, slot, st.L);
+        P.f[F::kUrr][slot] = st.u_rr;
+        P.f[F::kUbr][slot] = st.u_br;
+        P.f[F::kUs2][slot] = st.u_s2;
+        P.u[0][slot] = st.pid;
+        P.u[1][slot] = st.rng.pixel;
+        P.u[2][slot] = st.rng.sample;
+        P.u[3][slot] = kGwFresh;   // bounce 0, flight
+        tag = kTagWalk;
+      }
+    } else if (stage == kStageWalk) {
+      // ---- W visit: advance up to 32 walks ----
+      uint32_t pix = 0, smp = 0, seg = 0, bfl = 0;
+      auto rb = [&](uint32_t call) { return philox_rk(U4{pix, smp, seg, call}, ps.rk); };
+      GridWalker<decltype(rb)> W(rb);
+      bool active = false, ended = false, pending = false, shadow = false;
+      if (slot >= 0) {
+        bfl = P.u[3][slot];
+        pix = P.u[1][slot];
+        smp = P.u[2][slot];
+        shadow = (bfl & kGwShadow) != 0;
+        uint32_t bounce = bfl & 0xFFFFu;
+        V3 o = load3(F::kPos, slot);
+        V3 d = shadow ? sc.sun_to : load3(F::kDir, slot);
+        // the shadow ray belongs to the segment that ended in the collision
+        seg = shadow ? bounce - 1u : bounce;
+        uint32_t call0 = shadow ? kCallShadow : 1u;
+        float rr = shadow ? kShadowRR : 0.0f;
+        active = true;
+        if (bfl & kGwFresh) {
+          if (!W.begin(sc.grid, call0, o, d, shadow, INFINITY, rr)) {
+            active = false;
+            ended = true;
+          }
+        } else {
+          GridPark pk{P.f[F::kWt][slot], P.f[F::kWtau][slot], P.f[F::kWw][slot], P.u[4][slot],
+                      (int)P.u[5][slot]};
+          W.resume(sc.grid, call0, o, d, shadow, INFINITY, rr, pk);
+        }
+      }
+      const int n0 = __popc(__ballot_sync(full, active));
+      while (true) {
+        // DDA phase: lanes without a pending tentative collision step on
+        while (true) {
+          if (active && !pending) {
+            int r = W.dda(sc.grid);
+            if (r == 1) {
+              pending = true;
+            } else if (r == 2) {
+              active = false;
+              ended = true;
+            }
+          }
+          int nstep = __popc(__ballot_sync(full, active && !pending));
+          int npend = __popc(__ballot_sync(full, pending));
+          if (nstep * MF_GW_NUM <= npend * MF_GW_DEN) break;
+        }
+        // tentative collisions of every pending lane
+        if (pending) {
+          if (W.tentative(sc.grid, sc.media[0])) {
+            active = false;
+            ended = true;
+          }
+          pending = false;
+        }
+        int nact = __popc(__ballot_sync(full, active));
+        if (nact * 8 < n0 * MF_GW_EXIT || nact == 0) break;
+      }
+      if (active) {
+        // park the unfinished walk
+        GridPark pk = W.park();
+        cn.v[kStViolations] += (uint32_t)W.w.violations;
+        P.f[F::kWt][slot] = pk.t;
+        P.f[F::kWtau][slot] = pk.tau;
+        P.f[F::kWw][slot] = pk.weight;
+        P.u[4][slot] = pk.cell;
+        P.u[5][slot] = (uint32_t)pk.steps;
+        P.u[3][slot] = bfl & ~kGwFresh;
+        tag = kTagWalk;
+      } else if (ended) {
+        const GridWalk& w = W.w;
+        cn.v[kStTrackSteps] += (uint32_t)max(w.steps, 0);
+        cn.v[kStViolations] += (uint32_t)w.violations;
+        if (shadow) {
+          if (w.steps < 0) cn.v[kStCapped]++;   // iteration cap: raised by the host
+          float tr = w.steps < 0 ? 0.0f : w.weight;
+          V3 c = loadc(F::kNee, slot), L = loadc(F::kL, slot);
+          L = add3(L, v3(c.x * tr, c.y * tr, c.z * tr));
+          if (bfl & kGwDone) {
+            finish(P.u[0][slot], L);
+          } else {
+            storec(F::kL, slot, L);
+            P.u[3][slot] = (bfl & 0xFFFFu) | kGwFresh;   // the next segment's flight
+            cn.v[kStSegments]++;
+            tag = kTagWalk;
+          }
+        } else {
+          int outcome = w.steps < 0 ? -1 : w.outcome;
+          if (outcome == kCollided) {
+            store3(F::kPos, slot, w.pos);
+            tag = P.f[F::kUbr][slot] < sc.media[0].mix ? kTagBeck : kTagHemi;
+          } else {
+            V3 L = loadc(F::kL, slot);
+            if (outcome == kEscaped) {
+              V3 T = loadc(F::kT, slot);
+              V3 e = env_radiance(sc, W.dir);   // render.py:54-57
+              L = add3(L, v3(T.x * e.x, T.y * e.y, T.z * e.z));
+              cn.v[kStEscaped]++;
+            } else if (outcome == kAbsorbed) {
+              cn.v[kStAbsorbed]++;
+            } else {
+              cn.v[kStCapped]++;
+            }
+            finish(P.u[0][slot], L);
+          }
+        }
+      }
+    } else if (slot >= 0) {
+      // ---- B / H visit: the collision's scatter stages up to the walks ----
+      PathState st;
+      st.dir = load3(F::kDir, slot);
+      st.pos = load3(F::kPos, slot);
+      st.T = loadc(F::kT, slot);
+      st.L = loadc(F::kL, slot);
+      st.u_rr = P.f[F::kUrr][slot];
+      st.u_br = P.f[F::kUbr][slot];
+      st.u_s2 = P.f[F::kUs2][slot];
+      uint32_t pid = P.u[0][slot], pix = P.u[1][slot], smp = P.u[2][slot];
+      st.bounce = (int)(P.u[3][slot] & 0xFFFFu);
+      CollisionLocal<2> loc(sc, st.pos);
+      const MediumK& m = loc.m;
+      const Frame& fr = loc.fr;
+      V3 wo = to_local(fr, st.dir);
+      float sig_o = proj_area<kSpec, true>(m, wo);
+      cn.v[kStScatters]++;
+      if (!(sig_o >= 1e-12f)) {
+        cn.v[kStDegenerate]++;
+        finish(pid, st.L);
+      } else {
+        // NEE towards the sun: the phase value now, the transmittance by the
+        // queued shadow walk
+        bool want_shadow = false;
+        V3 nee = v3(0.0f, 0.0f, 0.0f);
+        if (sc.has_sun) {
+          V3 wl = to_local(fr, sc.sun_to);
+          V3 ph = phase_eval<kSpec, true>(m, wo, wl, sig_o);
+          if (ph.x > 0.0f || ph.y > 0.0f || ph.z > 0.0f) {
+            cn.v[kStNee]++;
+            want_shadow = true;
+            nee = v3(st.T.x * ph.x * sc.sun_L.x, st.T.y * ph.y * sc.sun_L.y,
+                     st.T.z * ph.z * sc.sun_L.z);
+          }
+        }
+        V3 v = neg3(wo);
+        float uu = remap_branch_uniform_render(st.u_br, m);
+        float sig_b = (kSpec == kSpecBeckAlbedo || (kSpec == kSpecRuntime && m.kind == kBeckmann))
+                          ? sig_o : proj_area_erf<true>(wo, m.ax, m.ay, 0.0f);
+        V3 wm;
+        float vm;
+        if (stage == kStageBeck && sig_b > 1e-12f) {
+          int iters = 0;
+          wm = beckmann_visible_normal<kRenderSlopeGuard, true>(m, v, uu, st.u_s2, &iters);
+          vm = dot3(v, wm);
+          cn.v[kStSlopeIters] += (uint32_t)iters;
+        } else {
+          wm = hemisphere_about(v, uu, st.u_s2);
+          vm = uu;
+        }
+        PhaseSample smpl = phase_sample_tail<kSpec, true>(m, v, wm, vm, sig_o, sig_b,
+                                                         sig_b > 1e-12f);
+        st.dir = to_world(fr, smpl.wi);
+        st.T = v3(st.T.x * smpl.weight.x, st.T.y * smpl.weight.y, st.T.z * smpl.weight.z);
+        st.bounce++;
+        bool done = false;
+        if (st.bounce >= ps.max_bounces) {             // render.py:92-94
+          done = true;
+        } else if (st.bounce > 8) {                    // render.py:96-105
+          float q = kMono ? fminf(st.T.x, 1.0f) : fminf(fmaxf(st.T.x, fmaxf(st.T.y, st.T.z)), 1.0f);
+          if (st.u_rr >= q) {
+            done = true;
+          } else {
+            st.T = mul3(st.T, 1.0f / q);
+          }
+        }
+        if (done && !want_shadow) {
+          finish(pid, st.L);
+        } else {
+          uint32_t fl = (uint32_t)st.bounce;
+          if (!done) {
+            // the next segment's uniforms (flight_stage's block)
+            U4 b = philox_rk(U4{pix, smp, (uint32_t)st.bounce, 0u}, ps.rk);
+            P.f[F::kUbr][slot] = u01(b.y);
+            P.f[F::kUs2][slot] = u01(b.z);
+            P.f[F::kUrr][slot] = u01(b.w);
+            store3(F::kDir, slot, st.dir);
+            storec(F::kT, slot, st.T);
+          } else {
+            fl |= kGwDone;
+          }
+          if (want_shadow) {
+            storec(F::kNee, slot, nee);
+            fl |= kGwShadow;
+          } else {
+            cn.v[kStSegments]++;
+          }
+          P.u[3][slot] = fl | kGwFresh;
+          tag = kTagWalk;
+        }
+      }
+    }
+    __syncwarp();
+    {
+      unsigned m0 = __ballot_sync(full, slot >= 0 && tag == kTagEmpty);
+      unsigned m1 = __ballot_sync(full, slot >= 0 && tag == kTagBeck);
+      unsigned m2 = __ballot_sync(full, slot >= 0 && tag == kTagHemi);
+      unsigned m3 = __ballot_sync(full, slot >= 0 && tag == kTagWalk);
+      if (slot >= 0) {
+        unsigned mine = tag == kTagEmpty ? m0 : (tag == kTagBeck ? m1 : (tag == kTagHemi ? m2 : m3));
+        unsigned tl = tag == kTagEmpty ? tail[0]
+                                       : (tag == kTagBeck ? tail[1] : (tag == kTagHemi ? tail[2] : tail[3]));
+        P.ring[tag][(tl + (unsigned)__popc(mine & lt)) & (kRing - 1)] = (uint8_t)slot;
+      }
+      tail[0] += (unsigned)__popc(m0);
+      tail[1] += (unsigned)__popc(m1);
+      tail[2] += (unsigned)__popc(m2);
+      tail[3] += (unsigned)__popc(m3);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < kStCount; ++i) {
+    unsigned v = __reduce_add_sync(full, cn.v[i]);
+    if (lane == 0 && v) atomicAdd(ps.stats + i, (unsigned long long)v);
+  }
+}
+
 // fixed-point pixel sums -> the caller's fp32 image (render.py:165-166):
 // one thread per local pixel, sum * 2^-k / spp in double, added to (or
 // written into) accum[pixel][c]
@@ -1684,7 +2060,7 @@ int attach_slope_table(SceneDev* sc, cudaStream_t st) {
 
 struct Occupancy {
   int sms = 0;
-  int blocks[28] = {};
+  int blocks[32] = {};
 };
 
 template <bool kPoint, bool kMono, int kSpec>
@@ -1779,6 +2155,11 @@ int device_occupancy(Occupancy* occ) {
   MF_CUDA((occ_curved<3, true, kCurvedSpec>(&o.blocks[25])));
   MF_CUDA((occ_curved<2, false, kCurvedSpec>(&o.blocks[26])));
   MF_CUDA((occ_curved<2, true, kCurvedSpec>(&o.blocks[27])));
+  // grid path pool with pooled walks: blocks[28 + mono + 2 spec]
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[28], grid_pool_kernel<false, 0>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[29], grid_pool_kernel<true, 0>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[30], grid_pool_kernel<false, kCurvedSpec>, kBlock, 0));
+  MF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks[31], grid_pool_kernel<true, kCurvedSpec>, kBlock, 0));
   MF_CUDA((occ_pool<false, false, 2>(&o.blocks[16])));
   MF_CUDA((occ_pool<true, false, 2>(&o.blocks[17])));
   MF_CUDA((occ_pool<false, true, 2>(&o.blocks[18])));
@@ -1933,8 +2314,22 @@ int launch_paths(const SceneDev& sc_in, const PassDev& ps, bool caller_rays, cud
     if (caller_rays) path_kernel<2, true><<<grid, kBlock, 0, st>>>(sc, ps);
     else if (megakernel_requested()) path_kernel<2, false><<<grid, kBlock, 0, st>>>(sc, ps);
     else {
-      // the grid-field path pool (MF_MEGAKERNEL=1: the megakernel)
-      launch_curved_pool(2, sc, ps, occ, need, st);
+      // the grid-field path pools (MF_MEGAKERNEL=1: the megakernel): pooled
+      // walks unless a point light needs per-path shadow directions
+      // (MF_GRID_WALK_POOL=0: walks inside the visits, for the comparison test)
+      const char* gp = std::getenv("MF_GRID_WALK_POOL");
+      if (sc.has_point || ps.max_bounces > 0xFFFF || sc.grid.n_maj > 1024 || (gp && gp[0] == '0')) {
+        launch_curved_pool(2, sc, ps, occ, need, st);
+      } else {
+        int spec = sc.media[0].fresnel == kAlbedo ? 1 : 0;
+        int pk = 28 + (sc.mono ? 1 : 0) + 2 * spec;
+        int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ.sms * occ.blocks[pk], need));
+        using K = void (*)(SceneDev, PassDev);
+        static const K ks[4] = {grid_pool_kernel<false, 0>, grid_pool_kernel<true, 0>,
+                                grid_pool_kernel<false, kCurvedSpec>,
+                                grid_pool_kernel<true, kCurvedSpec>};
+        ks[pk - 28]<<<g2, kBlock, 0, st>>>(sc, ps);
+      }
     }
   }
   g_launches++;

@@ -3,6 +3,7 @@ unpinned by construction).  Self-consistency instead: a
 constant-sigma grid of a plane / sphere SDF must reproduce the analytic
 planar / sphere paths, and the majorant grid must never be exceeded."""
 
+import dataclasses
 import math
 
 import numpy as np
@@ -194,3 +195,26 @@ def test_grid_pool_matches_megakernel(cuda, monkeypatch):
     np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-7)
     sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
     assert sa == sb
+
+
+def test_grid_walk_pool_matches_curved_pool(cuda, monkeypatch):
+    """The grid pool with pooled walks (walks parked and resumed between W
+    visits, tentative collisions batched) against the pool that runs whole
+    walks inside its visits (MF_GRID_WALK_POOL=0): the same decisions
+    (identical event counts), the same image to float rounding; colour
+    scenes too; deterministic for any tile size."""
+    for colour in (False, True):
+        sc = configs.config5_scene(64, 48, n_sdf=96, n_sigma=48)
+        if colour:
+            sc = dataclasses.replace(sc, environment=mf.Environment(radiance=(0.2, 0.1, 0.05)))
+        a, sa = mf.render_device(sc, 16, 4, max_bounces=64, stats=True)
+        a = a.cpu().numpy()
+        a2, _ = mf.render_device(sc, 16, 4, max_bounces=64, tile=8)
+        assert np.array_equal(a, a2.cpu().numpy())
+        monkeypatch.setenv("MF_GRID_WALK_POOL", "0")
+        b, sb = mf.render_device(sc, 16, 4, max_bounces=64, stats=True)
+        monkeypatch.delenv("MF_GRID_WALK_POOL")
+        b = b.cpu().numpy()
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-7)
+        sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
+        assert sa == sb
