@@ -149,6 +149,11 @@ MF_HD float grid_extinction(const GridDev& g, const MediumK& base, V3 p, V3 dir,
 }
 
 constexpr int kGridIterCap = 1000000;
+// empty cells at Chebyshev distance >= this jump (a jump re-locates the
+// cell from the position, ~3 plain DDA steps of work)
+#ifndef MF_GRID_SKIP_MIN
+#define MF_GRID_SKIP_MIN 2
+#endif
 
 struct GridWalk {
   int outcome;   // kEscaped / kAbsorbed / kCollided (values of mf_transport.cuh)
@@ -308,14 +313,17 @@ struct GridWalker {
 
   // One loop iteration of the DDA.  Returns 1 when a tentative collision
   // lies in the current cell (t is advanced to it; call tentative()), 2 when
-  // the walk has ended (w is final), 0 otherwise.
+  // the walk has left the grid or reached t1 (t is the end parameter; the
+  // driver calls end_at(t) once), 0 otherwise.  Apart from the three exits
+  // (collision, end, empty-space jump) the step is branch-free, so the
+  // lanes of a warp that step together stay converged.
   MF_HDM int dda(const GridDev& g) {
     MF_GSTAT(0);
     int n = g.n_maj;
     float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
-    mu = ldg(g.maj + ((size_t)cx * n + cy) * n + cz);
+    mu = ldg(g.maj + (unsigned)((cx * n + cy) * n + cz));
+    float need = mu * (t_exit - t);
     if (mu > 0.0f) {
-      float need = mu * (t_exit - t);
       if (tau < need) {
         t += tau / mu;
         return 1;
@@ -323,41 +331,29 @@ struct GridWalker {
       tau -= need;
       MF_GSTAT(4);
     }
-    // leave the cell
-    if (t_exit >= t1) {
-      end_at(t1);
+    // leave the cell.  Empty space (mu = -D): jump (D - 1) cells in every
+    // axis, then restart the DDA from the cell at the landing point
+    float tj = t + (-mu - 1.0f) * dt_min;
+    bool skip = mu <= -(float)MF_GRID_SKIP_MIN && tj > t_exit;
+    float tn = skip ? tj : t_exit;
+    if (tn >= t1) {
+      t = t1;
       return 2;   // escaped the grid (or reached the light)
     }
-    if (mu <= -2.0f) {
-      // empty space: jump (D - 1) cells in every axis, then restart the DDA
-      float tj = t + (-mu - 1.0f) * dt_min;
-      if (tj >= t1) {
-        end_at(t1);
-        return 2;
-      }
-      if (tj > t_exit) {
-        MF_GSTAT(2);
-        t = tj;
-        locate(g);
-        return 0;
-      }
+    t = tn;
+    if (skip) {
+      MF_GSTAT(2);
+      locate(g);
+      return 0;
     }
-    t = t_exit;
-    if (tx <= ty && tx <= tz) {
-      cx += sx;
-      tx = fmaf((float)cx, wax, wbx);
-    } else if (ty <= tz) {
-      cy += sy;
-      ty = fmaf((float)cy, way, wby);
-    } else {
-      cz += sz;
-      tz = fmaf((float)cz, waz, wbz);
-    }
-    if ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n || (unsigned)cz >= (unsigned)n) {
-      end_at(t);
-      return 2;
-    }
-    return 0;
+    bool ax = tx <= ty && tx <= tz;
+    bool ay = !ax && ty <= tz;
+    cx += ax ? sx : 0;
+    cy += ay ? sy : 0;
+    cz += (ax || ay) ? 0 : sz;
+    walls();
+    return ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n ||
+            (unsigned)cz >= (unsigned)n) ? 2 : 0;
   }
 
   // The tentative collision at t (majorant mu): true when the walk ends.
@@ -418,7 +414,11 @@ MF_HD GridWalk grid_walk(const GridDev& g, const MediumK& base, RngBlock rng_blo
   if (!W.begin(g, call0, pos, dir, ratio, t_max, rr_min)) return W.w;
   while (true) {
     int r = W.dda(g);
-    if (r == 2 || (r == 1 && W.tentative(g, base))) break;
+    if (r == 2) {
+      W.end_at(W.t);
+      break;
+    }
+    if (r == 1 && W.tentative(g, base)) break;
   }
   return W.w;
 }

@@ -1402,6 +1402,12 @@ __global__ void __launch_bounds__(kBlock, kMode == 2 ? MF_GRID_POOL_MIN_BLOCKS
 #ifndef MF_GW_EXIT
 #define MF_GW_EXIT 4
 #endif
+// slots per warp of the grid pool
+#ifndef MF_GRID_POOL
+#define MF_GRID_POOL 96
+#endif
+constexpr int kGPool = MF_GRID_POOL;
+static_assert(kGPool % 32 == 0 && kGPool <= kRing, "grid pool size: whole warps of slots");
 constexpr int kStageWalk = 3;
 constexpr uint8_t kTagWalk = 3;
 constexpr uint32_t kGwShadow = 1u << 16, kGwDone = 1u << 17, kGwFresh = 1u << 18;
@@ -1415,8 +1421,8 @@ struct GridPoolF {
 };
 template <bool kMono>
 struct GridPoolSlots {
-  float f[GridPoolF<kMono>::kCount][kPool];
-  uint32_t u[6][kPool];   // pid pixel sample bounce|flags cell steps
+  float f[GridPoolF<kMono>::kCount][kGPool];
+  uint32_t u[6][kGPool];   // pid pixel sample bounce|flags cell steps
   uint8_t ring[4][kRing];
 };
 
@@ -1458,9 +1464,9 @@ __global__ void __launch_bounds__(kBlock, MF_GRID_WALK_POOL_MIN_BLOCKS) grid_poo
     }
   };
 #pragma unroll
-  for (int w = 0; w < kPoolWords; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
+  for (int w = 0; w < kGPool / 32; ++w) P.ring[kTagEmpty][w * 32 + lane] = (uint8_t)(w * 32 + lane);
   __syncwarp();
-  unsigned head[4] = {0, 0, 0, 0}, tail[4] = {kPool, 0, 0, 0};
+  unsigned head[4] = {0, 0, 0, 0}, tail[4] = {kGPool, 0, 0, 0};
   bool exhausted = false;
   while (true) {
     int ne = exhausted ? 0 : (int)(tail[0] - head[0]);
@@ -1519,7 +1525,10 @@ __global__ void __launch_bounds__(kBlock, MF_GRID_WALK_POOL_MIN_BLOCKS) grid_poo
       uint32_t pix = 0, smp = 0, seg = 0, bfl = 0;
       auto rb = [&](uint32_t call) { return philox_rk(U4{pix, smp, seg, call}, ps.rk); };
       GridWalker<decltype(rb)> W(rb);
-      bool active = false, ended = false, pending = false, shadow = false;
+      // lane state: 0 stepping (DDA), 1 a tentative collision pending, 2 the
+      // DDA ended the walk, 4 a tentative collision ended it, 3 no walk
+      int ls = 3;
+      bool shadow = false;
       if (slot >= 0) {
         bfl = P.u[3][slot];
         pix = P.u[1][slot];
@@ -1532,46 +1541,31 @@ __global__ void __launch_bounds__(kBlock, MF_GRID_WALK_POOL_MIN_BLOCKS) grid_poo
         seg = shadow ? bounce - 1u : bounce;
         uint32_t call0 = shadow ? kCallShadow : 1u;
         float rr = shadow ? kShadowRR : 0.0f;
-        active = true;
+        ls = 0;
         if (bfl & kGwFresh) {
-          if (!W.begin(sc.grid, call0, o, d, shadow, INFINITY, rr)) {
-            active = false;
-            ended = true;
-          }
+          if (!W.begin(sc.grid, call0, o, d, shadow, INFINITY, rr)) ls = 4;   // missed the grid
         } else {
           GridPark pk{P.f[F::kWt][slot], P.f[F::kWtau][slot], P.f[F::kWw][slot], P.u[4][slot],
                       (int)P.u[5][slot]};
           W.resume(sc.grid, call0, o, d, shadow, INFINITY, rr, pk);
         }
       }
-      const int n0 = __popc(__ballot_sync(full, active));
+      const int n0 = __popc(__ballot_sync(full, ls == 0));
       while (true) {
         // DDA phase: lanes without a pending tentative collision step on
         while (true) {
-          if (active && !pending) {
-            int r = W.dda(sc.grid);
-            if (r == 1) {
-              pending = true;
-            } else if (r == 2) {
-              active = false;
-              ended = true;
-            }
-          }
-          int nstep = __popc(__ballot_sync(full, active && !pending));
-          int npend = __popc(__ballot_sync(full, pending));
-          if (nstep * MF_GW_NUM <= npend * MF_GW_DEN) break;
+          if (ls == 0) ls = W.dda(sc.grid);
+          // stepping and pending lane counts by one warp reduction
+          unsigned cnt2 = __reduce_add_sync(full, ls == 0 ? 1u : (ls == 1 ? 0x100u : 0u));
+          if ((int)(cnt2 & 0xFFu) * MF_GW_NUM <= (int)(cnt2 >> 8) * MF_GW_DEN) break;
         }
         // tentative collisions of every pending lane
-        if (pending) {
-          if (W.tentative(sc.grid, sc.media[0])) {
-            active = false;
-            ended = true;
-          }
-          pending = false;
-        }
-        int nact = __popc(__ballot_sync(full, active));
+        if (ls == 1) ls = W.tentative(sc.grid, sc.media[0]) ? 4 : 0;
+        int nact = __popc(__ballot_sync(full, ls == 0));
         if (nact * 8 < n0 * MF_GW_EXIT || nact == 0) break;
       }
+      if (ls == 2) W.end_at(W.t);
+      const bool active = ls == 0, ended = ls == 2 || ls == 4;
       if (active) {
         // park the unfinished walk
         GridPark pk = W.park();
