@@ -229,6 +229,11 @@ struct GridWalker {
     }
   }
 
+  // walls of one axis (spacing h / |d|, the next one at tk) reached by tn
+  MF_HDM static int crossed(float tn, float tk, float d, float inv_h) {
+    return tn >= tk ? (int)((tn - tk) * (fabsf(d) * inv_h)) + 1 : 0;
+  }
+
   MF_HDM void walls() {
     tx = fmaf((float)cx, wax, wbx);
     ty = fmaf((float)cy, way, wby);
@@ -341,16 +346,13 @@ struct GridWalker {
       return 2;   // escaped the grid (or reached the light)
     }
     t = tn;
-    if (skip) {
-      MF_GSTAT(2);
-      locate(g);
-      return 0;
-    }
-    bool ax = tx <= ty && tx <= tz;
-    bool ay = !ax && ty <= tz;
-    cx += ax ? sx : 0;
-    cy += ay ? sy : 0;
-    cz += (ax || ay) ? 0 : sz;
+    if (skip) MF_GSTAT(2);
+    // cell walls crossed on each axis up to tn: one on the exit axis for a
+    // plain step (tn is that wall), up to D - 1 per axis for a jump -- one
+    // code path for both, so stepping and jumping lanes stay converged
+    cx += sx * crossed(tn, tx, dir.x, g.inv_h_maj.x);
+    cy += sy * crossed(tn, ty, dir.y, g.inv_h_maj.y);
+    cz += sz * crossed(tn, tz, dir.z, g.inv_h_maj.z);
     walls();
     return ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n ||
             (unsigned)cz >= (unsigned)n) ? 2 : 0;

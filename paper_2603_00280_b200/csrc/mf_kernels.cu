@@ -1551,17 +1551,19 @@ __global__ void __launch_bounds__(kBlock, MF_GRID_WALK_POOL_MIN_BLOCKS) grid_poo
         }
       }
       const int n0 = __popc(__ballot_sync(full, ls == 0));
+      int nact = n0;
       while (true) {
-        // DDA phase: lanes without a pending tentative collision step on
+        // DDA phase: lanes without a pending tentative collision step on,
+        // until kGwNum / (kGwNum + kGwDen) of the phase's lanes have one (or
+        // have ended)
+        const int stop = nact * MF_GW_DEN;
         while (true) {
           if (ls == 0) ls = W.dda(sc.grid);
-          // stepping and pending lane counts by one warp reduction
-          unsigned cnt2 = __reduce_add_sync(full, ls == 0 ? 1u : (ls == 1 ? 0x100u : 0u));
-          if ((int)(cnt2 & 0xFFu) * MF_GW_NUM <= (int)(cnt2 >> 8) * MF_GW_DEN) break;
+          if (__popc(__ballot_sync(full, ls == 0)) * (MF_GW_NUM + MF_GW_DEN) <= stop) break;
         }
         // tentative collisions of every pending lane
         if (ls == 1) ls = W.tentative(sc.grid, sc.media[0]) ? 4 : 0;
-        int nact = __popc(__ballot_sync(full, ls == 0));
+        nact = __popc(__ballot_sync(full, ls == 0));
         if (nact * 8 < n0 * MF_GW_EXIT || nact == 0) break;
       }
       if (ls == 2) W.end_at(W.t);
