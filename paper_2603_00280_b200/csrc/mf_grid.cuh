@@ -210,6 +210,122 @@ struct GridWalker {
   V3 pos, dir;
   float t, t1, tau, lo_mult, rr_min;
   float tx, ty, tz, wax, way, waz, wbx, wby, wbz, dt_min, mu;
+  int cx, cy, cz, sx, sy, sz;
+  bool ratio;
+  uint32_t call0;
+
+  MF_HDM GridWalker(RngBlock rb) : rng_block(rb) {}
+
+  // wall distance of cell c on one axis is c * wa + wb (INFINITY for a ray
+  // parallel to the walls)
+  MF_HDM static void wall_coef(int s, float bmin, float h, float o, float d, float* wa, float* wb) {
+    if (!(fabsf(d) > 1e-30f)) {
+      *wa = 0.0f;
+      *wb = INFINITY;
+    } else {
+      float id = 1.0f / d;
+      *wa = h * id;
+      *wb = (bmin + (s > 0 ? h : 0.0f) - o) * id;
+    }
+  }
+
+  // walls of one axis (spacing h / |d|, the next one at tk) reached by tn
+  MF_HDM static int crossed(float tn, float tk, float d, float inv_h) {
+    return tn >= tk ? (int)((tn - tk) * (fabsf(d) * inv_h)) + 1 : 0;
+  }
+
+  MF_HDM void walls() {
+    tx = fmaf((float)cx, wax, wbx);
+    ty = fmaf((float)cy, way, wby);
+    tz = fmaf((float)cz, waz, wbz);
+  }
+
+  MF_HDM void locate(const GridDev& g) {
+    V3 q = grid_coord(g, fma3(dir, t, pos), g.inv_h_maj);
+    int n = g.n_maj;
+    cx = clampi((int)q.x, 0, n - 1);
+    cy = clampi((int)q.y, 0, n - 1);
+    cz = clampi((int)q.z, 0, n - 1);
+    walls();
+  }
+
+  // the ray's constants; false: the ray misses the grid.  t0 = entry distance
+  MF_HDM bool setup(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                   float rr, float* t0) {
+    w.outcome = 0;
+    w.pos = p0;
+    w.weight = 1.0f;
+    w.steps = 0;
+    w.violations = 0;
+    pos = p0;
+    dir = d;
+    ratio = ratio_walk;
+    rr_min = rr;
+    lo_mult = ratio ? -3.0f : -6.0f;
+    call0 = call0_;
+    if (!grid_box(g, pos, dir, t0, &t1)) return false;
+    t1 = fminf(t1, t_max);
+    sx = dir.x > 0.0f ? 1 : -1;
+    sy = dir.y > 0.0f ? 1 : -1;
+    sz = dir.z > 0.0f ? 1 : -1;
+    wall_coef(sx, g.bmin.x, g.h_maj.x, pos.x, dir.x, &wax, &wbx);
+    wall_coef(sy, g.bmin.y, g.h_maj.y, pos.y, dir.y, &way, &wby);
+    wall_coef(sz, g.bmin.z, g.h_maj.z, pos.z, dir.z, &waz, &wbz);
+    // parametric length of one cell on the axis the ray crosses fastest
+    dt_min = fminf(fminf(wax != 0.0f ? fabsf(wax) : INFINITY, way != 0.0f ? fabsf(way) : INFINITY),
+                   waz != 0.0f ? fabsf(waz) : INFINITY);
+    return true;
+  }
+
+  // false: the ray misses the grid (escaped at once)
+  MF_HDM bool begin(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                   float rr) {
+    float t0;
+    if (!setup(g, call0_, p0, d, ratio_walk, t_max, rr, &t0)) return false;
+    t = t0;
+    locate(g);
+    // optical depth left to the next tentative collision: sampled once per
+    // tentative and used up cell by cell (tau -= mu dt), instead of a fresh
+    // exponential (a uniform and a log) in every cell the ray crosses -- the
+    // same process (the majorant is piecewise constant along the ray), a
+    // fraction of the random numbers and logs
+    tau = -flog(u01(rng_block(call0).x));
+    MF_GSTAT(3);
+    return true;
+  }
+
+  MF_HDM GridPark park() const {
+    return GridPark{t, tau, w.weight, (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20),
+                    w.steps};
+  }
+
+  // continue a parked walk of the same ray (same arguments as begin())
+  MF_HDM void resume(const GridDev& g, uint32_t call0_, V3 p0, V3 d, bool ratio_walk, float t_max,
+                    float rr, const GridPark& k) {
+    float t0;
+    setup(g, call0_, p0, d, ratio_walk, t_max, rr, &t0);
+    t = k.t;
+    tau = k.tau;
+    w.weight = k.weight;
+    w.steps = k.steps;
+    cx = (int)(k.cell & 1023u);
+    cy = (int)((k.cell >> 10) & 1023u);
+    cz = (int)(k.cell >> 20);
+    walls();
+  }
+
+  MF_HDM void end_at(float te) { w.pos = fma3(dir, te, pos); }
+
+  // One loop iteration of the DDA.  Returns 1 when a tentative collision
+  // lies in the current cell (t is advanced to it; call tentative()), 2 when
+  // the walk has left the grid or reached t1 (t is the end parameter; the
+  // driver calls end_at(t) once), 0 otherwise.  Apart from the three exits
+  // (collision, end, empty-space jump) the step is branch-free, so the
+  // lanes of a warp that step together stay converged.
+  MF_HDM int dda(const GridDev& g) {
+    MF_GSTAT(0);
+    int n = g.n_maj;
+    float t_exit = fminf(fminf(tx, ty), fminf(tz, t1));
     mu = ldg(g.maj + (unsigned)((cx * n + cy) * n + cz));
     float need = mu * (t_exit - t);
     bool med = mu > 0.0f;
@@ -217,7 +333,7 @@ struct GridWalker {
       t = fmaf(tau, frcp(mu), t);
       return 1;
     }
-    tau = med ? tau - need : tau;
+    tau = med ? tau - need : tau;   // a select: medium and empty cells stay converged
     // leave the cell.  Empty space (mu = -D): jump (D - 1) cells in every
     // axis, then restart the DDA from the cell at the landing point
     float tj = t + (-mu - 1.0f) * dt_min;
@@ -236,9 +352,8 @@ struct GridWalker {
     cy += sy * crossed(tn, ty, dir.y, g.inv_h_maj.y);
     cz += sz * crossed(tn, tz, dir.z, g.inv_h_maj.z);
     walls();
-    if ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n || (unsigned)cz >= (unsigned)n)
-      return 2;
-    return 0;
+    return ((unsigned)cx >= (unsigned)n || (unsigned)cy >= (unsigned)n ||
+            (unsigned)cz >= (unsigned)n) ? 2 : 0;
   }
 
   // The tentative collision at t (majorant mu): true when the walk ends.
