@@ -429,7 +429,7 @@ def run_render(args, torch, dist, n, rank, local, dev):
     kernel = {"config4": "pool_kernel (single-plane path pool, grey)",
               "config2": "pool_kernel (single-plane path pool, grey)",
               "config3": "curved_pool_kernel<3> (single-sphere path pool, grey)",
-              "config5": "curved_pool_kernel<2> (grid-field path pool, grey)"}[args.workload]
+              "config5": "grid_pool_kernel (grid-field path pool with pooled walks, grey)"}[args.workload]
     roof = {"bound": rl["bound"], "achieved": rl["achieved"], "peak": rl["peak"],
             "unit": rl["unit"], "frac": rl["frac"], "traffic": ncu_traffic(args.workload),
             "peak_source": "measured on this device by mf_measure_peaks (FFMA / MUFU.EX2 issue "

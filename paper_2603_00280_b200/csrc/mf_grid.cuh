@@ -333,6 +333,7 @@ struct GridWalker {
       t = fmaf(tau, frcp(mu), t);
       return 1;
     }
+    if (med) MF_GSTAT(4);
     tau = med ? tau - need : tau;   // a select: medium and empty cells stay converged
     // leave the cell.  Empty space (mu = -D): jump (D - 1) cells in every
     // axis, then restart the DDA from the cell at the landing point

@@ -34,7 +34,7 @@ echo "ncu c1 rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"curved_pool_kernel" -s 1 -c 1 \
     -o gpurun_out/c3_full -f python tools/ncu_render.py config3 512 256 > gpurun_out/ncu_c3.log 2>&1
 echo "ncu c3 rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"curved_pool_kernel" -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"grid_pool_kernel" -s 1 -c 1 \
     -o gpurun_out/c5_full -f python tools/ncu_render.py config5 512 64 > gpurun_out/ncu_c5.log 2>&1
 echo "ncu c5 rc=$?"
 fi
