@@ -58,7 +58,7 @@ def test_shadow_roulette_is_unbiased(host_math):
         d = np.array(tg) - ORIGIN
         d = (d / np.linalg.norm(d)).astype(np.float32).astype(np.float64)
         ex = exact_ratio_tr(ORIGIN, d)
-        for rr in (0.0, 0.05):
+        for rr in (0.0, 0.05, 1.0):
             w = run(host_math, d, n, rr)
             se = max(w.std() / np.sqrt(n), 1e-7)
             assert abs(w.mean() - ex) <= 4 * se + 1e-6, (tg, rr, w.mean(), ex, se)
