@@ -711,37 +711,74 @@ MF_HD float sphere_sigma_dir(const MediumK& m, float g) {
                         : proj_area_erf<kFast>(v3(sn, 0.0f, g), m.ax, m.ay, m.az);
 }
 
+// The walker as a resumable object: step() runs one iteration of the loop
+// (a vacuum skip, an edge move or a tentative collision) and returns true
+// when the walk has ended (w is final).  Between two steps the whole state
+// is (p, w.travel, w.weight, w.steps, the position in the random stream),
+// so a walk can be parked and resumed (park_rng() / resume()): the path
+// pool's W visits advance 32 walks together and park the unfinished ones.
 // kSpec (see proj_area): the medium's NDF kind known at compile time
 template <int kSpec = kSpecRuntime>
-MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segment,
-                                  uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
-                                  float rr_min = 0.0f) {
-  const PrimDev& pr = sc.prims[0];
-  const MediumK& m = sc.media[0];
-  const MediumExtra& mx = sc.mx[0];
-  const float s = m.sigma, is = m.inv_sigma;
-  const float lo = ratio ? -3.0f * s : -6.0f * s, hi = 3.0f * s;
-  const float l_lo = ratio ? mx.lphi_lo_rat : mx.lphi_lo_col, l_hi = mx.lphi_hi;
-  // the tight bound, x 1.0001 for the float rounding of f and g along radial
-  // chords.  Ratio walks use it too: a looser majorant keeps more weight per
-  // tentative collision, but measured on config 3 (128^2 x 256 spp, 16
-  // renders) the shadow estimator's variance is invisible in the image
-  // (per-pixel variance 8.46e-5 at scale 1.0001, 1.5 and 2) while each
-  // doubling of the scale doubles the iterations (5.4 / 9.4 / 12.5 per path,
-  // 2.72 / 3.63 / 4.26 ms); the stepping walker: 12.4, 3.52 ms, 1.06e-4
-  const float mscale = 1.0001f;
+struct SphereWalker {
+  const SceneDev& sc;
+  PathRng rng;
+  uint32_t segment;
+  V3 p, dir;
+  bool ratio;
+  float t_max, rr_min;
   WalkResult w;
-  w.outcome = kEscaped;
-  w.prim = -1;
-  w.weight = 1.0f;
-  w.steps = 0;
-  w.violations = 0;
-  w.travel = 0.0f;
-  V3 p = pos;
-  uint32_t call = call0;
-  U4 bits = U4{0, 0, 0, 0};
-  int avail = 0;
-  auto draw = [&]() {
+  uint32_t call;
+  U4 bits;
+  int avail;
+
+  MF_HDM SphereWalker(const SceneDev& scene) : sc(scene) {}
+
+  MF_HDM void begin(PathRng r, uint32_t seg, uint32_t call0, V3 pos, V3 d, bool ratio_walk,
+                   float tmax, float rr) {
+    rng = r;
+    segment = seg;
+    p = pos;
+    dir = d;
+    ratio = ratio_walk;
+    t_max = tmax;
+    rr_min = rr;
+    w.outcome = kEscaped;
+    w.prim = -1;
+    w.pos = pos;
+    w.weight = 1.0f;
+    w.steps = 0;
+    w.violations = 0;
+    w.travel = 0.0f;
+    call = call0;
+    bits = U4{0, 0, 0, 0};
+    avail = 0;
+  }
+
+  // the position in the random stream as one word (the calls of a walk are
+  // consecutive from call0; a walk draws far fewer than 2^29 blocks)
+  MF_HDM uint32_t park_rng(uint32_t call0) const { return ((call - call0) << 2) | (uint32_t)avail; }
+
+  // continue a parked walk: begin()'s arguments plus the parked state
+  MF_HDM void resume(PathRng r, uint32_t seg, uint32_t call0, V3 d, bool ratio_walk, float tmax,
+                    float rr, V3 p_now, float travel, float weight, int steps, uint32_t rs) {
+    begin(r, seg, call0, p_now, d, ratio_walk, tmax, rr);
+    w.travel = travel;
+    w.weight = weight;
+    w.steps = steps;
+    call = call0 + (rs >> 2);
+    avail = (int)(rs & 3u);
+    if (avail) {
+      // the unread words of the block drawn last
+      bits = rng_block(rng, segment, call - 1u);
+      for (int k = avail; k < 4; ++k) {
+        bits.x = bits.y;
+        bits.y = bits.z;
+        bits.z = bits.w;
+      }
+    }
+  }
+
+  MF_HDM float draw() {
     if (avail == 0) {
       bits = rng_block(rng, segment, call++);
       avail = 4;
@@ -752,31 +789,46 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
     bits.z = bits.w;
     --avail;
     return u;
-  };
-  for (int iter = 0; iter < 1000000; ++iter) {
+  }
+
+  MF_HDM bool end(int outcome, V3 at) {
+    w.outcome = outcome;
+    w.pos = at;
+    return true;
+  }
+
+  // one iteration; true when the walk has ended
+  MF_HDM bool step() {
+    const PrimDev& pr = sc.prims[0];
+    const MediumK& m = sc.media[0];
+    const MediumExtra& mx = sc.mx[0];
+    const float s = m.sigma, is = m.inv_sigma;
+    const float lo = ratio ? -3.0f * s : -6.0f * s, hi = 3.0f * s;
+    const float l_lo = ratio ? mx.lphi_lo_rat : mx.lphi_lo_col, l_hi = mx.lphi_hi;
+    // the tight bound, x 1.0001 for the float rounding of f and g along radial
+    // chords.  Ratio walks use it too: a looser majorant keeps more weight per
+    // tentative collision, but measured on config 3 (128^2 x 256 spp, 16
+    // renders) the shadow estimator's variance is invisible in the image
+    // (per-pixel variance 8.46e-5 at scale 1.0001, 1.5 and 2) while each
+    // doubling of the scale doubles the iterations (5.4 / 9.4 / 12.5 per path,
+    // 2.72 / 3.63 / 4.26 ms); the stepping walker: 12.4, 3.52 ms, 1.06e-4
+    const float mscale = 1.0001f;
     V3 oc = sub3(p, pr.c);
     float r2 = dot3(oc, oc);
     float ir = frsqrt(fmaxf(r2, 1e-30f));
     float f = r2 * ir - pr.radius;
     float g = fminf(fmaxf(dot3(oc, dir) * ir, -1.0f), 1.0f);
-    if (!ratio && f < lo) {              // below the depth cap (transport.py:199-205)
-      w.outcome = kAbsorbed;
-      w.pos = p;
-      return w;
-    }
+    if (!ratio && f < lo)                // below the depth cap (transport.py:199-205)
+      return end(kAbsorbed, p);
     if (f < lo || f > hi) {
       // vacuum: above the shell, or (ratio) the core; skip to the band
       float gd = level_distance<true>(pr, p, dir, f > hi ? hi : lo);
-      if (!(gd < INFINITY) || w.travel + gd >= t_max) {
-        w.outcome = kEscaped;
-        w.pos = p;
-        return w;
-      }
+      if (!(gd < INFINITY) || w.travel + gd >= t_max) return end(kEscaped, p);
       float ulp = 4.8e-7f * (1.0f + fmaxf(fabsf(p.x), fmaxf(fabsf(p.y), fabsf(p.z))));
       float skip = fmaxf(gd, sc.min_skip) + ulp;
       p = fma3(dir, skip, p);
       w.travel += skip;
-      continue;
+      return false;
     }
     // majorant of the chord from here: Sigma at its start times rho of the
     // tangent line (the 1.0001 absorbs float rounding of f, g along radial
@@ -793,9 +845,7 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
       if (g > 0.0f && !(l1 < l_hi)) {
         // the tangent leaves the band first; f grows from here on (past the
         // closest approach), so the ray leaves the shell for good
-        w.outcome = kEscaped;
-        w.pos = p;
-        return w;
+        return end(kEscaped, p);
       }
       if (g < 0.0f && !(l1 >= l_lo)) {
         // the tangent reaches the region's lower edge first: go there and
@@ -826,14 +876,13 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
       }
     }
     if (w.travel + t1 >= t_max) {         // reached the light (ratio walks)
-      w.outcome = kEscaped;
-      w.pos = fma3(dir, t_max - w.travel, p);
+      V3 at = fma3(dir, t_max - w.travel, p);
       w.travel = t_max;
-      return w;
+      return end(kEscaped, at);
     }
     p = fma3(dir, t1, p);
     w.travel += t1;
-    if (edge) continue;
+    if (edge) return false;
     // the true extinction at the tentative point
     V3 oc1 = sub3(p, pr.c);
     float r21 = dot3(oc1, oc1);
@@ -854,22 +903,33 @@ MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segm
         float ur = draw();
         w.weight = ur * rr_min < w.weight ? rr_min : 0.0f;
       }
-      if (!(w.weight > 0.0f)) {
-        w.outcome = kEscaped;
-        w.pos = p;
-        return w;
-      }
+      if (!(w.weight > 0.0f)) return end(kEscaped, p);
     } else if (draw() * mubar1 < mu) {
-      w.outcome = kCollided;
       w.prim = 0;
-      w.pos = p;
-      return w;
+      return end(kCollided, p);
     }
+    return false;
   }
-  w.outcome = kAbsorbed;   // iteration cap (counted by the caller)
-  w.pos = p;
-  w.steps = -1;
-  return w;
+
+  // iteration cap reached (counted by the caller)
+  MF_HDM void cap() {
+    w.outcome = kAbsorbed;
+    w.pos = p;
+    w.steps = -1;
+  }
+};
+
+template <int kSpec = kSpecRuntime>
+MF_WALK_FN WalkResult sphere_walk(const SceneDev& sc, PathRng rng, uint32_t segment,
+                                  uint32_t call0, V3 pos, V3 dir, bool ratio, float t_max,
+                                  float rr_min = 0.0f) {
+  SphereWalker<kSpec> W(sc);
+  W.begin(rng, segment, call0, pos, dir, ratio, t_max, rr_min);
+  for (int iter = 0; iter < 1000000; ++iter) {
+    if (W.step()) return W.w;
+  }
+  W.cap();
+  return W.w;
 }
 
 }  // namespace mf
