@@ -15,7 +15,9 @@
 //   pool_kernel       shared-memory path pool for single-plane scenes (configs
 //                     2, 4): R / B / H visits over per-warp slot rings, every
 //                     visit at full warp width
-//   curved_pool_kernel the same pool for one sphere or a grid field (configs 3, 5)
+//   curved_pool_kernel the same pool for one sphere (config 3; grid fields with two lights)
+//   grid_pool_kernel  the pool with pooled walks for a grid field (config 5): W visits
+//                     batch DDA steps and tentative collisions, walks park and resume
 //   ratio_kernel      ratio-tracking transmittance samples (transport.py:300-313)
 //   walk_kernel       walk / sample_collision of caller rays (transport.py:144-416)
 //   curve_kernel      closed-form curves of one medium (cli.py:132-175)
