@@ -218,3 +218,20 @@ def test_grid_walk_pool_matches_curved_pool(cuda, monkeypatch):
         np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-7)
         sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
         assert sa == sb
+
+
+@pytest.mark.parametrize("width,height,spp,depth", [(3, 2, 1, 64), (5, 4, 3, 1), (16, 8, 4, 2),
+                                                     (33, 17, 2, 9)])
+def test_grid_walk_pool_small_and_shallow(cuda, monkeypatch, width, height, spp, depth):
+    """Partial visits (fewer paths than a warp), paths that end at their
+    first collisions (depth cap with a shadow walk still queued) and the
+    first roulette bounce: same event counts and image as the curved pool."""
+    sc = configs.config5_scene(width, height, n_sdf=64, n_sigma=32)
+    a, sa = mf.render_device(sc, spp, 7, max_bounces=depth, stats=True)
+    monkeypatch.setenv("MF_GRID_WALK_POOL", "0")
+    b, sb = mf.render_device(sc, spp, 7, max_bounces=depth, stats=True)
+    monkeypatch.delenv("MF_GRID_WALK_POOL")
+    np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-4, atol=1e-7)
+    sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
+    assert sa == sb
+    assert sa["paths"] == width * height * spp
