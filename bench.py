@@ -310,7 +310,18 @@ def ncu_memory(workload):
             d = json.load(fh)
         return {"dram_GB_s": d.get("dram_GB_s"), "l2_GB_s": d.get("l2_GB_s"),
                 "l2_hit_pct": d.get("l2_hit_pct"), "capture": d.get("source"),
-                "units_per_launch": d.get("units_per_launch")}
+                "units_per_launch": d.get("units_per_launch"),
+                # what the kernel actually issued in that capture (ncu pipe
+                # counters), next to the algorithmic figure above
+                "ncu_issue": {"issue_active_pct": d.get("issue_active_pct"),
+                              "active_lanes": d.get("active_lanes"),
+                              "pipe_fma_pct": d.get("pipe_fma_pct"),
+                              "pipe_alu_pct": d.get("pipe_alu_pct"),
+                              "pipe_xu_pct": d.get("pipe_xu_pct"),
+                              "thread_instructions_per_unit":
+                                  d.get("thread_instructions_per_unit"),
+                              "fp32_share_of_instructions":
+                                  d.get("fp32_share_of_instructions")}}
     except Exception:
         return None
 
