@@ -235,3 +235,56 @@ def test_grid_walk_pool_small_and_shallow(cuda, monkeypatch, width, height, spp,
     sa.pop("path_kernel_ms"), sb.pop("path_kernel_ms")
     assert sa == sb
     assert sa["paths"] == width * height * spp
+
+
+def test_config5_transmittance_matches_oracle_quadrature(cuda):
+    """Config 5's own heterogeneous fields (128^3 union-of-spheres SDF, 64^3
+    value-noise sigma, l_xy 0.03 / l_z 0.08) on the device against
+    oracle/gridfield.py: the ratio-tracked transmittance (mf_transmittance:
+    trilinear fetches, gradient frames, region rules, the majorant grid and
+    its DDA) must equal exp(-int sigma_t ds) from plain float64 quadrature
+    of the reference's coefficient functions on the same fields."""
+    from paper_2603_00280_b200.grid import config5_fields
+    from test_grid_host import _mid_transmittance_rays
+
+    sdf, sigma = config5_fields(n_sdf=128, n_sigma=64)
+    bounds = ((-1.6,) * 3, (1.6,) * 3)
+    med = GridMedium(sigma=sigma, l_xy=0.03, l_z=0.08, albedo=0.85)
+    cam = mf.Camera(position=(0.0, -4.0, 1.2), look_at=(0.0, 0.0, 0.0), fov_deg=40.0, width=4,
+                    height=4)
+    sc = mf.ShellScene(primitives=(mf.ShellPrimitive(sdf, med),), camera=cam)
+    n = 400_000
+    worst = 0.0
+    for k, (o, d, tr) in enumerate(_mid_transmittance_rays(sdf.values, sigma, bounds, 8, 13)):
+        mean, se = mf.transmittance_estimate((o, d), sc, n, mf.RandomStream(21 + k, 1))
+        assert abs(mean - tr) <= 4 * se + 2e-3, (k, mean, tr, se)
+        worst = max(worst, abs(mean - tr) / max(se, 1e-12))
+    print(f"config-5 field transmittance: worst |device - quadrature| = {worst:.2f} SE over 8 rays")
+
+
+def test_config5_single_scatter_matches_oracle_quadrature(cuda):
+    """Depth-1 radiance on config 5's own heterogeneous fields: trace_paths
+    at max_bounces = 1 (the grid flight, the collision's local medium and
+    gradient frame, NEE with a tracked shadow ray, the environment on
+    escape) against oracle/gridfield.single_scatter_radiance -- nested
+    float64 quadrature of T sigma_t phase Tr_sun with the reference's
+    coefficient functions evaluated on the same trilinear fields."""
+    from oracle import gridfield as og
+    from test_grid_host import _mid_transmittance_rays
+
+    sc = configs.config5_scene(4, 4, n_sdf=128, n_sigma=64)
+    pr = sc.primitives[0]
+    sdf, sigma = pr.sdf.values, pr.medium.sigma
+    bounds = ((-1.6,) * 3, (1.6,) * 3)
+    sun_to = -np.asarray(sc.sun.direction, dtype=np.float64)
+    sun_to /= np.linalg.norm(sun_to)
+    n = 1 << 20
+    for k, (o, d, _) in enumerate(_mid_transmittance_rays(sdf, sigma, bounds, 3, 17)):
+        quad = og.single_scatter_radiance(sdf, sigma, bounds, 0.03, 0.08, 0.85, o, d, sun_to,
+                                          float(sc.sun.radiance[0]),
+                                          float(sc.environment.radiance[0]))
+        keys = mf.PathKeys(77 + k, np.arange(n, dtype=np.uint32), np.zeros(n, dtype=np.uint32))
+        rad = mf.trace_paths(np.broadcast_to(o, (n, 3)), np.broadcast_to(d, (n, 3)), sc, 1, keys)
+        mc, se = float(rad[:, 0].mean()), float(rad[:, 0].std() / math.sqrt(n))
+        print(f"ray {k}: device {mc:.5f} +- {se:.5f}, quadrature {quad:.5f}")
+        assert abs(mc - quad) <= 4 * se + 0.01 * quad, (k, mc, quad, se)

@@ -116,3 +116,53 @@ def test_majorant_empty_space_distances(host_math):
     for c in np.argwhere(m <= 0):
         d = int(np.min(np.max(np.abs(full - c), axis=1)))
         assert m[tuple(c)] == -min(d, 16), (c, m[tuple(c)], d)
+
+
+def _mid_transmittance_rays(sdf, sigma, bounds, count, seed):
+    """Rays from the config-5 camera position whose transmittance through
+    the field is neither ~0 nor ~1 (coarse oracle quadrature to choose them,
+    fine quadrature for the value)."""
+    from oracle import gridfield as og
+
+    rs = np.random.default_rng(seed)
+    o = np.array([0.0, -4.0, 1.2])
+    out = []
+    for _ in range(400):
+        tgt = rs.uniform(-0.9, 0.9, 3)
+        d = (tgt - o) / np.linalg.norm(tgt - o)
+        d = d.astype(np.float32).astype(np.float64)
+        d /= np.linalg.norm(d)
+        coarse = og.transmittance(sdf, sigma, bounds, 0.03, 0.08, o, d, step=2e-3)
+        if 0.08 < coarse < 0.92:
+            out.append((o, d, og.transmittance(sdf, sigma, bounds, 0.03, 0.08, o, d, step=4e-5)))
+            if len(out) == count:
+                break
+    assert len(out) == count
+    return out
+
+
+def test_config5_transmittance_matches_oracle_quadrature(host_math):
+    """The grid walker on config 5's own fields (union-of-spheres SDF, value
+    noise sigma, l_xy 0.03 / l_z 0.08) against oracle/gridfield.py: ratio
+    tracking through the majorant grid must reproduce exp(-int sigma_t ds)
+    computed by plain float64 quadrature of the reference's coefficient
+    functions on the same trilinear fields."""
+    sdf, sigma = config5_fields(n_sdf=64, n_sigma=32)
+    bounds = ((-1.6,) * 3, (1.6,) * 3)
+    cs, _ = grid_scene(sdf.values, sigma, 0.03, 0.08, 32, host_math)
+    n = 40000
+    for k, (o, d, tr) in enumerate(_mid_transmittance_rays(sdf.values, sigma, bounds, 5, 9)):
+        _, _, w, viol = run_walk(host_math, cs, o, d, n, ratio=True, seed=31 + k)
+        w = w.astype(np.float64)
+        se = w.std() / math.sqrt(n)
+        assert viol == 0
+        assert abs(w.mean() - tr) <= 4 * se + 2e-3, (k, w.mean(), tr, se)
+        # delta tracking (collision walks, region down to -6 sigma): the escape
+        # probability is the transmittance of that wider region
+        from oracle import gridfield as og
+        tr6 = og.transmittance(sdf.values, sigma, bounds, 0.03, 0.08, o, d, step=4e-5, lo_mult=-6.0)
+        st, _, _, viol = run_walk(host_math, cs, o, d, n, seed=51 + k)
+        p_esc = float(np.mean(st == 0))
+        se6 = math.sqrt(max(tr6 * (1 - tr6), 1e-6) / n)
+        assert viol == 0
+        assert abs(p_esc - tr6) <= 4 * se6 + 2e-3, (k, p_esc, tr6, se6)
