@@ -288,3 +288,25 @@ def test_config5_single_scatter_matches_oracle_quadrature(cuda):
         mc, se = float(rad[:, 0].mean()), float(rad[:, 0].std() / math.sqrt(n))
         print(f"ray {k}: device {mc:.5f} +- {se:.5f}, quadrature {quad:.5f}")
         assert abs(mc - quad) <= 4 * se + 0.01 * quad, (k, mc, quad, se)
+
+
+def test_config5_white_furnace(cuda):
+    """White furnace on config 5's heterogeneous fields (acceptance 11 of the
+    reference, test_scene_render.py, on a grid field): a lossless medium
+    (albedo 1) in a uniform environment of radiance 1 with no lights returns
+    radiance 1 along every ray whatever the geometry -- the product of the
+    sampling weights phase / pdf over all bounces, on local media that change
+    from collision to collision, must average to 1."""
+    base = configs.config5_scene(64, 48, n_sdf=128, n_sigma=64)
+    pr = base.primitives[0]
+    med = dataclasses.replace(pr.medium, albedo=1.0)
+    sc = dataclasses.replace(base, primitives=(dataclasses.replace(pr, medium=med),),
+                             environment=mf.Environment(radiance=(1.0, 1.0, 1.0)), sun=None)
+    img, st = mf.render_device(sc, 256, 11, max_bounces=512, stats=True)
+    v = img[..., 0].double().cpu().numpy()
+    assert st["majorant_violations"] == 0 and st["capped"] == 0
+    assert st["scatters"] > 0.5 * st["paths"]    # the furnace really scattered
+    se = v.std() / math.sqrt(v.size)
+    print(f"grid white furnace: mean {v.mean():.6f} +- {se:.6f}, pixel max |L - 1| "
+          f"{np.abs(v - 1).max():.4f}, absorbed {st['absorbed'] / st['paths']:.2e}")
+    assert abs(v.mean() - 1.0) <= 4 * se + 1e-3, (v.mean(), se)

@@ -100,7 +100,19 @@ def test_config4_media(cuda, sigma, lz):
     weight: ndf.py:318-406, medium.py:181-193) for every config-4 medium
     (alpha_xy 0.283 ... 5.657; Beckmann and generalized), same bar as
     config 1."""
-    med = configs.planar_medium(sigma, 0.05, lz, 0.8)
+    _check_medium_queries(cuda, configs.planar_medium(sigma, 0.05, lz, 0.8), sigma)
+
+
+@pytest.mark.parametrize("sigma", (0.01, 0.05, 0.2))
+def test_config5_local_media(cuda, sigma):
+    """The same bar for the local media of config 5's field: the value-noise
+    sigma grid spans 0.01 ... 0.2 and the kernel lengths are l_xy 0.03 /
+    l_z 0.08, i.e. GENERALIZED media with alpha_xy 0.47 ... 9.4 and alpha_z
+    0.18 ... 3.5 (grid_medium in csrc/mf_grid.cuh builds them per collision)."""
+    _check_medium_queries(cuda, configs.planar_medium(sigma, 0.03, 0.08, 0.85), sigma)
+
+
+def _check_medium_queries(cuda, med, sigma):
     m = parity.f32_medium(med)
     rs = np.random.default_rng(44)
     n = 1 << 16
