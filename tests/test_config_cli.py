@@ -45,6 +45,25 @@ def test_configs_match_the_baseline_scenes():
     assert abs(m.a3.ax - math.sqrt(2)) < 1e-12
 
 
+def test_config_box_and_env_map(tmp_path):
+    """Box shells and lat-long PFM environments (reference config.py:207-227)."""
+    import numpy as np
+
+    px = np.arange(4 * 8 * 3, dtype=np.float32).reshape(4, 8, 3)
+    mf.write_pfm(mf.RadianceImage(px), str(tmp_path / "env.pfm"))
+    text = ("[kernel]\nsigma = 0.05\nlx = 0.05\nly = 0.05\nlz = 0.1\n"
+            f"[scene]\nenv_map = {tmp_path / 'env.pfm'}\n"
+            "primitive0_shape = box\nprimitive0_center = 0,1,2\n"
+            "primitive0_half_extents = 1,2,0.5\n")
+    sc = scene_from_config(parse_config(text))
+    box = sc.primitives[0].sdf
+    assert isinstance(box, mf.Box)
+    assert box.center == (0.0, 1.0, 2.0) and box.half_extents == (1.0, 2.0, 0.5)
+    assert np.array_equal(sc.environment.latlong, px)
+    with pytest.raises(mf.IoError):
+        scene_from_config(parse_config(f"[scene]\nenv_map = {tmp_path / 'missing.pfm'}\n"))
+
+
 def test_cli_exit_codes(tmp_path, capsys):
     # cli.py:324-343 exit codes: config error 1, I/O error 3
     bad = tmp_path / "bad.cfg"
